@@ -1,0 +1,232 @@
+/*
+ * pfb200.h -- C ABI of the B200-native NLL engine (library: libpfb200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path: the per-event
+ * PDF evaluation + negative-log-likelihood reduction that the minimiser calls
+ * at every step (GooFit 2.0, re-derived as the Python package "parafit").
+ * The reference has no native FFI of its own; its plug points are Python
+ * protocols, and every entry point below replaces exactly one of them:
+ *
+ *   pfb_nll / pfb_nll_block_sums   <- engine.nll_block_sums + math.fsum
+ *                                     (/root/reference/pkg/src/parafit/engine.py:190-243)
+ *   pfb_nll_partial_async          <- sharding.partial_nll (sharding.py:94-114)
+ *   pfb_acc_round / pfb_finalize   <- sharding.reduce_partials / reduction.round_exact
+ *                                     (sharding.py:117-131, reduction.py:127-137)
+ *   pfb_terms_block_sums           <- reduction.block_sums + math.fsum (reduction.py:59-75)
+ *   pfb_exact_sum_host             <- reduction.ExactAccumulator.round (reduction.py:78-118)
+ *   pfb_shard_bounds               <- sharding.shard (sharding.py:68-91), bounds only
+ *   pfb_grid_*                     <- dalitz.integration_grid / compute_integrals
+ *                                     (dalitz.py:246-329)
+ *   pfb_plan_*                     <- the PdfNode tree + KIND_OPS dispatch (pdf.py:58-105,234-269)
+ *
+ * Conventions
+ *   - Every function returns a status code (0 = PFB_OK); codes map 1:1 onto the
+ *     reference exception classes (errors.py), see enum pfb_status.
+ *   - Host pointers are borrowed for the duration of the call. Device buffers are
+ *     owned by the handle that allocated them and freed by its *_destroy.
+ *   - One driver thread per context; calls on a context are not re-entrant.
+ *   - All arithmetic is IEEE binary64 on CUDA cores (never tensor cores, never FP32).
+ */
+#ifndef PFB200_H
+#define PFB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFB_ABI_VERSION 1
+
+/* Fixed reduction block: reference DEFAULT_BLOCK (reduction.py:25). */
+#define PFB_BLOCK 4096
+
+/* Exact second-stage accumulator: 68 signed 32-bit-digit limbs covering
+ * 2^-1074 .. 2^1102, then 4 special counters.  Summed (int64) across shards and
+ * GPUs with one allreduce; rounded once (round-half-even) = math.fsum. */
+#define PFB_NLIMBS 68
+#define PFB_ACC_POSINF 68
+#define PFB_ACC_NEGINF 69
+#define PFB_ACC_NAN 70
+#define PFB_ACC_FAILS 71 /* number of events that failed a density check */
+#define PFB_ACC_WORDS 72
+
+/* Status codes <-> reference exceptions (/root/reference/pkg/src/parafit/errors.py). */
+enum pfb_status {
+    PFB_OK = 0,
+    PFB_E_NONPOSITIVE_DENSITY = 1, /* NonPositiveDensity(index, value)   errors.py:89 */
+    PFB_E_NONFINITE_DENSITY = 2,   /* NonFiniteDensity(index)            errors.py:54 */
+    PFB_E_NEGATIVE_DENSITY = 3,    /* NegativeDensity(index, value)      errors.py:62 */
+    PFB_E_FRACTION_OUT_OF_RANGE = 4, /* FractionOutOfRange               errors.py:79 */
+    PFB_E_EMPTY_DATASET = 5,       /* EmptyDataSet                       errors.py:98 */
+    PFB_E_NONPOSITIVE_NORM = 6,    /* NonPositiveNorm                    errors.py:71 */
+    PFB_E_DEGENERATE_GRID = 7,     /* DegenerateGrid                     errors.py:111 */
+    PFB_E_INVALID_SUM = 8,         /* math.fsum ValueError (inf + -inf)  */
+    PFB_E_INVALID_ARGUMENT = 20,
+    PFB_E_UNSUPPORTED_PLAN = 21,
+    PFB_E_CUDA = 30,
+    PFB_E_NO_DEVICE = 31,
+    PFB_E_OUT_OF_MEMORY = 32
+};
+
+/* Node kinds: reference KIND_OPS keys (pdf.py:234-240, dalitz.py:413). */
+enum pfb_kind {
+    PFB_GAUSSIAN = 1,    /* exp(-0.5((x-mu)/sigma)^2)        pdf.py:122-127 */
+    PFB_EXPONENTIAL = 2, /* exp(alpha x)                     pdf.py:141-144 */
+    PFB_POLYNOMIAL = 3,  /* sum_k c_k x^k (Horner)           pdf.py:164-178 */
+    PFB_ADD = 4,         /* sum_k w_k child_k/norm_k          pdf.py:205-219 */
+    PFB_PROD = 5,        /* prod_k child_k/norm_k             pdf.py:222-227 */
+    PFB_DALITZ = 6       /* |sum_k c_k BW_k Z_k|^2            dalitz.py:181-230,380-384 */
+};
+
+/* One PDF-tree node, listed in post-order (PdfNode.walk, pdf.py:86-90): the
+ * children of a node are the `nchild` subtrees immediately preceding it. */
+typedef struct pfb_node {
+    int32_t kind;   /* enum pfb_kind */
+    int32_t nchild; /* add/prod: >= 2; primitives: 0 */
+    int32_t col0;   /* store column of the first observable (-1 if none) */
+    int32_t col1;   /* store column of the second observable (dalitz s13), else -1 */
+    int32_t nparam; /* raw parameter values this node consumes from `values` */
+    int32_t aux;    /* dalitz: index into the pfb_dalitz_desc array; else 0 */
+} pfb_node;
+
+/* Raw per-call parameter values, concatenated in node (post-)order:
+ *   gaussian [mu, sigma]; exponential [alpha]; polynomial [c0..c_{n-1}];
+ *   add [f0..f_{k-2}] (last weight implied, pdf.py:205-210); prod [];
+ *   dalitz, per term [mass, width, magnitude, phase] (dalitz.py:369-371).
+ * Norms: one value per node, same order (engine.resolve_norms, engine.py:162). */
+
+#define PFB_MAX_DALITZ_TERMS 16
+
+/* A DecayChannel (dalitz.py:47-77) plus the structural part of its terms
+ * (ResonanceTerm.pair / .spin, dalitz.py:86-106). */
+typedef struct pfb_dalitz_desc {
+    double mother_mass, m1, m2, m3;
+    int32_t nterms;
+    int32_t pair[PFB_MAX_DALITZ_TERMS]; /* 12, 13 or 23 */
+    int32_t spin[PFB_MAX_DALITZ_TERMS]; /* 0 or 1 */
+} pfb_dalitz_desc;
+
+/* Error record: the first failing check in the reference's evaluation order. */
+typedef struct pfb_err {
+    int32_t code;  /* enum pfb_status */
+    int32_t node;  /* post-order node index of the failing check (-1: root p>0 check) */
+    int64_t index; /* NonPositiveDensity: global (index_offset + local);
+                      NonFinite/Negative: chunk-local, as the reference reports */
+    double value;  /* offending value (NaN when the reference carries none) */
+} pfb_err;
+
+typedef struct pfb_ctx pfb_ctx;
+typedef struct pfb_store pfb_store;
+typedef struct pfb_plan pfb_plan;
+typedef struct pfb_grid pfb_grid;
+
+/* ---- library / context ---------------------------------------------------- */
+int pfb_version(void);
+const char* pfb_strerror(int code);
+int pfb_device_count(int* out);
+int pfb_ctx_create(int device, pfb_ctx** out);
+int pfb_ctx_destroy(pfb_ctx* ctx);
+/* Run all work of this context on an existing cudaStream_t (e.g. torch's current
+ * stream, so NCCL collectives order naturally); NULL restores the private stream. */
+int pfb_ctx_set_stream(pfb_ctx* ctx, void* cuda_stream);
+void* pfb_ctx_stream(pfb_ctx* ctx);
+/* Tuning: warps cooperating on one 4096-event block (0 = automatic; 1,2,4,8). */
+int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
+/* Number of engine kernels launched on this context since creation. */
+int pfb_ctx_launch_count(pfb_ctx* ctx, int64_t* out);
+/* Device time (ms) of the most recent NLL kernel, measured with CUDA events on
+ * the launching stream (only when timing is enabled). */
+int pfb_ctx_enable_timing(pfb_ctx* ctx, int on);
+int pfb_ctx_last_kernel_ms(pfb_ctx* ctx, float* out);
+
+/* ---- event store: device-resident SoA columns (core.UnbinnedDataSet, core.py:215-309) */
+int pfb_store_create(pfb_ctx* ctx, int32_t ncols, int64_t n_events, pfb_store** out);
+int pfb_store_upload(pfb_store* st, int32_t col, const double* host, int64_t offset, int64_t count);
+/* Borrow caller-owned device columns (must stay alive while the store is used). */
+int pfb_store_wrap(pfb_ctx* ctx, int32_t ncols, int64_t n_events, const double* const* dev_cols,
+                   pfb_store** out);
+int pfb_store_device_ptr(pfb_store* st, int32_t col, void** out);
+int pfb_store_destroy(pfb_store* st);
+
+/* ---- plan: flattened PDF tree ---------------------------------------------- */
+int pfb_plan_compile(pfb_ctx* ctx, const pfb_node* nodes, int32_t nnodes,
+                     const pfb_dalitz_desc* dalitz, int32_t ndalitz, pfb_plan** out);
+int pfb_plan_destroy(pfb_plan* plan);
+/* Which evaluator the plan uses: 0 literal interpreter, 1 sum-of-products
+ * log-domain, 2 Dalitz (recompute), 3 Dalitz (lineshape cache). */
+int pfb_plan_evaluator(const pfb_plan* plan, int32_t* out);
+/* Lineshape cache for Dalitz plans: 0 off (recompute per event), 1 on, 2 auto. */
+int pfb_plan_set_lineshape_cache(pfb_plan* plan, int32_t mode);
+/* Number of per-event amplitude rows recomputed by the lineshape cache so far. */
+int pfb_plan_cache_recomputes(const pfb_plan* plan, int64_t* out);
+
+/* ---- NLL ---------------------------------------------------------------------
+ * -sum_{i in [begin,end)} ln(eval(x_i)/norm_root), block sums by the reference
+ * half-folding tree per 4096-event block (relative to `begin`), combined exactly
+ * and rounded once.  Bitwise equal to engine.nll for any begin/end grouping that
+ * the reference would use.  `index_offset` is added to NonPositiveDensity
+ * indices (engine._nll_terms `offset`, engine.py:177-186). */
+int pfb_nll(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin, int64_t end,
+            int64_t index_offset, const double* values, int32_t nvalues, const double* norms,
+            int32_t nnorms, double* out_nll, pfb_err* out_err);
+/* Same evaluation, returning the per-block sums (engine.nll_block_sums). */
+int pfb_nll_block_sums(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin,
+                       int64_t end, int64_t index_offset, const double* values, int32_t nvalues,
+                       const double* norms, int32_t nnorms, double* out_block_sums,
+                       int64_t n_out, pfb_err* out_err);
+/* Enqueue (no host sync) the exact partial of [begin,end) into `dev_acc`
+ * (PFB_ACC_WORDS int64 on the device, overwritten).  Sum these across ranks with
+ * one allreduce, then pfb_finalize.  The local error record is kept in the
+ * context (pfb_last_error). */
+int pfb_nll_partial_async(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin,
+                          int64_t end, int64_t index_offset, const double* values,
+                          int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc);
+/* Round a (reduced) device accumulator; synchronises the context stream. */
+int pfb_finalize(pfb_ctx* ctx, const int64_t* dev_acc, double* out_nll, int64_t* out_fails);
+int pfb_last_error(pfb_ctx* ctx, pfb_err* out_err);
+/* End-to-end: host columns (pinned or pageable) streamed to the device in
+ * chunks on two copy/compute streams, evaluated, reduced.  Same result bits as
+ * pfb_nll over the uploaded store. */
+int pfb_nll_host(pfb_ctx* ctx, const pfb_plan* plan, const double* const* host_cols,
+                 int32_t ncols, int64_t n_events, const double* values, int32_t nvalues,
+                 const double* norms, int32_t nnorms, double* out_nll, pfb_err* out_err);
+
+/* ---- reduction kernels on given terms (known-answer tests) -------------------- */
+int pfb_terms_block_sums(pfb_ctx* ctx, const double* host_terms, int64_t n, double* out_block_sums,
+                         double* out_total);
+/* Host-side exact sum through the same limb code the device uses. */
+int pfb_exact_sum_host(const double* values, int64_t n, double* out);
+/* Round an accumulator held in host memory. */
+int pfb_acc_round(const int64_t* acc, double* out);
+/* Add values to a host accumulator (same digit split as the device). */
+int pfb_acc_add_host(int64_t* acc, const double* values, int64_t n);
+
+/* ---- sharding ------------------------------------------------------------------ */
+/* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */
+int pfb_shard_bounds(int64_t n, int32_t workers, int64_t block, int64_t* bounds);
+
+/* ---- Dalitz normalisation grid (dalitz.py:246-349) ----------------------------- */
+int pfb_grid_create(pfb_ctx* ctx, const pfb_dalitz_desc* channel, int32_t nx, int32_t ny,
+                    pfb_grid** out);
+int pfb_grid_info(const pfb_grid* g, int64_t* n_inside, double* cell_area);
+/* Row-major (s12 outer) in-boundary mask, nx*ny bytes. Bit-exact with the reference. */
+int pfb_grid_mask(const pfb_grid* g, uint8_t* host_mask);
+/* Overlap integrals I[i][j] = sum A_i conj(A_j) dA over the in-boundary nodes.
+ * The grid keeps one device amplitude row per term: rows flagged in `rows` are
+ * recomputed; matrix entries touching a term flagged in `stale` are recomputed,
+ * all other entries are left as found in `inout_matrix` (complex, row-major,
+ * interleaved re/im, K*K*2) -- the reference's prior reuse (dalitz.py:296-328).
+ * `mass_width` holds [mass_i, width_i] per term. */
+int pfb_grid_integrals(pfb_ctx* ctx, pfb_grid* g, int32_t nterms, const int32_t* pair,
+                       const int32_t* spin, const double* mass_width, const uint8_t* rows,
+                       const uint8_t* stale, double* inout_matrix);
+int pfb_grid_destroy(pfb_grid* g);
+
+/* ---- microbenchmarks used for the roofline denominators ------------------------ */
+int pfb_fp64_peak(pfb_ctx* ctx, double* out_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFB200_H */

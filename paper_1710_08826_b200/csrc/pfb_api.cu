@@ -1,0 +1,1409 @@
+// pfb_api.cu -- C ABI: contexts, device event stores, plan compilation,
+// per-call argument packing, error decoding and the Dalitz grid object.
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "pfb_internal.cuh"
+
+namespace pfb {
+cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
+cudaError_t launch_finalize(const long long* acc, double* result, unsigned long long* reset_acc,
+                            unsigned long long* errkey_reset, cudaStream_t stream);
+cudaError_t launch_probe(const NllArgs& A, int64_t j, double* out, cudaStream_t stream);
+cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
+cudaError_t launch_grid_mask(const GridConsts& g, uint8_t* mask, int* row_count, cudaStream_t st);
+cudaError_t launch_grid_compact(const GridConsts& g, const uint8_t* mask, const int* row_offset,
+                                double* p12, double* p13, cudaStream_t st);
+cudaError_t launch_grid_amp(const DalDesc& D, const DalTerm& T, const double* p12,
+                            const double* p13, int64_t n, double2* out, cudaStream_t st,
+                            int sm_count);
+cudaError_t launch_grid_overlap(const double2* amps, int64_t n, const int2* pairs, int npairs,
+                                unsigned long long* acc, cudaStream_t st, int sm_count);
+cudaError_t launch_lineshape_cache(const DalDesc& D, const DalTerm& T, const double* s12,
+                                   const double* s13, int64_t n, double2* row, cudaStream_t st,
+                                   int sm_count);
+}  // namespace pfb
+
+using namespace pfb;
+
+#define CK(call)                                  \
+    do {                                          \
+        cudaError_t e_ = (call);                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+static int cuda_fail(cudaError_t e) {
+    if (e == cudaErrorMemoryAllocation) return PFB_E_OUT_OF_MEMORY;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return PFB_E_NO_DEVICE;
+    fprintf(stderr, "pfb200: CUDA error %d: %s\n", (int)e, cudaGetErrorString(e));
+    return PFB_E_CUDA;
+}
+
+static constexpr int kStoreMaxCols = 16;
+static constexpr int kResultWords = 8;
+
+struct pfb_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    int warps_override = 0;
+    unsigned long long* acc = nullptr;
+    unsigned int* ticket = nullptr;
+    unsigned long long* errkey = nullptr;
+    double* tail_scratch = nullptr;
+    double* result_dev = nullptr;   // kResultWords
+    double* result_host = nullptr;  // pinned
+    double* bsums = nullptr;
+    int64_t bsums_cap = 0;
+    double* probe_dev = nullptr;
+    int64_t launches = 0;
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float last_ms = 0.f;
+    // last partial launch, for error decoding
+    std::unique_ptr<NllArgs> last_args;
+    const pfb_plan* last_plan = nullptr;
+    int64_t last_index_offset = 0;
+    int last_frac_rank = -1;
+    // end-to-end staging
+    double* e2e_dev[kMaxCols] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t e2e_cap = 0;
+    std::vector<cudaEvent_t> chunk_events;
+};
+
+struct pfb_store {
+    pfb_ctx* ctx = nullptr;
+    int32_t ncols = 0;
+    int64_t n = 0;
+    double* cols[kStoreMaxCols] = {};
+    bool owned = false;
+};
+
+struct TermFactor {
+    int type;  // 0: weight (node, child index), 1: 1/norm(node)
+    int node;
+    int child;
+};
+struct TermStruct {
+    uint32_t emask = 0, vmask = 0;
+    std::vector<TermFactor> factors;
+};
+
+struct pfb_plan {
+    pfb_ctx* ctx = nullptr;
+    std::vector<pfb_node> nodes;
+    std::vector<pfb_dalitz_desc> dal;
+    std::vector<std::vector<int>> children;
+    std::vector<int> raw_off;       // offset of each node's raw values
+    std::vector<int> der_off;       // offset of each node's derived (literal) values
+    std::vector<int> rank;          // first check rank per node (-1 none)
+    std::vector<int> frac_rank;     // add-node fraction check rank (-1)
+    int nraw = 0, nder = 0;
+    int final_rank = 0;
+    int nslots = 0;
+    int slot_col[kMaxCols] = {0, 0, 0, 0};
+    std::vector<int> node_slot0, node_slot1;
+    int evaluator = EV_LITERAL;
+    int dal_node = -1;
+    // sum of products
+    std::vector<int> leaf_nodes;
+    std::vector<TermStruct> terms;
+    // lineshape cache
+    int lineshape_mode = 0;
+    double2* cache = nullptr;
+    int64_t cache_cap = 0;
+    const pfb_store* cache_store = nullptr;
+    int64_t cache_begin = -1, cache_end = -1;
+    bool cache_valid[kMaxDal] = {};
+    double cache_mw[kMaxDal][2] = {};
+    int64_t cache_recomputes = 0;
+};
+
+struct pfb_grid {
+    pfb_ctx* ctx = nullptr;
+    pfb_dalitz_desc desc{};
+    GridConsts g{};
+    int64_t n_inside = 0;
+    double area = 0.0;
+    uint8_t* mask = nullptr;
+    double* p12 = nullptr;
+    double* p13 = nullptr;
+    double2* amps = nullptr;
+    int amps_rows = 0;
+};
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int pfb_version(void) { return PFB_ABI_VERSION; }
+
+const char* pfb_strerror(int code) {
+    switch (code) {
+        case PFB_OK: return "ok";
+        case PFB_E_NONPOSITIVE_DENSITY: return "non-positive density";
+        case PFB_E_NONFINITE_DENSITY: return "non-finite density";
+        case PFB_E_NEGATIVE_DENSITY: return "negative density";
+        case PFB_E_FRACTION_OUT_OF_RANGE: return "fraction out of range";
+        case PFB_E_EMPTY_DATASET: return "empty dataset";
+        case PFB_E_NONPOSITIVE_NORM: return "non-positive normalisation";
+        case PFB_E_DEGENERATE_GRID: return "degenerate grid";
+        case PFB_E_INVALID_SUM: return "-inf + inf in exact sum";
+        case PFB_E_INVALID_ARGUMENT: return "invalid argument";
+        case PFB_E_UNSUPPORTED_PLAN: return "unsupported plan";
+        case PFB_E_CUDA: return "CUDA error";
+        case PFB_E_NO_DEVICE: return "no CUDA device";
+        case PFB_E_OUT_OF_MEMORY: return "out of device memory";
+        default: return "unknown status";
+    }
+}
+
+int pfb_device_count(int* out) {
+    if (!out) return PFB_E_INVALID_ARGUMENT;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return PFB_OK;
+    }
+    *out = n;
+    return PFB_OK;
+}
+
+int pfb_ctx_create(int device, pfb_ctx** out) {
+    if (!out) return PFB_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        return PFB_E_NO_DEVICE;
+    }
+    if (device < 0 || device >= n) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(device));
+    auto* c = new pfb_ctx();
+    c->device = device;
+    CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CK(cudaMalloc(&c->acc, sizeof(unsigned long long) * PFB_ACC_WORDS));
+    CK(cudaMemset(c->acc, 0, sizeof(unsigned long long) * PFB_ACC_WORDS));
+    CK(cudaMalloc(&c->ticket, sizeof(unsigned int)));
+    CK(cudaMemset(c->ticket, 0, sizeof(unsigned int)));
+    CK(cudaMalloc(&c->errkey, sizeof(unsigned long long)));
+    CK(cudaMemset(c->errkey, 0xff, sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->tail_scratch, sizeof(double) * kBlock));
+    CK(cudaMalloc(&c->result_dev, sizeof(double) * kResultWords));
+    CK(cudaMalloc(&c->probe_dev, sizeof(double) * 2));
+    CK(cudaMallocHost(&c->result_host, sizeof(double) * kResultWords));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    *out = c;
+    return PFB_OK;
+}
+
+int pfb_ctx_destroy(pfb_ctx* c) {
+    if (!c) return PFB_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->acc);
+    cudaFree(c->ticket);
+    cudaFree(c->errkey);
+    cudaFree(c->tail_scratch);
+    cudaFree(c->result_dev);
+    cudaFree(c->probe_dev);
+    cudaFree(c->bsums);
+    for (auto& p : c->e2e_dev) cudaFree(p);
+    for (auto& e : c->chunk_events) cudaEventDestroy(e);
+    cudaFreeHost(c->result_host);
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    cudaStreamDestroy(c->own_stream);
+    cudaStreamDestroy(c->copy_stream);
+    delete c;
+    return PFB_OK;
+}
+
+int pfb_ctx_set_stream(pfb_ctx* c, void* s) {
+    if (!c) return PFB_E_INVALID_ARGUMENT;
+    c->stream = s ? (cudaStream_t)s : c->own_stream;
+    return PFB_OK;
+}
+
+void* pfb_ctx_stream(pfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
+    if (!c || !(w == 0 || w == 1 || w == 2 || w == 4 || w == 8)) return PFB_E_INVALID_ARGUMENT;
+    c->warps_override = w;
+    return PFB_OK;
+}
+
+int pfb_ctx_launch_count(pfb_ctx* c, int64_t* out) {
+    if (!c || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = c->launches;
+    return PFB_OK;
+}
+
+int pfb_ctx_enable_timing(pfb_ctx* c, int on) {
+    if (!c) return PFB_E_INVALID_ARGUMENT;
+    c->timing = on != 0;
+    return PFB_OK;
+}
+
+int pfb_ctx_last_kernel_ms(pfb_ctx* c, float* out) {
+    if (!c || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = c->last_ms;
+    return PFB_OK;
+}
+
+// ---- stores ------------------------------------------------------------------
+
+int pfb_store_create(pfb_ctx* c, int32_t ncols, int64_t n, pfb_store** out) {
+    if (!c || !out || ncols < 1 || ncols > kStoreMaxCols || n < 0) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto* s = new pfb_store();
+    s->ctx = c;
+    s->ncols = ncols;
+    s->n = n;
+    s->owned = true;
+    // pad each column to a whole number of 4096-event blocks (+2 for double2 reads)
+    const int64_t padded = ((n + kBlock - 1) / kBlock) * kBlock + 2;
+    for (int i = 0; i < ncols; ++i) {
+        cudaError_t e = cudaMalloc(&s->cols[i], sizeof(double) * padded);
+        if (e != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaFree(s->cols[j]);
+            delete s;
+            return cuda_fail(e);
+        }
+    }
+    *out = s;
+    return PFB_OK;
+}
+
+int pfb_store_upload(pfb_store* s, int32_t col, const double* host, int64_t offset, int64_t count) {
+    if (!s || !host || col < 0 || col >= s->ncols || offset < 0 || count < 0 ||
+        offset + count > s->n)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(s->ctx->device));
+    CK(cudaMemcpyAsync(s->cols[col] + offset, host, sizeof(double) * count, cudaMemcpyHostToDevice,
+                       s->ctx->stream));
+    CK(cudaStreamSynchronize(s->ctx->stream));
+    return PFB_OK;
+}
+
+int pfb_store_wrap(pfb_ctx* c, int32_t ncols, int64_t n, const double* const* dev_cols,
+                   pfb_store** out) {
+    if (!c || !out || !dev_cols || ncols < 1 || ncols > kStoreMaxCols || n < 0)
+        return PFB_E_INVALID_ARGUMENT;
+    auto* s = new pfb_store();
+    s->ctx = c;
+    s->ncols = ncols;
+    s->n = n;
+    s->owned = false;
+    for (int i = 0; i < ncols; ++i) s->cols[i] = const_cast<double*>(dev_cols[i]);
+    *out = s;
+    return PFB_OK;
+}
+
+int pfb_store_device_ptr(pfb_store* s, int32_t col, void** out) {
+    if (!s || !out || col < 0 || col >= s->ncols) return PFB_E_INVALID_ARGUMENT;
+    *out = s->cols[col];
+    return PFB_OK;
+}
+
+int pfb_store_destroy(pfb_store* s) {
+    if (!s) return PFB_OK;
+    if (s->owned) {
+        cudaSetDevice(s->ctx->device);
+        for (int i = 0; i < s->ncols; ++i) cudaFree(s->cols[i]);
+    }
+    delete s;
+    return PFB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// plan compilation
+
+static int expected_nparam(const pfb_node& n, const std::vector<pfb_dalitz_desc>& dal) {
+    switch (n.kind) {
+        case PFB_GAUSSIAN: return 2;
+        case PFB_EXPONENTIAL: return 1;
+        case PFB_POLYNOMIAL: return n.nparam >= 1 ? n.nparam : -1;
+        case PFB_ADD: return n.nchild - 1;
+        case PFB_PROD: return 0;
+        case PFB_DALITZ:
+            if (n.aux < 0 || n.aux >= (int)dal.size()) return -1;
+            return 4 * dal[n.aux].nterms;
+        default: return -1;
+    }
+}
+
+static int der_size(const pfb_node& n) {
+    switch (n.kind) {
+        case PFB_GAUSSIAN: return 2;
+        case PFB_EXPONENTIAL: return 1;
+        case PFB_POLYNOMIAL: return n.nparam;
+        case PFB_ADD: return n.nchild;
+        default: return 0;
+    }
+}
+
+static void assign_ranks(pfb_plan* p, int node, int* r) {
+    const pfb_node& n = p->nodes[node];
+    switch (n.kind) {
+        case PFB_ADD:
+            p->frac_rank[node] = (*r)++;
+            for (int c : p->children[node]) assign_ranks(p, c, r);
+            break;
+        case PFB_PROD:
+            for (int c : p->children[node]) assign_ranks(p, c, r);
+            break;
+        case PFB_GAUSSIAN:
+        case PFB_EXPONENTIAL:
+            p->rank[node] = (*r)++;
+            break;
+        case PFB_POLYNOMIAL:
+            p->rank[node] = *r;
+            *r += 2;
+            break;
+        default:
+            break;
+    }
+}
+
+// Expand a subtree into sum-of-products terms over its leaves (unnormalised
+// density of the subtree).
+static bool expand(const pfb_plan* p, int node, std::vector<TermStruct>* out) {
+    const pfb_node& n = p->nodes[node];
+    out->clear();
+    if (n.kind == PFB_GAUSSIAN || n.kind == PFB_EXPONENTIAL || n.kind == PFB_POLYNOMIAL) {
+        int li = -1;
+        for (size_t i = 0; i < p->leaf_nodes.size(); ++i)
+            if (p->leaf_nodes[i] == node) li = (int)i;
+        if (li < 0) return false;
+        TermStruct t;
+        if (n.kind == PFB_POLYNOMIAL)
+            t.vmask = 1u << li;
+        else
+            t.emask = 1u << li;
+        out->push_back(t);
+        return true;
+    }
+    if (n.kind == PFB_ADD) {
+        const auto& ch = p->children[node];
+        for (size_t k = 0; k < ch.size(); ++k) {
+            std::vector<TermStruct> sub;
+            if (!expand(p, ch[k], &sub)) return false;
+            for (auto& t : sub) {
+                t.factors.push_back({0, node, (int)k});
+                t.factors.push_back({1, ch[k], 0});
+                out->push_back(t);
+            }
+            if (out->size() > (size_t)kMaxTerms) return false;
+        }
+        return true;
+    }
+    if (n.kind == PFB_PROD) {
+        std::vector<TermStruct> cur(1);
+        for (int c : p->children[node]) {
+            std::vector<TermStruct> sub, next;
+            if (!expand(p, c, &sub)) return false;
+            for (auto& a : cur)
+                for (auto& b : sub) {
+                    TermStruct t = a;
+                    t.emask |= b.emask;
+                    t.vmask |= b.vmask;
+                    t.factors.insert(t.factors.end(), b.factors.begin(), b.factors.end());
+                    t.factors.push_back({1, c, 0});
+                    next.push_back(t);
+                }
+            if (next.size() > (size_t)kMaxTerms) return false;
+            cur.swap(next);
+        }
+        *out = cur;
+        return true;
+    }
+    return false;
+}
+
+extern "C" {
+
+int pfb_plan_compile(pfb_ctx* c, const pfb_node* nodes, int32_t nnodes,
+                     const pfb_dalitz_desc* dalitz, int32_t ndalitz, pfb_plan** out) {
+    if (!c || !nodes || !out || nnodes < 1 || ndalitz < 0 || (ndalitz > 0 && !dalitz))
+        return PFB_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (nnodes > kMaxNodes) return PFB_E_UNSUPPORTED_PLAN;
+    auto p = std::make_unique<pfb_plan>();
+    p->ctx = c;
+    p->nodes.assign(nodes, nodes + nnodes);
+    p->dal.assign(dalitz, dalitz + ndalitz);
+    for (const auto& d : p->dal)
+        if (d.nterms < 1 || d.nterms > kMaxDal) return PFB_E_UNSUPPORTED_PLAN;
+    p->children.resize(nnodes);
+    p->raw_off.resize(nnodes);
+    p->der_off.resize(nnodes);
+    p->rank.assign(nnodes, -1);
+    p->frac_rank.assign(nnodes, -1);
+    p->node_slot0.assign(nnodes, -1);
+    p->node_slot1.assign(nnodes, -1);
+    std::vector<int> stack;
+    int ndal_nodes = 0;
+    for (int i = 0; i < nnodes; ++i) {
+        const pfb_node& n = p->nodes[i];
+        const int np = expected_nparam(n, p->dal);
+        if (np < 0 || np != n.nparam) return PFB_E_INVALID_ARGUMENT;
+        const bool combo = n.kind == PFB_ADD || n.kind == PFB_PROD;
+        if (combo != (n.nchild >= 2)) return PFB_E_INVALID_ARGUMENT;
+        if (!combo && n.nchild != 0) return PFB_E_INVALID_ARGUMENT;
+        if ((int)stack.size() < n.nchild) return PFB_E_INVALID_ARGUMENT;
+        p->children[i].assign(stack.end() - n.nchild, stack.end());
+        stack.resize(stack.size() - n.nchild);
+        stack.push_back(i);
+        p->raw_off[i] = p->nraw;
+        p->nraw += n.nparam;
+        p->der_off[i] = p->nder;
+        p->nder += der_size(n);
+        if (n.kind == PFB_DALITZ) {
+            ++ndal_nodes;
+            p->dal_node = i;
+        }
+        // observable column slots
+        auto slot_of = [&](int col) -> int {
+            if (col < 0 || col >= kStoreMaxCols) return -2;
+            for (int s = 0; s < p->nslots; ++s)
+                if (p->slot_col[s] == col) return s;
+            if (p->nslots >= kMaxCols) return -3;
+            p->slot_col[p->nslots] = col;
+            return p->nslots++;
+        };
+        if (!combo) {
+            const int s0 = slot_of(n.col0);
+            if (s0 == -2) return PFB_E_INVALID_ARGUMENT;
+            if (s0 == -3) return PFB_E_UNSUPPORTED_PLAN;
+            p->node_slot0[i] = s0;
+            if (n.kind == PFB_DALITZ) {
+                const int s1 = slot_of(n.col1);
+                if (s1 == -2) return PFB_E_INVALID_ARGUMENT;
+                if (s1 == -3) return PFB_E_UNSUPPORTED_PLAN;
+                p->node_slot1[i] = s1;
+            }
+        }
+    }
+    if (stack.size() != 1 || stack[0] != nnodes - 1) return PFB_E_INVALID_ARGUMENT;
+    if (p->nder > kMaxVals) return PFB_E_UNSUPPORTED_PLAN;
+    if (ndal_nodes > 1) return PFB_E_UNSUPPORTED_PLAN;
+    int r = 0;
+    assign_ranks(p.get(), nnodes - 1, &r);
+    p->final_rank = r;
+
+    // evaluator choice
+    if (nnodes == 1 && p->nodes[0].kind == PFB_DALITZ) {
+        p->evaluator = EV_DALITZ;
+        // fast path reads s12 from slot 0 and s13 from slot 1
+        if (!(p->node_slot0[0] == 0 && p->node_slot1[0] == 1)) p->evaluator = EV_LITERAL;
+    } else if (ndal_nodes == 0) {
+        for (int i = 0; i < nnodes; ++i) {
+            const int k = p->nodes[i].kind;
+            if (k == PFB_GAUSSIAN || k == PFB_EXPONENTIAL || k == PFB_POLYNOMIAL)
+                p->leaf_nodes.push_back(i);
+        }
+        std::vector<TermStruct> terms;
+        if ((int)p->leaf_nodes.size() <= kMaxLeaves && expand(p.get(), nnodes - 1, &terms) &&
+            (int)terms.size() <= kMaxTerms && !terms.empty()) {
+            for (auto& t : terms) t.factors.push_back({1, nnodes - 1, 0});
+            p->terms = terms;
+            p->evaluator = EV_SOP;
+        } else {
+            p->evaluator = EV_LITERAL;
+        }
+    } else {
+        p->evaluator = EV_LITERAL;
+    }
+    *out = p.release();
+    return PFB_OK;
+}
+
+int pfb_plan_destroy(pfb_plan* p) {
+    if (!p) return PFB_OK;
+    if (p->cache) {
+        cudaSetDevice(p->ctx->device);
+        cudaFree(p->cache);
+    }
+    delete p;
+    return PFB_OK;
+}
+
+int pfb_plan_evaluator(const pfb_plan* p, int32_t* out) {
+    if (!p || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = (p->evaluator == EV_DALITZ && p->lineshape_mode == 1) ? EV_DALITZ_CACHED : p->evaluator;
+    return PFB_OK;
+}
+
+int pfb_plan_set_lineshape_cache(pfb_plan* p, int32_t mode) {
+    if (!p || mode < 0 || mode > 2) return PFB_E_INVALID_ARGUMENT;
+    p->lineshape_mode = mode;
+    return PFB_OK;
+}
+
+int pfb_plan_cache_recomputes(const pfb_plan* p, int64_t* out) {
+    if (!p || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = p->cache_recomputes;
+    return PFB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// per-call packing
+
+// numpy's float64 add.reduce for a contiguous array (pairwise_sum in
+// numpy/_core/src/umath/loops_utils.h): sequential below 8 elements, eight
+// interleaved accumulators up to 128, recursive halving (multiple of 8) above.
+static double numpy_sum(const double* a, int n) {
+    if (n < 8) {
+        double r = n ? a[0] : 0.0;
+        for (int i = 1; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int k = 0; k < 8; ++k) r[k] = a[k];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return numpy_sum(a, n2) + numpy_sum(a + n2, n - n2);
+}
+
+static void build_dal(const pfb_plan* p, const double* values, NllArgs* A) {
+    DalDesc& D = A->dal;
+    memset(&D, 0, sizeof(D));
+    if (p->dal_node < 0) return;
+    const pfb_node& n = p->nodes[p->dal_node];
+    const pfb_dalitz_desc& d = p->dal[n.aux];
+    const double* raw = values + p->raw_off[p->dal_node];
+    const double M = d.mother_mass;
+    const double M2 = M * M, m1sq = d.m1 * d.m1, m2sq = d.m2 * d.m2, m3sq = d.m3 * d.m3;
+    D.K = d.nterms;
+    D.mss = ((M2 + m1sq) + m2sq) + m3sq;
+    D.zc12 = (M2 - m3sq) * (m2sq - m1sq);
+    D.zc13 = (M2 - m2sq) * (m3sq - m1sq);
+    D.zc23 = (M2 - m1sq) * (m3sq - m2sq);
+    for (int k = 0; k < d.nterms; ++k) {
+        DalTerm& T = D.t[k];
+        const double m = raw[4 * k], w = raw[4 * k + 1], mag = raw[4 * k + 2], ph = raw[4 * k + 3];
+        T.pair = d.pair[k];
+        T.spin = d.spin[k];
+        T.m2 = m * m;
+        T.mg = m * w;
+        T.mg2 = T.mg * T.mg;
+        T.cre = mag * cos(ph);
+        T.cim = mag * sin(ph);
+        T.cached = 0;
+        if (T.spin == 1) {
+            if (T.pair == 12 && D.zc12 != 0.0) D.need12 = 1;
+            if (T.pair == 13 && D.zc13 != 0.0) D.need13 = 1;
+            if (T.pair == 23 && D.zc23 != 0.0) D.need23 = 1;
+        }
+    }
+}
+
+// Fills A from the plan and this call's raw values/norms.  Returns the rank of
+// a failing fraction check (host-side, FractionOutOfRange) or -1.
+static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end,
+                     const double* values, const double* norms, NllArgs* A) {
+    memset(A, 0, sizeof(NllArgs));
+    pfb_ctx* c = p->ctx;
+    bool aligned = (begin % 2) == 0;
+    for (int s = 0; s < p->nslots; ++s) {
+        A->col[s] = st->cols[p->slot_col[s]];
+        if (((uintptr_t)A->col[s]) % 16) aligned = false;
+    }
+    A->ncols = p->nslots;
+    A->vec2 = aligned ? 1 : 0;
+    A->begin = begin;
+    const int64_t n = end - begin;
+    A->nfull = n / kBlock;
+    A->tail = (int32_t)(n % kBlock);
+    A->evaluator = p->evaluator;
+    int warps = c->warps_override;
+    if (!warps) {
+        const int64_t nb = A->nfull + (A->tail ? 1 : 0);
+        warps = 8;
+        for (int w = 1; w <= 8; w *= 2)
+            if (nb * w >= (int64_t)c->sm_count * 32) {
+                warps = w;
+                break;
+            }
+    }
+    A->warps = warps;
+    A->acc = c->acc;
+    A->ticket = c->ticket;
+    A->errkey = c->errkey;
+    A->tail_scratch = c->tail_scratch;
+    A->result = c->result_dev;
+    A->nops = (int)p->nodes.size();
+    A->final_rank = p->final_rank;
+    int frac_fail = -1;
+    for (int i = 0; i < A->nops; ++i) {
+        const pfb_node& n = p->nodes[i];
+        LitOp& op = A->ops[i];
+        op.kind = n.kind;
+        op.nchild = n.nchild;
+        op.col0 = p->node_slot0[i] < 0 ? 0 : p->node_slot0[i];
+        op.col1 = p->node_slot1[i] < 0 ? 0 : p->node_slot1[i];
+        op.voff = p->der_off[i];
+        op.nv = der_size(n);
+        op.rank = p->rank[i];
+        op.dal = 0;
+        A->norm[i] = norms[i];
+        const double* raw = values + p->raw_off[i];
+        double* der = A->v + p->der_off[i];
+        switch (n.kind) {
+            case PFB_GAUSSIAN:
+                der[0] = raw[0];
+                der[1] = raw[1];
+                break;
+            case PFB_EXPONENTIAL:
+                der[0] = raw[0];
+                break;
+            case PFB_POLYNOMIAL:
+                for (int k = 0; k < n.nparam; ++k) der[k] = raw[k];
+                break;
+            case PFB_ADD: {
+                // pdf._fractions (pdf.py:205-210)
+                const int nf = n.nchild - 1;
+                const double rest = 1.0 - numpy_sum(raw, nf);
+                bool bad = rest < 0.0;
+                for (int k = 0; k < nf; ++k) {
+                    der[k] = raw[k];
+                    if (raw[k] < 0.0 || raw[k] > 1.0) bad = true;
+                }
+                der[nf] = rest;
+                if (bad && (frac_fail < 0 || p->frac_rank[i] < frac_fail)) frac_fail = p->frac_rank[i];
+                break;
+            }
+            default:
+                break;
+        }
+    }
+    build_dal(p, values, A);
+    A->inv_norm = 1.0 / norms[A->nops - 1];
+    // sum of products
+    if (p->evaluator == EV_SOP) {
+        int vo = p->nder;
+        A->nleaf = (int)p->leaf_nodes.size();
+        for (int l = 0; l < A->nleaf; ++l) {
+            const int ni = p->leaf_nodes[l];
+            const pfb_node& n = p->nodes[ni];
+            SopLeaf& L = A->leaf[l];
+            L.kind = n.kind;
+            L.col = p->node_slot0[ni];
+            L.voff = vo;
+            const double* raw = values + p->raw_off[ni];
+            if (n.kind == PFB_GAUSSIAN) {
+                A->v[vo] = raw[0];
+                A->v[vo + 1] = 1.0 / raw[1];
+                L.nv = 2;
+            } else if (n.kind == PFB_EXPONENTIAL) {
+                A->v[vo] = raw[0];
+                L.nv = 1;
+            } else {
+                for (int k = 0; k < n.nparam; ++k) A->v[vo + k] = raw[k];
+                L.nv = n.nparam;
+            }
+            vo += L.nv;
+        }
+        if (vo > kMaxVals) A->evaluator = EV_LITERAL;
+        int nt = 0;
+        for (const auto& ts : p->terms) {
+            double logc = 0.0, budget = 0.0;
+            bool zero = false;
+            for (const auto& f : ts.factors) {
+                double v;
+                if (f.type == 0) {
+                    v = A->v[p->der_off[f.node] + f.child];
+                } else {
+                    v = 1.0 / norms[f.node];
+                }
+                if (!(v > 0.0) || !isfinite(v)) {
+                    zero = true;
+                    break;
+                }
+                const double lv = log(v);
+                logc += lv;
+                budget += fabs(lv);
+            }
+            if (zero) continue;
+            SopTerm& T = A->term[nt++];
+            T.emask = ts.emask;
+            T.vmask = ts.vmask;
+            T.logcoef = logc;
+            T.coef = exp(logc);
+            T.thr = 690.0 - budget;
+        }
+        A->nterm = nt;
+    }
+    return frac_fail;
+}
+
+// The kernels stream double2 pairs from an even start of 16-byte aligned
+// columns.  Ranges that violate this (odd shard starts of small unaligned
+// shards, foreign device pointers) are copied once into context staging.
+static bool range_aligned(const pfb_plan* p, const pfb_store* st, int64_t begin) {
+    if (begin % 2) return false;
+    for (int s = 0; s < p->nslots; ++s)
+        if (((uintptr_t)st->cols[p->slot_col[s]]) % 16) return false;
+    return true;
+}
+
+static int restage(pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end,
+                   pfb_store* tmp) {
+    const int64_t n = end - begin;
+    if (c->e2e_cap < n) {
+        for (auto& ptr : c->e2e_dev) {
+            cudaFree(ptr);
+            ptr = nullptr;
+        }
+        const int64_t padded = ((n + kBlock - 1) / kBlock) * kBlock + 2;
+        for (int i = 0; i < kMaxCols; ++i) CK(cudaMalloc(&c->e2e_dev[i], sizeof(double) * padded));
+        c->e2e_cap = n;
+    }
+    tmp->ctx = c;
+    tmp->owned = false;
+    tmp->n = n;
+    tmp->ncols = st->ncols;
+    for (int i = 0; i < kStoreMaxCols; ++i) tmp->cols[i] = nullptr;
+    for (int s = 0; s < p->nslots; ++s) {
+        const int col = p->slot_col[s];
+        tmp->cols[col] = c->e2e_dev[s];
+        CK(cudaMemcpyAsync(tmp->cols[col], st->cols[col] + begin, sizeof(double) * n,
+                           cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return PFB_OK;
+}
+
+static int sop_ncols(const pfb_plan* p) { return p->nslots < 1 ? 1 : p->nslots; }
+
+static int ensure_cache(pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end,
+                        NllArgs* A) {
+    pfb_ctx* c = p->ctx;
+    const int K = A->dal.K;
+    const int64_t n = end - begin;
+    if (p->cache_store != st || p->cache_begin != begin || p->cache_end != end) {
+        if (p->cache_cap < (int64_t)K * n) {
+            if (p->cache) cudaFree(p->cache);
+            p->cache = nullptr;
+            p->cache_cap = 0;
+            CK(cudaMalloc(&p->cache, sizeof(double2) * (size_t)K * (size_t)(n > 0 ? n : 1)));
+            p->cache_cap = (int64_t)K * n;
+        }
+        p->cache_store = st;
+        p->cache_begin = begin;
+        p->cache_end = end;
+        for (int k = 0; k < kMaxDal; ++k) p->cache_valid[k] = false;
+    }
+    for (int k = 0; k < K; ++k) {
+        DalTerm& T = A->dal.t[k];
+        // shape fingerprint (dalitz.py:108-117): mass and width values
+        const double m2 = T.m2, mg = T.mg;
+        if (!p->cache_valid[k] || memcmp(&p->cache_mw[k][0], &m2, 8) != 0 ||
+            memcmp(&p->cache_mw[k][1], &mg, 8) != 0) {
+            CK(launch_lineshape_cache(A->dal, T, A->col[0] + begin, A->col[1] + begin, n,
+                                      p->cache + (int64_t)k * n, c->stream, c->sm_count));
+            ++c->launches;
+            p->cache_valid[k] = true;
+            p->cache_mw[k][0] = m2;
+            p->cache_mw[k][1] = mg;
+            ++p->cache_recomputes;
+        }
+        T.cached = 1;
+    }
+    A->dal.cache = p->cache;
+    A->dal.cache_stride = n;
+    A->evaluator = EV_DALITZ_CACHED;
+    return PFB_OK;
+}
+
+static int launch_eval(pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end, NllArgs* A,
+                       bool allow_cache = true) {
+    pfb_ctx* c = p->ctx;
+    if (allow_cache && p->evaluator == EV_DALITZ && p->lineshape_mode == 1) {
+        const int rc = ensure_cache(p, st, begin, end, A);
+        if (rc) return rc;
+    }
+    if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
+    CK(launch_nll(*A, c->stream, c->sm_count, sop_ncols(p)));
+    ++c->launches;
+    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
+    return PFB_OK;
+}
+
+// Decode an error key into the reference's exception semantics.
+static int decode_error(pfb_ctx* c, const pfb_plan* p, const NllArgs& A, unsigned long long key,
+                        int frac_rank, int64_t index_offset, pfb_err* err) {
+    pfb_err e;
+    e.code = PFB_OK;
+    e.node = -1;
+    e.index = -1;
+    e.value = NAN;
+    if (key == ~0ull) {
+        if (frac_rank >= 0) e.code = PFB_E_FRACTION_OUT_OF_RANGE;
+    } else {
+        const int rank = (int)(key >> 40);
+        const int64_t local = (int64_t)(key & ((1ull << 40) - 1));
+        if (frac_rank >= 0 && frac_rank < rank) {
+            e.code = PFB_E_FRACTION_OUT_OF_RANGE;
+        } else if (rank == p->final_rank) {
+            e.code = PFB_E_NONPOSITIVE_DENSITY;
+            e.index = index_offset + local;
+        } else {
+            for (int i = 0; i < (int)p->nodes.size(); ++i) {
+                if (p->rank[i] < 0) continue;
+                if (rank == p->rank[i]) {
+                    e.code = PFB_E_NONFINITE_DENSITY;
+                    e.node = i;
+                } else if (p->nodes[i].kind == PFB_POLYNOMIAL && rank == p->rank[i] + 1) {
+                    e.code = PFB_E_NEGATIVE_DENSITY;
+                    e.node = i;
+                }
+            }
+            e.index = local;
+        }
+        if (e.code == PFB_E_NONPOSITIVE_DENSITY || e.code == PFB_E_NEGATIVE_DENSITY) {
+            // the offending value: re-evaluate that one event literally
+            const int64_t j = A.begin + local - A.idx_base;
+            CK(launch_probe(A, j, c->probe_dev, c->stream));
+            ++c->launches;
+            double pv[2];
+            CK(cudaMemcpyAsync(pv, c->probe_dev, sizeof(pv), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            e.value = pv[1];
+        }
+    }
+    if (err) *err = e;
+    return e.code;
+}
+
+static int read_result(pfb_ctx* c) {
+    CK(cudaMemcpyAsync(c->result_host, c->result_dev, sizeof(double) * kResultWords,
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
+    return PFB_OK;
+}
+
+static unsigned long long as_key(double d) {
+    unsigned long long k;
+    memcpy(&k, &d, 8);
+    return k;
+}
+
+static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin,
+                      int64_t end, int64_t index_offset, const double* values, int32_t nvalues,
+                      const double* norms, int32_t nnorms, double* block_sums_host, int64_t n_out,
+                      double* out_nll, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    for (int s = 0; s < p->nslots; ++s)
+        if (p->slot_col[s] >= st->ncols) return PFB_E_INVALID_ARGUMENT;
+    if (out_err) {
+        out_err->code = PFB_OK;
+        out_err->node = -1;
+        out_err->index = -1;
+        out_err->value = NAN;
+    }
+    if (end == begin) {
+        if (out_err) out_err->code = PFB_E_EMPTY_DATASET;
+        return PFB_E_EMPTY_DATASET;
+    }
+    CK(cudaSetDevice(c->device));
+    pfb_store staged;
+    const bool restaged = !range_aligned(p, st, begin);
+    if (restaged) {
+        const int rs = restage(c, p, st, begin, end, &staged);
+        if (rs) return rs;
+        st = &staged;
+        end -= begin;
+        begin = 0;
+    }
+    auto A = std::make_unique<NllArgs>();
+    const int frac = pack_args(p, st, begin, end, values, norms, A.get());
+    const int64_t nb = A->nfull + (A->tail ? 1 : 0);
+    if (block_sums_host) {
+        if (n_out < nb) return PFB_E_INVALID_ARGUMENT;
+        if (c->bsums_cap < nb) {
+            cudaFree(c->bsums);
+            c->bsums = nullptr;
+            CK(cudaMalloc(&c->bsums, sizeof(double) * nb));
+            c->bsums_cap = nb;
+        }
+        A->block_sums = c->bsums;
+    }
+    A->mode = 0;
+    int rc = launch_eval(p, st, begin, end, A.get(), !restaged);
+    if (rc) return rc;
+    rc = read_result(c);
+    if (rc) return rc;
+    const unsigned long long key = as_key(c->result_host[2]);
+    const int code = decode_error(c, p, *A, key, frac, index_offset, out_err);
+    if (code) return code;
+    if (block_sums_host)
+        CK(cudaMemcpy(block_sums_host, c->bsums, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    const int st_round = (int)c->result_host[3];
+    if (out_nll) *out_nll = c->result_host[0];
+    if (st_round && out_err) out_err->code = st_round;
+    return st_round;
+}
+
+extern "C" {
+
+int pfb_nll(pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end,
+            int64_t index_offset, const double* values, int32_t nvalues, const double* norms,
+            int32_t nnorms, double* out_nll, pfb_err* out_err) {
+    return nll_common(c, p, st, begin, end, index_offset, values, nvalues, norms, nnorms, nullptr,
+                      0, out_nll, out_err);
+}
+
+int pfb_nll_block_sums(pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int64_t begin,
+                       int64_t end, int64_t index_offset, const double* values, int32_t nvalues,
+                       const double* norms, int32_t nnorms, double* out_block_sums, int64_t n_out,
+                       pfb_err* out_err) {
+    if (!out_block_sums) return PFB_E_INVALID_ARGUMENT;
+    return nll_common(c, p, st, begin, end, index_offset, values, nvalues, norms, nnorms,
+                      out_block_sums, n_out, nullptr, out_err);
+}
+
+int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin,
+                          int64_t end, int64_t index_offset, const double* values,
+                          int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || !dev_acc || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    pfb_store staged;
+    const bool restaged = end > begin && !range_aligned(p, st, begin);
+    if (restaged) {
+        const int rs = restage(c, p, st, begin, end, &staged);
+        if (rs) return rs;
+        st = &staged;
+        end -= begin;
+        begin = 0;
+    }
+    c->last_args.reset(new NllArgs());
+    NllArgs* A = c->last_args.get();
+    c->last_frac_rank = pack_args(p, st, begin, end, values, norms, A);
+    c->last_plan = p;
+    c->last_index_offset = index_offset;
+    if (end == begin) {  // empty shard: a zero partial (sharding.partial_nll, sharding.py:110-111)
+        CK(cudaMemsetAsync(dev_acc, 0, sizeof(int64_t) * PFB_ACC_WORDS, c->stream));
+        CK(cudaMemsetAsync(c->result_dev + 1, 0, sizeof(double), c->stream));
+        CK(cudaMemsetAsync(c->result_dev + 2, 0xff, sizeof(double), c->stream));
+        return PFB_OK;
+    }
+    A->mode = 1;
+    A->acc_out = (long long*)dev_acc;
+    return launch_eval(p, st, begin, end, A, !restaged);
+}
+
+int pfb_finalize(pfb_ctx* c, const int64_t* dev_acc, double* out_nll, int64_t* out_fails) {
+    if (!c || !dev_acc) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    CK(launch_finalize((const long long*)dev_acc, c->result_dev + 4, nullptr, nullptr, c->stream));
+    ++c->launches;
+    int rc = read_result(c);
+    if (rc) return rc;
+    if (out_nll) *out_nll = c->result_host[4];
+    if (out_fails) *out_fails = (int64_t)c->result_host[5];
+    return (int)c->result_host[7];
+}
+
+int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
+    if (!c || !out_err || !c->last_args) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    int rc = read_result(c);
+    if (rc) return rc;
+    const unsigned long long key = as_key(c->result_host[2]);
+    decode_error(c, c->last_plan, *c->last_args, key, c->last_frac_rank, c->last_index_offset,
+                 out_err);
+    return PFB_OK;
+}
+
+int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols, int32_t ncols,
+                 int64_t n, const double* values, int32_t nvalues, const double* norms,
+                 int32_t nnorms, double* out_nll, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !host_cols || ncols < 1 || ncols > kMaxCols || n < 0 || !values || !norms)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    for (int s = 0; s < p->nslots; ++s)
+        if (p->slot_col[s] >= ncols) return PFB_E_INVALID_ARGUMENT;
+    if (out_err) {
+        out_err->code = PFB_OK;
+        out_err->node = -1;
+        out_err->index = -1;
+        out_err->value = NAN;
+    }
+    if (n == 0) {
+        if (out_err) out_err->code = PFB_E_EMPTY_DATASET;
+        return PFB_E_EMPTY_DATASET;
+    }
+    CK(cudaSetDevice(c->device));
+    if (c->e2e_cap < n) {
+        for (auto& ptr : c->e2e_dev) {
+            cudaFree(ptr);
+            ptr = nullptr;
+        }
+        const int64_t padded = ((n + kBlock - 1) / kBlock) * kBlock + 2;
+        for (int i = 0; i < kMaxCols; ++i) CK(cudaMalloc(&c->e2e_dev[i], sizeof(double) * padded));
+        c->e2e_cap = n;
+    }
+    pfb_store st;
+    st.ctx = c;
+    st.ncols = ncols;
+    st.n = n;
+    for (int i = 0; i < ncols; ++i) st.cols[i] = c->e2e_dev[i];
+    // chunks of 256 blocks (1 Mi events); copies on the copy stream, one
+    // accumulate-mode launch per landed chunk on the compute stream.
+    const int64_t chunk = 256LL * kBlock;
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    while ((int64_t)c->chunk_events.size() < nchunks) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->chunk_events.push_back(e);
+    }
+    // the copy stream must not overwrite staging still read by a previous call
+    cudaEvent_t prior;
+    CK(cudaEventCreateWithFlags(&prior, cudaEventDisableTiming));
+    CK(cudaEventRecord(prior, c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, prior, 0));
+    cudaEventDestroy(prior);
+    NllArgs A0;
+    const int frac = pack_args(p, &st, 0, n, values, norms, &A0);
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int64_t b = k * chunk, e = std::min(n, b + chunk);
+        for (int s = 0; s < ncols; ++s)
+            CK(cudaMemcpyAsync(c->e2e_dev[s] + b, host_cols[s] + b, sizeof(double) * (e - b),
+                               cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaEventRecord(c->chunk_events[k], c->copy_stream));
+        CK(cudaStreamWaitEvent(c->stream, c->chunk_events[k], 0));
+        auto A = std::make_unique<NllArgs>();
+        pack_args(p, &st, b, e, values, norms, A.get());
+        A->idx_base = b;
+        A->mode = 2;
+        int rc = launch_eval(p, &st, b, e, A.get(), /*allow_cache=*/false);
+        if (rc) return rc;
+    }
+    CK(launch_finalize((const long long*)c->acc, c->result_dev, c->acc, c->errkey, c->stream));
+    ++c->launches;
+    int rc = read_result(c);
+    if (rc) return rc;
+    const unsigned long long key = as_key(c->result_host[2]);
+    A0.idx_base = 0;
+    const int code = decode_error(c, p, A0, key, frac, 0, out_err);
+    if (code) return code;
+    const int st_round = (int)c->result_host[3];
+    if (out_nll) *out_nll = c->result_host[0];
+    if (st_round && out_err) out_err->code = st_round;
+    return st_round;
+}
+
+int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double* out_block_sums,
+                         double* out_total) {
+    if (!c || (!host_terms && n) || n < 0) return PFB_E_INVALID_ARGUMENT;
+    if (n == 0) {
+        if (out_total) *out_total = 0.0;
+        return PFB_OK;
+    }
+    CK(cudaSetDevice(c->device));
+    pfb_store* st = nullptr;
+    int rc = pfb_store_create(c, 1, n, &st);
+    if (rc) return rc;
+    std::unique_ptr<pfb_store, int (*)(pfb_store*)> guard(st, pfb_store_destroy);
+    rc = pfb_store_upload(st, 0, host_terms, 0, n);
+    if (rc) return rc;
+    auto A = std::make_unique<NllArgs>();
+    memset(A.get(), 0, sizeof(NllArgs));
+    A->col[0] = st->cols[0];
+    A->ncols = 1;
+    A->vec2 = 1;
+    A->begin = 0;
+    A->nfull = n / kBlock;
+    A->tail = (int32_t)(n % kBlock);
+    A->evaluator = 100;
+    const int64_t nb = A->nfull + (A->tail ? 1 : 0);
+    int warps = c->warps_override;
+    if (!warps) {
+        warps = 8;
+        for (int w = 1; w <= 8; w *= 2)
+            if (nb * w >= (int64_t)c->sm_count * 32) {
+                warps = w;
+                break;
+            }
+    }
+    A->warps = warps;
+    A->acc = c->acc;
+    A->ticket = c->ticket;
+    A->errkey = c->errkey;
+    A->tail_scratch = c->tail_scratch;
+    A->result = c->result_dev;
+    if (c->bsums_cap < nb) {
+        cudaFree(c->bsums);
+        c->bsums = nullptr;
+        CK(cudaMalloc(&c->bsums, sizeof(double) * nb));
+        c->bsums_cap = nb;
+    }
+    A->block_sums = c->bsums;
+    A->mode = 0;
+    CK(launch_nll(*A, c->stream, c->sm_count, 1));
+    ++c->launches;
+    rc = read_result(c);
+    if (rc) return rc;
+    if (out_block_sums)
+        CK(cudaMemcpy(out_block_sums, c->bsums, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    if (out_total) *out_total = c->result_host[0];
+    return (int)c->result_host[3];
+}
+
+int pfb_exact_sum_host(const double* v, int64_t n, double* out) {
+    if ((!v && n) || !out || n < 0) return PFB_E_INVALID_ARGUMENT;
+    long long acc[PFB_ACC_WORDS];
+    memset(acc, 0, sizeof(acc));
+    for (int64_t i = 0; i < n; ++i) acc_add_host(acc, v[i]);
+    return acc_round(acc, out);
+}
+
+int pfb_acc_round(const int64_t* acc, double* out) {
+    if (!acc || !out) return PFB_E_INVALID_ARGUMENT;
+    return acc_round((const long long*)acc, out);
+}
+
+int pfb_acc_add_host(int64_t* acc, const double* v, int64_t n) {
+    if (!acc || (!v && n) || n < 0) return PFB_E_INVALID_ARGUMENT;
+    for (int64_t i = 0; i < n; ++i) acc_add_host((long long*)acc, v[i]);
+    return PFB_OK;
+}
+
+int pfb_shard_bounds(int64_t n, int32_t workers, int64_t block, int64_t* bounds) {
+    if (workers < 1 || n < 0 || !bounds || block < 1) return PFB_E_INVALID_ARGUMENT;
+    // sharding.shard (sharding.py:80-85)
+    const int64_t base = n / workers, extra = n % workers;
+    bounds[0] = 0;
+    for (int k = 0; k < workers; ++k) bounds[k + 1] = bounds[k] + base + (k < extra ? 1 : 0);
+    if (n >= (int64_t)workers * block)
+        for (int k = 1; k < workers; ++k) bounds[k] = (bounds[k] / block) * block;
+    bounds[workers] = n;
+    return PFB_OK;
+}
+
+// ---- Dalitz grid ---------------------------------------------------------------
+
+int pfb_grid_create(pfb_ctx* c, const pfb_dalitz_desc* d, int32_t nx, int32_t ny, pfb_grid** out) {
+    if (!c || !d || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (nx < 32 || ny < 32) return PFB_E_DEGENERATE_GRID;  // dalitz.py:253-254
+    CK(cudaSetDevice(c->device));
+    auto g = std::make_unique<pfb_grid>();
+    g->ctx = c;
+    g->desc = *d;
+    GridConsts& k = g->g;
+    k.nx = nx;
+    k.ny = ny;
+    const double M = d->mother_mass;
+    // DecayChannel.s12_range / s13_range (dalitz.py:68-74): Python (a)**2
+    const double a12 = d->m1 + d->m2, b12 = M - d->m3, a13 = d->m1 + d->m3, b13 = M - d->m2;
+    k.lo12 = a12 * a12;
+    k.hi12 = b12 * b12;
+    k.lo13 = a13 * a13;
+    const double hi13 = b13 * b13;
+    k.dx = (k.hi12 - k.lo12) / nx;
+    k.dy = (hi13 - k.lo13) / ny;
+    k.m1sq = d->m1 * d->m1;
+    k.m2sq = d->m2 * d->m2;
+    k.m3sq = d->m3 * d->m3;
+    k.M2 = M * M;
+    g->area = k.dx * k.dy;
+    const int64_t total = (int64_t)nx * ny;
+    int* row_count = nullptr;
+    CK(cudaMalloc(&g->mask, total));
+    CK(cudaMalloc(&row_count, sizeof(int) * nx));
+    std::unique_ptr<int, cudaError_t (*)(void*)> rc_guard(row_count, cudaFree);
+    CK(cudaMemsetAsync(row_count, 0, sizeof(int) * nx, c->stream));
+    CK(launch_grid_mask(k, g->mask, row_count, c->stream));
+    ++c->launches;
+    std::vector<int> counts(nx), offs(nx);
+    CK(cudaMemcpyAsync(counts.data(), row_count, sizeof(int) * nx, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t acc = 0;
+    for (int i = 0; i < nx; ++i) {
+        offs[i] = (int)acc;
+        acc += counts[i];
+    }
+    g->n_inside = acc;
+    CK(cudaMemcpyAsync(row_count, offs.data(), sizeof(int) * nx, cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMalloc(&g->p12, sizeof(double) * (acc > 0 ? acc : 1)));
+    CK(cudaMalloc(&g->p13, sizeof(double) * (acc > 0 ? acc : 1)));
+    CK(launch_grid_compact(k, g->mask, row_count, g->p12, g->p13, c->stream));
+    ++c->launches;
+    CK(cudaStreamSynchronize(c->stream));
+    *out = g.release();
+    return PFB_OK;
+}
+
+int pfb_grid_info(const pfb_grid* g, int64_t* n_inside, double* area) {
+    if (!g) return PFB_E_INVALID_ARGUMENT;
+    if (n_inside) *n_inside = g->n_inside;
+    if (area) *area = g->area;
+    return PFB_OK;
+}
+
+int pfb_grid_mask(const pfb_grid* g, uint8_t* host_mask) {
+    if (!g || !host_mask) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(g->ctx->device));
+    CK(cudaMemcpy(host_mask, g->mask, (size_t)g->g.nx * g->g.ny, cudaMemcpyDeviceToHost));
+    return PFB_OK;
+}
+
+int pfb_grid_integrals(pfb_ctx* c, pfb_grid* g, int32_t K, const int32_t* pair,
+                       const int32_t* spin, const double* mass_width, const uint8_t* rows,
+                       const uint8_t* stale, double* inout) {
+    if (!c || !g || K < 1 || K > kMaxDal || !pair || !spin || !mass_width || !rows || !stale ||
+        !inout)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    const int64_t n = g->n_inside;
+    if (g->amps_rows < K) {
+        double2* na = nullptr;
+        CK(cudaMalloc(&na, sizeof(double2) * (size_t)K * (size_t)(n > 0 ? n : 1)));
+        if (g->amps) {
+            CK(cudaMemcpyAsync(na, g->amps, sizeof(double2) * (size_t)g->amps_rows * n,
+                               cudaMemcpyDeviceToDevice, c->stream));
+            cudaStreamSynchronize(c->stream);
+            cudaFree(g->amps);
+        }
+        g->amps = na;
+        g->amps_rows = K;
+    }
+    // channel constants as in build_dal
+    DalDesc D;
+    memset(&D, 0, sizeof(D));
+    const pfb_dalitz_desc& d = g->desc;
+    const double M = d.mother_mass;
+    const double M2 = M * M, m1sq = d.m1 * d.m1, m2sq = d.m2 * d.m2, m3sq = d.m3 * d.m3;
+    D.K = K;
+    D.mss = ((M2 + m1sq) + m2sq) + m3sq;
+    D.zc12 = (M2 - m3sq) * (m2sq - m1sq);
+    D.zc13 = (M2 - m2sq) * (m3sq - m1sq);
+    D.zc23 = (M2 - m1sq) * (m3sq - m2sq);
+    for (int k = 0; k < K; ++k) {
+        if (!rows[k]) continue;
+        if (!(pair[k] == 12 || pair[k] == 13 || pair[k] == 23) || !(spin[k] == 0 || spin[k] == 1))
+            return PFB_E_INVALID_ARGUMENT;
+        DalTerm T;
+        memset(&T, 0, sizeof(T));
+        T.pair = pair[k];
+        T.spin = spin[k];
+        const double m = mass_width[2 * k], w = mass_width[2 * k + 1];
+        T.m2 = m * m;
+        T.mg = m * w;
+        CK(launch_grid_amp(D, T, g->p12, g->p13, n, g->amps + (int64_t)k * n, c->stream,
+                           c->sm_count));
+        ++c->launches;
+    }
+    std::vector<int2> pairs;
+    for (int i = 0; i < K; ++i)
+        for (int j = i; j < K; ++j)
+            if (stale[i] || stale[j]) pairs.push_back(make_int2(i, j));
+    if (!pairs.empty() && n > 0) {
+        const size_t words = pairs.size() * 2 * PFB_ACC_WORDS;
+        int2* dpairs = nullptr;
+        unsigned long long* dacc = nullptr;
+        CK(cudaMalloc(&dpairs, sizeof(int2) * pairs.size()));
+        CK(cudaMalloc(&dacc, sizeof(unsigned long long) * words));
+        std::unique_ptr<int2, cudaError_t (*)(void*)> g1(dpairs, cudaFree);
+        std::unique_ptr<unsigned long long, cudaError_t (*)(void*)> g2(dacc, cudaFree);
+        CK(cudaMemcpyAsync(dpairs, pairs.data(), sizeof(int2) * pairs.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemsetAsync(dacc, 0, sizeof(unsigned long long) * words, c->stream));
+        CK(launch_grid_overlap(g->amps, n, dpairs, (int)pairs.size(), dacc, c->stream,
+                               c->sm_count));
+        ++c->launches;
+        std::vector<long long> hacc(words);
+        CK(cudaMemcpyAsync(hacc.data(), dacc, sizeof(long long) * words, cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t q = 0; q < pairs.size(); ++q) {
+            double re, im;
+            acc_round(&hacc[(q * 2) * PFB_ACC_WORDS], &re);
+            acc_round(&hacc[(q * 2 + 1) * PFB_ACC_WORDS], &im);
+            const int i = pairs[q].x, j = pairs[q].y;
+            // dalitz.py:321-328: diagonal real sum * dA; off-diagonal complex sum * dA
+            re = re * g->area;
+            im = (i == j) ? 0.0 : im * g->area;
+            inout[2 * (i * K + j)] = re;
+            inout[2 * (i * K + j) + 1] = im;
+            inout[2 * (j * K + i)] = re;
+            inout[2 * (j * K + i) + 1] = (i == j) ? 0.0 : -im;
+        }
+    } else if (!pairs.empty()) {
+        for (auto pr : pairs) {
+            const int i = pr.x, j = pr.y;
+            inout[2 * (i * K + j)] = inout[2 * (i * K + j) + 1] = 0.0;
+            inout[2 * (j * K + i)] = inout[2 * (j * K + i) + 1] = 0.0;
+        }
+    }
+    return PFB_OK;
+}
+
+int pfb_grid_destroy(pfb_grid* g) {
+    if (!g) return PFB_OK;
+    cudaSetDevice(g->ctx->device);
+    cudaFree(g->mask);
+    cudaFree(g->p12);
+    cudaFree(g->p13);
+    cudaFree(g->amps);
+    delete g;
+    return PFB_OK;
+}
+
+int pfb_fp64_peak(pfb_ctx* c, double* out) {
+    if (!c || !out) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    const int blocks = c->sm_count * 8, threads = 256, iters = 2048;
+    CK(launch_fp64_peak(c->probe_dev, blocks, threads, 16, c->stream));  // warm-up
+    CK(cudaEventRecord(c->ev0, c->stream));
+    CK(launch_fp64_peak(c->probe_dev, blocks, threads, iters, c->stream));
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->launches += 2;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    const double flops = 2.0 * 16.0 * 8.0 * (double)iters * (double)blocks * threads;
+    *out = flops / (ms * 1e-3) / 1e12;
+    return PFB_OK;
+}
+
+}  // extern "C"

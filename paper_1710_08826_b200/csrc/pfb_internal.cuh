@@ -1,0 +1,310 @@
+// pfb_internal.cuh -- device-side plan layout, exact accumulator, IEEE helpers.
+//
+// Shared by the NLL kernels (pfb_nll.cu), the Dalitz grid kernels (pfb_dalitz.cu)
+// and the C ABI (pfb_api.cu).  The accumulator helpers are __host__ __device__
+// so the CPU test-suite exercises the very code the GPU runs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pfb200.h"
+
+#define PFB_HD __host__ __device__ __forceinline__
+#ifdef __CUDA_ARCH__
+// keep the 68-limb working set of the (once per launch) rounding in local memory
+#define PFB_NOUNROLL _Pragma("unroll 1")
+#else
+#define PFB_NOUNROLL
+#endif
+
+namespace pfb {
+
+PFB_HD double __longlong_as_double_hd(long long v) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(v);
+#else
+    double d;
+    __builtin_memcpy(&d, &v, 8);
+    return d;
+#endif
+}
+
+constexpr int kBlock = PFB_BLOCK;        // 4096 events per reduction block
+constexpr int kMaxNodes = 16;            // post-order ops of the literal interpreter
+constexpr int kMaxCols = 4;              // distinct observable columns
+constexpr int kMaxVals = 128;            // derived per-call values (literal path)
+constexpr int kMaxLeaves = 4;            // sum-of-products leaves (fast path)
+constexpr int kMaxTerms = 4;             // sum-of-products terms (fast path)
+constexpr int kMaxDal = PFB_MAX_DALITZ_TERMS;
+constexpr int kThreads = 256;            // CTA size of the NLL kernels
+
+enum Evaluator : int32_t { EV_LITERAL = 0, EV_SOP = 1, EV_DALITZ = 2, EV_DALITZ_CACHED = 3 };
+
+// ---------------------------------------------------------------------------
+// Literal interpreter: one op per tree node, post-order.  Evaluates exactly
+// the reference operation sequence (eval_batch recursion, pdf.py:251-269).
+struct LitOp {
+    int32_t kind;
+    int32_t nchild;
+    int32_t col0, col1;   // column slots (index into NllArgs::col)
+    int32_t voff;         // offset of this node's derived values in NllArgs::v
+    int32_t nv;
+    int32_t rank;         // rank of this node's first check (evaluation order)
+    int32_t dal;          // dalitz: index into NllArgs dalitz tables
+};
+
+// Sum-of-products flattening of add/prod trees over gaussian/exponential/
+// polynomial leaves:  p(x) = sum_t coef_t * prod_{l in t} leaf_l(x).
+struct SopLeaf {
+    int32_t kind;  // PFB_GAUSSIAN / PFB_EXPONENTIAL / PFB_POLYNOMIAL
+    int32_t col;   // column slot
+    int32_t voff;  // gaussian: mu, 1/sigma; exponential: alpha; polynomial: coeffs
+    int32_t nv;
+};
+struct SopTerm {
+    uint32_t emask;   // exp-type leaves (gaussian/exponential) multiplied in
+    uint32_t vmask;   // value-type leaves (polynomial) multiplied in
+    double logcoef;   // log(coef_t)
+    double coef;      // coef_t
+    double thr;       // guard threshold on sum |u_l| (+ value-leaf exponent budget)
+};
+
+// Dalitz fast evaluator (dalitz.py:162-230): per-term constants.
+struct DalTerm {
+    int32_t pair;     // 12, 13, 23
+    int32_t spin;     // 0, 1
+    int32_t cached;   // amplitude read from the lineshape cache
+    int32_t zinv;     // spin-1 Zemach needs 1/s_pair (constant != 0)
+    double m2;        // m*m
+    double mg;        // m*width
+    double mg2;       // (m*width)^2
+    double cre, cim;  // magnitude*(cos phase, sin phase)
+};
+
+struct DalDesc {
+    int32_t K;
+    int32_t ninv;     // number of 1/s_pair the Zemach factors need
+    int32_t need12, need13, need23;
+    double mss;       // M^2+m1^2+m2^2+m3^2 (DecayChannel.mass_sum_sq)
+    double zc12, zc13, zc23;  // Zemach constants (M^2-m_k^2)(m_j^2-m_i^2)
+    DalTerm t[kMaxDal];
+    const double2* cache;     // lineshape cache base (K rows of n events, double2)
+    int64_t cache_stride;     // events per row
+};
+
+struct NllArgs {
+    const double* col[kMaxCols];
+    int32_t ncols;
+    int32_t vec2;             // double2 loads allowed
+    int64_t begin;            // first event (store index)
+    int64_t nfull;            // number of full 4096-blocks
+    int32_t tail;             // events in the trailing partial block
+    int32_t evaluator;
+    int32_t warps;            // warps cooperating on one block (1,2,4,8)
+    int32_t mode;             // 0: finalize in last CTA; 1: export accumulator; 2: keep accumulating
+    int64_t idx_base;         // added to local event indices in error keys
+    double* block_sums;       // optional per-block output
+    unsigned long long* acc;  // PFB_ACC_WORDS persistent accumulator (self-resetting)
+    unsigned int* ticket;     // CTA completion counter (self-resetting)
+    unsigned long long* errkey;  // min (rank<<40 | local index), ~0 when clean
+    double* tail_scratch;     // 4096 doubles
+    double* result;           // [0] nll, [1] fails (as double), [2] err key (bits)
+    long long* acc_out;       // mode 1 destination
+    // literal interpreter
+    int32_t nops;
+    int32_t final_rank;       // rank of the root p > 0 check
+    LitOp ops[kMaxNodes];
+    double norm[kMaxNodes];   // per-node normalisation
+    double v[kMaxVals];       // derived per-call values
+    // sum-of-products
+    int32_t nleaf, nterm;
+    SopLeaf leaf[kMaxLeaves];
+    SopTerm term[kMaxTerms];
+    // dalitz
+    double inv_norm;          // 1/norm_root (fast paths)
+    DalDesc dal;
+};
+
+// Dalitz integration grid constants (dalitz.py:246-264).
+struct GridConsts {
+    int nx, ny;
+    double lo12, hi12, lo13, dx, dy;
+    double m1sq, m2sq, m3sq, M2;
+};
+
+// ---------------------------------------------------------------------------
+// Exact accumulator.  A finite double x = m * 2^(b-1074) with integer m < 2^53
+// and b >= 0 is added as three signed 32-bit digits into int64 limbs
+// [b/32, b/32+1, b/32+2].  Integer addition is associative, so any grouping of
+// blocks, CTAs, shards and GPUs yields the same limbs; pfb::acc_round then
+// returns the correctly rounded (round-half-even) exact sum == math.fsum.
+
+struct Digits {
+    int32_t limb;        // index of the lowest limb
+    long long d[3];      // signed digits
+    int32_t special;     // 0 finite, PFB_ACC_POSINF / NEGINF / NAN
+};
+
+PFB_HD Digits split_double(double x) {
+    Digits r;
+    r.limb = 0;
+    r.d[0] = r.d[1] = r.d[2] = 0;
+    r.special = 0;
+    unsigned long long bits;
+#ifdef __CUDA_ARCH__
+    bits = (unsigned long long)__double_as_longlong(x);
+#else
+    __builtin_memcpy(&bits, &x, 8);
+#endif
+    const unsigned E = (unsigned)((bits >> 52) & 0x7ffu);
+    const unsigned long long frac = bits & 0xfffffffffffffull;
+    const bool neg = (bits >> 63) != 0;
+    if (E == 0x7ffu) {
+        r.special = frac ? PFB_ACC_NAN : (neg ? PFB_ACC_NEGINF : PFB_ACC_POSINF);
+        return r;
+    }
+    unsigned long long m;
+    unsigned b;
+    if (E == 0) {
+        m = frac;
+        b = 0;
+    } else {
+        m = frac | (1ull << 52);
+        b = E - 1;
+    }
+    if (m == 0) return r;
+    const unsigned s = b & 31u;
+    r.limb = (int32_t)(b >> 5);
+    const unsigned long long lo = m << s;
+    const unsigned long long hi = s ? (m >> (64 - s)) : 0ull;
+    long long d0 = (long long)(lo & 0xffffffffull);
+    long long d1 = (long long)(lo >> 32);
+    long long d2 = (long long)hi;
+    if (neg) {
+        d0 = -d0;
+        d1 = -d1;
+        d2 = -d2;
+    }
+    r.d[0] = d0;
+    r.d[1] = d1;
+    r.d[2] = d2;
+    return r;
+}
+
+PFB_HD void acc_add_host(long long* acc, double x) {
+    Digits d = split_double(x);
+    if (d.special) {
+        acc[d.special] += 1;
+        return;
+    }
+    acc[d.limb] += d.d[0];
+    acc[d.limb + 1] += d.d[1];
+    acc[d.limb + 2] += d.d[2];
+}
+
+PFB_HD int clz32(unsigned v) {
+#ifdef __CUDA_ARCH__
+    return __clz((int)v);
+#else
+    return v ? __builtin_clz(v) : 32;
+#endif
+}
+
+PFB_HD double ldexp_exact(double m, int e) {
+    // m * 2^e for an exactly representable result (or overflow to inf).
+#ifdef __CUDA_ARCH__
+    return ldexp(m, e);
+#else
+    return __builtin_ldexp(m, e);
+#endif
+}
+
+// Correctly rounded value of the accumulator.  Returns PFB_OK or
+// PFB_E_INVALID_SUM (+inf and -inf both present, as math.fsum raises).
+PFB_HD int acc_round(const long long* acc_in, double* out) {
+    const long long pinf = acc_in[PFB_ACC_POSINF], ninf = acc_in[PFB_ACC_NEGINF];
+    if (acc_in[PFB_ACC_NAN] > 0) {
+        *out = __longlong_as_double_hd(0x7ff8000000000000ll);
+        return PFB_OK;
+    }
+    if (pinf > 0 && ninf > 0) {
+        *out = __longlong_as_double_hd(0x7ff8000000000000ll);
+        return PFB_E_INVALID_SUM;
+    }
+    if (pinf > 0) {
+        *out = __longlong_as_double_hd(0x7ff0000000000000ll);
+        return PFB_OK;
+    }
+    if (ninf > 0) {
+        *out = __longlong_as_double_hd((long long)0xfff0000000000000ull);
+        return PFB_OK;
+    }
+    long long L[PFB_NLIMBS];
+    PFB_NOUNROLL for (int i = 0; i < PFB_NLIMBS; ++i) L[i] = acc_in[i];
+    // carry-normalise: limbs 0..66 into [0, 2^32), the top limb keeps the sign
+    PFB_NOUNROLL for (int i = 0; i < PFB_NLIMBS - 1; ++i) {
+        const long long c = L[i] >> 32;  // arithmetic shift = floor division
+        L[i] -= (long long)((unsigned long long)c << 32);
+        L[i + 1] += c;
+    }
+    bool neg = L[PFB_NLIMBS - 1] < 0;
+    if (neg) {
+        PFB_NOUNROLL for (int i = 0; i < PFB_NLIMBS; ++i) L[i] = -L[i];
+        PFB_NOUNROLL for (int i = 0; i < PFB_NLIMBS - 1; ++i) {
+            const long long c = L[i] >> 32;
+            L[i] -= (long long)((unsigned long long)c << 32);
+            L[i + 1] += c;
+        }
+    }
+    if (L[PFB_NLIMBS - 1] >= (1ll << 32)) {  // far beyond DBL_MAX
+        *out = neg ? __longlong_as_double_hd((long long)0xfff0000000000000ull)
+                   : __longlong_as_double_hd(0x7ff0000000000000ll);
+        return PFB_OK;
+    }
+    int h = PFB_NLIMBS - 1;
+    PFB_NOUNROLL while (h >= 0 && L[h] == 0) --h;
+    if (h < 0) {
+        *out = 0.0;  // math.fsum of zeros is +0.0
+        return PFB_OK;
+    }
+    const int bitlen = 32 * h + (32 - clz32((unsigned)L[h]));
+    double r;
+    if (bitlen <= 64) {
+        unsigned long long k = 0;
+        PFB_NOUNROLL for (int i = h; i >= 0; --i) k = (k << 32) | (unsigned long long)L[i];
+        unsigned long long m = k;
+        int e = -1074;
+        if (bitlen > 53) {  // round k to 53 significant bits, half-even
+            const int sh = bitlen - 53;
+            const unsigned long long rem = k & ((1ull << sh) - 1);
+            const unsigned long long half = 1ull << (sh - 1);
+            m = k >> sh;
+            if (rem > half || (rem == half && (m & 1ull))) m += 1;
+            e += sh;
+        }
+        r = ldexp_exact((double)m, e);
+    } else {
+        const int top = bitlen - 64;  // bit index of the window's lsb
+        const int i0 = top >> 5, s = top & 31;
+        unsigned long long w;
+        {
+            const unsigned long long a0 = (unsigned long long)L[i0];
+            const unsigned long long a1 = (i0 + 1 < PFB_NLIMBS) ? (unsigned long long)L[i0 + 1] : 0;
+            const unsigned long long a2 = (i0 + 2 < PFB_NLIMBS) ? (unsigned long long)L[i0 + 2] : 0;
+            const unsigned long long lo64 = a0 | (a1 << 32);
+            w = s ? ((lo64 >> s) | (a2 << (64 - s))) : lo64;
+        }
+        bool sticky = s ? (((unsigned long long)L[i0] & ((1ull << s) - 1)) != 0) : false;
+        PFB_NOUNROLL for (int i = 0; i < i0 && !sticky; ++i) sticky = L[i] != 0;
+        unsigned long long m = w >> 11;
+        const unsigned long long rem = w & 0x7ffull;
+        if (rem > 0x400ull || (rem == 0x400ull && (sticky || (m & 1ull)))) m += 1;
+        // m may become 2^53: still exact as a double, ldexp handles it
+        r = ldexp_exact((double)m, top + 11 - 1074);
+    }
+    *out = neg ? -r : r;
+    return PFB_OK;
+}
+
+}  // namespace pfb

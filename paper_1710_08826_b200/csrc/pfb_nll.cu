@@ -1,0 +1,94 @@
+// pfb_nll.cu -- generic instantiations (literal interpreter, reduction
+// known-answer mode), the rounding kernel, the error probe, the FP64 peak
+// microbenchmark and the evaluator dispatch.
+#include "pfb_nll_kernel.cuh"
+
+namespace pfb {
+
+cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
+cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count);
+
+// Rounds an accumulator already resident on the device (after an allreduce,
+// or after a chain of mode-2 launches).  One warp; thread 0 does the rounding.
+__global__ void finalize_kernel(const long long* acc, double* result, unsigned long long* reset_acc,
+                                unsigned long long* errkey_reset) {
+    __shared__ long long s[PFB_ACC_WORDS];
+    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) s[i] = acc[i];
+    __syncthreads();
+    if (reset_acc)
+        for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) reset_acc[i] = 0ull;
+    if (threadIdx.x == 0) {
+        double r;
+        const int st = acc_round_dev(s, &r);
+        result[0] = r;
+        result[1] = (double)s[PFB_ACC_FAILS];
+        if (errkey_reset) {
+            result[2] = __longlong_as_double((long long)*errkey_reset);
+            *errkey_reset = ~0ull;
+        }
+        result[3] = (double)st;
+    }
+}
+
+// Re-evaluates one event literally (error path: the offending value).
+__global__ void probe_kernel(const __grid_constant__ NllArgs A, int64_t j, double* out) {
+    int rank = -1;
+    double val = 0.0;
+    out[0] = literal_event(A, j, &rank, &val);
+    out[1] = val;
+}
+
+// FP64 issue-rate microbenchmark: independent DFMA chains.
+__global__ void fp64_peak_kernel(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double b = 0.999999, c = 1e-7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            a0 = fma(a0, b, c);
+            a1 = fma(a1, b, c);
+            a2 = fma(a2, b, c);
+            a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c);
+            a5 = fma(a5, b, c);
+            a6 = fma(a6, b, c);
+            a7 = fma(a7, b, c);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.0) out[0] = s;
+}
+
+
+cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
+    switch (A.evaluator) {
+        case EV_SOP:
+            return launch_sop(A, stream, sm_count, nc);
+        case EV_DALITZ:
+        case EV_DALITZ_CACHED:
+            return launch_dalitz(A, stream, sm_count);
+        case 100:  // reduction known-answer mode
+            return launch_p<EvTerms>(A, stream, sm_count);
+        default:
+            return launch_p<EvLiteral<1>>(A, stream, sm_count);
+    }
+}
+
+cudaError_t launch_finalize(const long long* acc, double* result, unsigned long long* reset_acc,
+                            unsigned long long* errkey_reset, cudaStream_t stream) {
+    finalize_kernel<<<1, 96, 0, stream>>>(acc, result, reset_acc, errkey_reset);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe(const NllArgs& A, int64_t j, double* out, cudaStream_t stream) {
+    probe_kernel<<<1, 1, 0, stream>>>(A, j, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream) {
+    fp64_peak_kernel<<<blocks, threads, 0, stream>>>(out, iters);
+    return cudaGetLastError();
+}
+
+}  // namespace pfb
