@@ -131,6 +131,8 @@ int pfb_ctx_destroy(pfb_ctx* ctx);
  * stream, so NCCL collectives order naturally); NULL restores the private stream. */
 int pfb_ctx_set_stream(pfb_ctx* ctx, void* cuda_stream);
 void* pfb_ctx_stream(pfb_ctx* ctx);
+/* Block until all work enqueued on the context's stream has finished. */
+int pfb_ctx_synchronize(pfb_ctx* ctx);
 /* Tuning: warps cooperating on one 4096-event block (0 = automatic; 1,2,4,8). */
 int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
 /* Number of engine kernels launched on this context since creation. */

@@ -13,8 +13,10 @@
 
 namespace pfb {
 cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
-cudaError_t launch_finalize(const long long* acc, double* result, unsigned long long* reset_acc,
-                            unsigned long long* errkey_reset, cudaStream_t stream);
+cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count);
+cudaError_t launch_export(unsigned long long* acc, long long* out, long long* result_i,
+                          unsigned long long* fix_counter, unsigned long long* errkey,
+                          cudaStream_t stream);
 cudaError_t launch_probe(const NllArgs& A, int64_t j, double* out, cudaStream_t stream);
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
 cudaError_t launch_grid_mask(const GridConsts& g, uint8_t* mask, int* row_count, cudaStream_t st);
@@ -46,7 +48,9 @@ static int cuda_fail(cudaError_t e) {
 }
 
 static constexpr int kStoreMaxCols = 16;
-static constexpr int kResultWords = 8;
+// result words: [0, 72) exported accumulator, [72] deferred-block count, [73] error key
+static constexpr int kResWords = PFB_ACC_WORDS + 2;
+enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
 struct pfb_ctx {
     int device = 0;
@@ -57,10 +61,14 @@ struct pfb_ctx {
     int warps_override = 0;
     unsigned long long* acc = nullptr;
     unsigned int* ticket = nullptr;
+    unsigned long long* work_counter = nullptr;
     unsigned long long* errkey = nullptr;
     double* tail_scratch = nullptr;
-    double* result_dev = nullptr;   // kResultWords
-    double* result_host = nullptr;  // pinned
+    long long* res_dev = nullptr;   // kResWords
+    long long* res_host = nullptr;  // pinned mirror
+    unsigned long long* fix_counter = nullptr;
+    int64_t* fix_list = nullptr;
+    int64_t fix_cap = 0;
     double* bsums = nullptr;
     int64_t bsums_cap = 0;
     double* probe_dev = nullptr;
@@ -198,12 +206,17 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
     CK(cudaMemset(c->acc, 0, sizeof(unsigned long long) * PFB_ACC_WORDS));
     CK(cudaMalloc(&c->ticket, sizeof(unsigned int)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned int)));
+    CK(cudaMalloc(&c->work_counter, sizeof(unsigned long long)));
+    CK(cudaMemset(c->work_counter, 0, sizeof(unsigned long long)));
     CK(cudaMalloc(&c->errkey, sizeof(unsigned long long)));
     CK(cudaMemset(c->errkey, 0xff, sizeof(unsigned long long)));
     CK(cudaMalloc(&c->tail_scratch, sizeof(double) * kBlock));
-    CK(cudaMalloc(&c->result_dev, sizeof(double) * kResultWords));
+    CK(cudaMalloc(&c->res_dev, sizeof(long long) * kResWords));
+    CK(cudaMemset(c->res_dev, 0, sizeof(long long) * kResWords));
+    CK(cudaMalloc(&c->fix_counter, sizeof(unsigned long long)));
+    CK(cudaMemset(c->fix_counter, 0, sizeof(unsigned long long)));
     CK(cudaMalloc(&c->probe_dev, sizeof(double) * 2));
-    CK(cudaMallocHost(&c->result_host, sizeof(double) * kResultWords));
+    CK(cudaMallocHost(&c->res_host, sizeof(long long) * kResWords));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     *out = c;
@@ -216,14 +229,17 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaFree(c->acc);
     cudaFree(c->ticket);
+    cudaFree(c->work_counter);
     cudaFree(c->errkey);
     cudaFree(c->tail_scratch);
-    cudaFree(c->result_dev);
+    cudaFree(c->res_dev);
+    cudaFree(c->fix_counter);
+    cudaFree(c->fix_list);
     cudaFree(c->probe_dev);
     cudaFree(c->bsums);
     for (auto& p : c->e2e_dev) cudaFree(p);
     for (auto& e : c->chunk_events) cudaEventDestroy(e);
-    cudaFreeHost(c->result_host);
+    cudaFreeHost(c->res_host);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);
@@ -239,6 +255,13 @@ int pfb_ctx_set_stream(pfb_ctx* c, void* s) {
 }
 
 void* pfb_ctx_stream(pfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int pfb_ctx_synchronize(pfb_ctx* c) {
+    if (!c) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    return PFB_OK;
+}
 
 int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
     if (!c || !(w == 0 || w == 1 || w == 2 || w == 4 || w == 8)) return PFB_E_INVALID_ARGUMENT;
@@ -642,22 +665,22 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     A->nfull = n / kBlock;
     A->tail = (int32_t)(n % kBlock);
     A->evaluator = p->evaluator;
-    int warps = c->warps_override;
-    if (!warps) {
-        const int64_t nb = A->nfull + (A->tail ? 1 : 0);
-        warps = 8;
-        for (int w = 1; w <= 8; w *= 2)
-            if (nb * w >= (int64_t)c->sm_count * 32) {
-                warps = w;
-                break;
-            }
-    }
+    // one 4096-event block per 8-warp group: measured fastest for every
+    // evaluator at 1M-10M events (scripts/kernel_sweep.py)
+    const int warps = c->warps_override ? c->warps_override : 8;
     A->warps = warps;
     A->acc = c->acc;
     A->ticket = c->ticket;
+    A->work_counter = c->work_counter;
     A->errkey = c->errkey;
     A->tail_scratch = c->tail_scratch;
-    A->result = c->result_dev;
+    A->acc_out = c->res_dev;
+    A->result_i = c->res_dev + PFB_ACC_WORDS;
+    A->fix_counter = c->fix_counter;
+    A->fix_list = c->fix_list;
+    A->fix_count = c->res_dev + PFB_ACC_WORDS;
+    A->block_base = 0;
+    A->mode = MODE_EXPORT;
     A->nops = (int)p->nodes.size();
     A->final_rank = p->final_rank;
     int frac_fail = -1;
@@ -902,17 +925,48 @@ static int decode_error(pfb_ctx* c, const pfb_plan* p, const NllArgs& A, unsigne
 }
 
 static int read_result(pfb_ctx* c) {
-    CK(cudaMemcpyAsync(c->result_host, c->result_dev, sizeof(double) * kResultWords,
+    CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * kResWords,
                        cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     return PFB_OK;
 }
 
-static unsigned long long as_key(double d) {
-    unsigned long long k;
-    memcpy(&k, &d, 8);
-    return k;
+static int ensure_fix(pfb_ctx* c, int64_t nblocks) {
+    if (c->fix_cap >= nblocks) return PFB_OK;
+    cudaFree(c->fix_list);
+    c->fix_list = nullptr;
+    c->fix_cap = 0;
+    CK(cudaMalloc(&c->fix_list, sizeof(int64_t) * (nblocks > 0 ? nblocks : 1)));
+    c->fix_cap = nblocks;
+    return PFB_OK;
+}
+
+// Exact fix-up of the blocks a fast launch deferred (listed on the device).
+static int launch_fixup(pfb_ctx* c, const NllArgs& A, long long* out) {
+    NllArgs F = A;
+    F.mode = MODE_ADD_EXPORT;
+    F.acc_out = out;
+    F.fix_count = c->res_dev + PFB_ACC_WORDS;
+    CK(launch_fix(F, c->stream, c->sm_count));
+    ++c->launches;
+    return PFB_OK;
+}
+
+// Host rounding of the exported accumulator words in res_host[0..72).
+static int round_result(pfb_ctx* c, double* out) {
+    double r = 0.0;
+    const int st = acc_round(c->res_host, &r);
+    if (out) *out = r;
+    return st;
+}
+
+static void clear_err(pfb_err* e) {
+    if (!e) return;
+    e->code = PFB_OK;
+    e->node = -1;
+    e->index = -1;
+    e->value = NAN;
 }
 
 static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin,
@@ -926,12 +980,7 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
     if (begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
     for (int s = 0; s < p->nslots; ++s)
         if (p->slot_col[s] >= st->ncols) return PFB_E_INVALID_ARGUMENT;
-    if (out_err) {
-        out_err->code = PFB_OK;
-        out_err->node = -1;
-        out_err->index = -1;
-        out_err->value = NAN;
-    }
+    clear_err(out_err);
     if (end == begin) {
         if (out_err) out_err->code = PFB_E_EMPTY_DATASET;
         return PFB_E_EMPTY_DATASET;
@@ -946,9 +995,11 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
         end -= begin;
         begin = 0;
     }
+    const int64_t nb = (end - begin + kBlock - 1) / kBlock;
+    int rc = ensure_fix(c, nb);
+    if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
     const int frac = pack_args(p, st, begin, end, values, norms, A.get());
-    const int64_t nb = A->nfull + (A->tail ? 1 : 0);
     if (block_sums_host) {
         if (n_out < nb) return PFB_E_INVALID_ARGUMENT;
         if (c->bsums_cap < nb) {
@@ -959,18 +1010,24 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
         }
         A->block_sums = c->bsums;
     }
-    A->mode = 0;
-    int rc = launch_eval(p, st, begin, end, A.get(), !restaged);
+    rc = launch_eval(p, st, begin, end, A.get(), !restaged);
     if (rc) return rc;
     rc = read_result(c);
     if (rc) return rc;
-    const unsigned long long key = as_key(c->result_host[2]);
+    if (c->res_host[PFB_ACC_WORDS] > 0) {  // deferred blocks: exact fix-up
+        rc = launch_fixup(c, *A, c->res_dev);
+        if (rc) return rc;
+        const float fast_ms = c->last_ms;
+        rc = read_result(c);
+        if (rc) return rc;
+        c->last_ms = fast_ms;
+    }
+    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
     const int code = decode_error(c, p, *A, key, frac, index_offset, out_err);
     if (code) return code;
     if (block_sums_host)
         CK(cudaMemcpy(block_sums_host, c->bsums, sizeof(double) * nb, cudaMemcpyDeviceToHost));
-    const int st_round = (int)c->result_host[3];
-    if (out_nll) *out_nll = c->result_host[0];
+    const int st_round = round_result(c, out_nll);
     if (st_round && out_err) out_err->code = st_round;
     return st_round;
 }
@@ -1011,6 +1068,8 @@ int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, i
         end -= begin;
         begin = 0;
     }
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
+    if (rc) return rc;
     c->last_args.reset(new NllArgs());
     NllArgs* A = c->last_args.get();
     c->last_frac_rank = pack_args(p, st, begin, end, values, norms, A);
@@ -1018,25 +1077,28 @@ int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, i
     c->last_index_offset = index_offset;
     if (end == begin) {  // empty shard: a zero partial (sharding.partial_nll, sharding.py:110-111)
         CK(cudaMemsetAsync(dev_acc, 0, sizeof(int64_t) * PFB_ACC_WORDS, c->stream));
-        CK(cudaMemsetAsync(c->result_dev + 1, 0, sizeof(double), c->stream));
-        CK(cudaMemsetAsync(c->result_dev + 2, 0xff, sizeof(double), c->stream));
+        CK(cudaMemsetAsync(c->res_dev + PFB_ACC_WORDS, 0, sizeof(long long), c->stream));
+        CK(cudaMemsetAsync(c->res_dev + PFB_ACC_WORDS + 1, 0xff, sizeof(long long), c->stream));
         return PFB_OK;
     }
-    A->mode = 1;
     A->acc_out = (long long*)dev_acc;
-    return launch_eval(p, st, begin, end, A, !restaged);
+    rc = launch_eval(p, st, begin, end, A, !restaged);
+    if (rc) return rc;
+    // no host round trip: the fix-up launch reads the deferred count on the device
+    return launch_fixup(c, *A, (long long*)dev_acc);
 }
 
 int pfb_finalize(pfb_ctx* c, const int64_t* dev_acc, double* out_nll, int64_t* out_fails) {
     if (!c || !dev_acc) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
-    CK(launch_finalize((const long long*)dev_acc, c->result_dev + 4, nullptr, nullptr, c->stream));
-    ++c->launches;
-    int rc = read_result(c);
-    if (rc) return rc;
-    if (out_nll) *out_nll = c->result_host[4];
-    if (out_fails) *out_fails = (int64_t)c->result_host[5];
-    return (int)c->result_host[7];
+    long long h[PFB_ACC_WORDS];
+    CK(cudaMemcpyAsync(h, dev_acc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double r = 0.0;
+    const int st = acc_round(h, &r);
+    if (out_nll) *out_nll = r;
+    if (out_fails) *out_fails = (int64_t)h[PFB_ACC_FAILS];
+    return st;
 }
 
 int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
@@ -1044,7 +1106,7 @@ int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
     CK(cudaSetDevice(c->device));
     int rc = read_result(c);
     if (rc) return rc;
-    const unsigned long long key = as_key(c->result_host[2]);
+    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
     decode_error(c, c->last_plan, *c->last_args, key, c->last_frac_rank, c->last_index_offset,
                  out_err);
     return PFB_OK;
@@ -1059,12 +1121,7 @@ int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols,
     if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
     for (int s = 0; s < p->nslots; ++s)
         if (p->slot_col[s] >= ncols) return PFB_E_INVALID_ARGUMENT;
-    if (out_err) {
-        out_err->code = PFB_OK;
-        out_err->node = -1;
-        out_err->index = -1;
-        out_err->value = NAN;
-    }
+    clear_err(out_err);
     if (n == 0) {
         if (out_err) out_err->code = PFB_E_EMPTY_DATASET;
         return PFB_E_EMPTY_DATASET;
@@ -1079,6 +1136,8 @@ int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols,
         for (int i = 0; i < kMaxCols; ++i) CK(cudaMalloc(&c->e2e_dev[i], sizeof(double) * padded));
         c->e2e_cap = n;
     }
+    int rc = ensure_fix(c, (n + kBlock - 1) / kBlock);
+    if (rc) return rc;
     pfb_store st;
     st.ctx = c;
     st.ncols = ncols;
@@ -1111,20 +1170,26 @@ int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols,
         auto A = std::make_unique<NllArgs>();
         pack_args(p, &st, b, e, values, norms, A.get());
         A->idx_base = b;
-        A->mode = 2;
-        int rc = launch_eval(p, &st, b, e, A.get(), /*allow_cache=*/false);
+        A->block_base = b / kBlock;
+        A->mode = MODE_ACCUM;
+        rc = launch_eval(p, &st, b, e, A.get(), /*allow_cache=*/false);
         if (rc) return rc;
     }
-    CK(launch_finalize((const long long*)c->acc, c->result_dev, c->acc, c->errkey, c->stream));
+    CK(launch_export(c->acc, c->res_dev, c->res_dev + PFB_ACC_WORDS, c->fix_counter, c->errkey,
+                     c->stream));
     ++c->launches;
-    int rc = read_result(c);
+    rc = read_result(c);
     if (rc) return rc;
-    const unsigned long long key = as_key(c->result_host[2]);
-    A0.idx_base = 0;
+    if (c->res_host[PFB_ACC_WORDS] > 0) {
+        rc = launch_fixup(c, A0, c->res_dev);
+        if (rc) return rc;
+        rc = read_result(c);
+        if (rc) return rc;
+    }
+    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
     const int code = decode_error(c, p, A0, key, frac, 0, out_err);
     if (code) return code;
-    const int st_round = (int)c->result_host[3];
-    if (out_nll) *out_nll = c->result_host[0];
+    const int st_round = round_result(c, out_nll);
     if (st_round && out_err) out_err->code = st_round;
     return st_round;
 }
@@ -1143,6 +1208,9 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     std::unique_ptr<pfb_store, int (*)(pfb_store*)> guard(st, pfb_store_destroy);
     rc = pfb_store_upload(st, 0, host_terms, 0, n);
     if (rc) return rc;
+    const int64_t nb = (n + kBlock - 1) / kBlock;
+    rc = ensure_fix(c, nb);
+    if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
     memset(A.get(), 0, sizeof(NllArgs));
     A->col[0] = st->cols[0];
@@ -1152,22 +1220,18 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->nfull = n / kBlock;
     A->tail = (int32_t)(n % kBlock);
     A->evaluator = 100;
-    const int64_t nb = A->nfull + (A->tail ? 1 : 0);
-    int warps = c->warps_override;
-    if (!warps) {
-        warps = 8;
-        for (int w = 1; w <= 8; w *= 2)
-            if (nb * w >= (int64_t)c->sm_count * 32) {
-                warps = w;
-                break;
-            }
-    }
+    const int warps = c->warps_override ? c->warps_override : 8;
     A->warps = warps;
     A->acc = c->acc;
     A->ticket = c->ticket;
+    A->work_counter = c->work_counter;
     A->errkey = c->errkey;
     A->tail_scratch = c->tail_scratch;
-    A->result = c->result_dev;
+    A->acc_out = c->res_dev;
+    A->result_i = c->res_dev + PFB_ACC_WORDS;
+    A->fix_counter = c->fix_counter;
+    A->fix_list = c->fix_list;
+    A->mode = MODE_EXPORT;
     if (c->bsums_cap < nb) {
         cudaFree(c->bsums);
         c->bsums = nullptr;
@@ -1175,15 +1239,15 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
         c->bsums_cap = nb;
     }
     A->block_sums = c->bsums;
-    A->mode = 0;
+    if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
     CK(launch_nll(*A, c->stream, c->sm_count, 1));
     ++c->launches;
+    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
     rc = read_result(c);
     if (rc) return rc;
     if (out_block_sums)
         CK(cudaMemcpy(out_block_sums, c->bsums, sizeof(double) * nb, cudaMemcpyDeviceToHost));
-    if (out_total) *out_total = c->result_host[0];
-    return (int)c->result_host[3];
+    return round_result(c, out_total);
 }
 
 int pfb_exact_sum_host(const double* v, int64_t n, double* out) {

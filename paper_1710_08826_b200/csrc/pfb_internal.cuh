@@ -102,15 +102,20 @@ struct NllArgs {
     int32_t tail;             // events in the trailing partial block
     int32_t evaluator;
     int32_t warps;            // warps cooperating on one block (1,2,4,8)
-    int32_t mode;             // 0: finalize in last CTA; 1: export accumulator; 2: keep accumulating
+    int32_t mode;             // KernelMode: export / add-export / accumulate
     int64_t idx_base;         // added to local event indices in error keys
-    double* block_sums;       // optional per-block output
+    int64_t block_base;       // global block index of this range's block 0
+    double* block_sums;       // optional per-block output (indexed block_base + b)
     unsigned long long* acc;  // PFB_ACC_WORDS persistent accumulator (self-resetting)
     unsigned int* ticket;     // CTA completion counter (self-resetting)
+    unsigned long long* work_counter;  // dynamic block scheduler (self-resetting)
     unsigned long long* errkey;  // min (rank<<40 | local index), ~0 when clean
     double* tail_scratch;     // 4096 doubles
-    double* result;           // [0] nll, [1] fails (as double), [2] err key (bits)
-    long long* acc_out;       // mode 1 destination
+    long long* acc_out;       // PFB_ACC_WORDS export target
+    long long* result_i;      // [0] deferred-block count, [1] error key
+    unsigned long long* fix_counter;  // deferred-block list fill (self-resetting)
+    int64_t* fix_list;        // deferred global block indices
+    const long long* fix_count;       // list length for the fix-up launch (device)
     // literal interpreter
     int32_t nops;
     int32_t final_rank;       // rank of the root p > 0 check

@@ -1,6 +1,6 @@
 // pfb_nll.cu -- generic instantiations (literal interpreter, reduction
-// known-answer mode), the rounding kernel, the error probe, the FP64 peak
-// microbenchmark and the evaluator dispatch.
+// known-answer mode, the list-driven fix-up launch), the accumulator export,
+// the error probe, the FP64 peak microbenchmark and the evaluator dispatch.
 #include "pfb_nll_kernel.cuh"
 
 namespace pfb {
@@ -8,25 +8,15 @@ namespace pfb {
 cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count);
 
-// Rounds an accumulator already resident on the device (after an allreduce,
-// or after a chain of mode-2 launches).  One warp; thread 0 does the rounding.
-__global__ void finalize_kernel(const long long* acc, double* result, unsigned long long* reset_acc,
-                                unsigned long long* errkey_reset) {
-    __shared__ long long s[PFB_ACC_WORDS];
-    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) s[i] = acc[i];
-    __syncthreads();
-    if (reset_acc)
-        for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) reset_acc[i] = 0ull;
+// Export a chained accumulator (after MODE_ACCUM launches): out = acc, reset;
+// deferred-block count and error key to result_i.
+__global__ void export_kernel(unsigned long long* acc, long long* out, long long* result_i,
+                              unsigned long long* fix_counter, unsigned long long* errkey) {
+    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x)
+        out[i] = (long long)atomicExch(acc + i, 0ull);
     if (threadIdx.x == 0) {
-        double r;
-        const int st = acc_round_dev(s, &r);
-        result[0] = r;
-        result[1] = (double)s[PFB_ACC_FAILS];
-        if (errkey_reset) {
-            result[2] = __longlong_as_double((long long)*errkey_reset);
-            *errkey_reset = ~0ull;
-        }
-        result[3] = (double)st;
+        result_i[0] = (long long)atomicExch(fix_counter, 0ull);
+        result_i[1] = (long long)atomicExch(errkey, ~0ull);
     }
 }
 
@@ -60,7 +50,6 @@ __global__ void fp64_peak_kernel(double* out, int iters) {
     if (s == 12345.0) out[0] = s;
 }
 
-
 cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
     switch (A.evaluator) {
         case EV_SOP:
@@ -75,9 +64,17 @@ cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int 
     }
 }
 
-cudaError_t launch_finalize(const long long* acc, double* result, unsigned long long* reset_acc,
-                            unsigned long long* errkey_reset, cudaStream_t stream) {
-    finalize_kernel<<<1, 96, 0, stream>>>(acc, result, reset_acc, errkey_reset);
+// Exact recomputation of the deferred blocks listed by a fast launch.
+cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    NllArgs F = A;
+    F.warps = 8;
+    return launch_p<EvLiteral<1>, true>(F, stream, sm_count);
+}
+
+cudaError_t launch_export(unsigned long long* acc, long long* out, long long* result_i,
+                          unsigned long long* fix_counter, unsigned long long* errkey,
+                          cudaStream_t stream) {
+    export_kernel<<<1, 96, 0, stream>>>(acc, out, result_i, fix_counter, errkey);
     return cudaGetLastError();
 }
 

@@ -169,7 +169,7 @@ struct EvTerms {
     static constexpr int NC = 1;
     static constexpr int U = 8;
     __device__ static __forceinline__ double2 eval2(const NllArgs&, const double2 (&x)[1], int64_t,
-                                                    long long*, int) {
+                                                    long long*, int, bool&) {
         return x[0];
     }
 };
@@ -180,7 +180,7 @@ struct EvLiteral {
     static constexpr int NC = NC_;
     static constexpr int U = 1;
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&)[NC_],
-                                                    int64_t local, long long* sacc, int nvalid) {
+                                                    int64_t local, long long* sacc, int nvalid, bool&) {
         double2 t;
         t.x = literal_or_fail(A, local, sacc);
         t.y = nvalid > 1 ? literal_or_fail(A, local + 1, sacc) : 0.0;
@@ -194,10 +194,21 @@ struct EvLiteral {
 // Guard: every exponent |u| <= 600 and every term's log-magnitude budget below
 // its host-computed threshold => the reference computation has no underflow,
 // overflow, non-finite or non-positive value, so both agree to rounding.
-template <int NC_>
+// NL / NT are the leaf and term counts when EXACT (a shape-specialised
+// instantiation), else upper bounds checked against the plan at run time.
+// KINDS (optional) fixes the leaf kinds at compile time, 2 bits per leaf
+// (1 gaussian, 2 exponential, 3 polynomial).
+template <int NC_, int NL = kMaxLeaves, int NT = kMaxTerms, bool EXACT = false, int KINDS = 0>
 struct EvSop {
     static constexpr int NC = NC_;
     static constexpr int U = 4;
+
+    __device__ static __forceinline__ constexpr bool has_value_leaf() {
+        if (KINDS == 0) return true;
+        for (int l = 0; l < NL; ++l)
+            if (((KINDS >> (2 * l)) & 3) == PFB_POLYNOMIAL) return true;
+        return false;
+    }
 
     __device__ static __forceinline__ double pick(const double2 (&x)[NC_], int col, int which) {
         double r = which ? x[0].y : x[0].x;
@@ -209,24 +220,25 @@ struct EvSop {
 
     __device__ static __forceinline__ double one(const NllArgs& A, const double2 (&x)[NC_],
                                                  int which, bool* ok) {
-        double u[kMaxLeaves];
-        double lv[kMaxLeaves];  // |log2| budget of value leaves
+        double u[NL];
+        double lv[NL];  // |log| budget of value leaves
         bool good = true;
 #pragma unroll
-        for (int l = 0; l < kMaxLeaves; ++l) {
+        for (int l = 0; l < NL; ++l) {
             u[l] = 0.0;
             lv[l] = 0.0;
-            if (l < A.nleaf) {
+            if (EXACT || l < A.nleaf) {
                 const SopLeaf& L = A.leaf[l];
                 const double xv = pick(x, L.col, which);
-                if (L.kind == PFB_GAUSSIAN) {
+                const int kind = KINDS ? ((KINDS >> (2 * l)) & 3) : L.kind;
+                if (kind == PFB_GAUSSIAN) {
                     const double z = (xv - A.v[L.voff]) * A.v[L.voff + 1];
                     u[l] = -0.5 * z * z;
                     good &= (u[l] >= -600.0) || (u[l] < -746.0);
-                } else if (L.kind == PFB_EXPONENTIAL) {
+                } else if (kind == PFB_EXPONENTIAL) {
                     u[l] = A.v[L.voff] * xv;
                     good &= (fabs(u[l]) <= 600.0) || (u[l] < -746.0);
-                } else {  // polynomial value (Horner, as np.polynomial.polynomial.polyval)
+                } else if (has_value_leaf()) {  // polynomial (Horner, as polyval)
                     const double* c = A.v + L.voff;
                     double acc = c[L.nv - 1];
                     for (int i = 2; i <= L.nv; ++i) acc = fma(acc, xv, c[L.nv - i]);
@@ -237,25 +249,25 @@ struct EvSop {
                 }
             }
         }
-        double L0 = 0.0, V0 = 1.0, Lm = -1e300, s = 0.0;
+        double Lm = -1e300, s = 0.0;
         bool live = false;
-        double Lt[kMaxTerms], Vt[kMaxTerms];
+        double Lt[NT], Vt[NT];
 #pragma unroll
-        for (int t = 0; t < kMaxTerms; ++t) {
+        for (int t = 0; t < NT; ++t) {
             Lt[t] = -1e300;
             Vt[t] = 1.0;
-            if (t < A.nterm) {
+            if (EXACT || t < A.nterm) {
                 const SopTerm& T = A.term[t];
                 double lsum = T.logcoef, budget = 0.0, vprod = 1.0;
                 bool dead = false;  // a leaf underflows to exactly 0 in the reference
 #pragma unroll
-                for (int l = 0; l < kMaxLeaves; ++l) {
+                for (int l = 0; l < NL; ++l) {
                     if ((T.emask >> l) & 1u) {
                         lsum += u[l];
                         budget += fabs(u[l]);
                         dead |= (u[l] < -746.0);
                     }
-                    if ((T.vmask >> l) & 1u) {
+                    if (has_value_leaf() && ((T.vmask >> l) & 1u)) {
                         vprod *= u[l];
                         budget += lv[l];
                     }
@@ -268,31 +280,29 @@ struct EvSop {
             }
         }
         *ok = good && live;
-        if (A.nterm == 1) {
-            L0 = Lt[0];
-            V0 = Vt[0];
-            return (A.term[0].vmask ? -(L0 + log(V0)) : -L0);
+        if (NT == 1 || (!EXACT && A.nterm == 1)) {
+            if (!has_value_leaf()) return -Lt[0];
+            return (A.term[0].vmask ? -(Lt[0] + log(Vt[0])) : -Lt[0]);
         }
-        if (A.nterm == 2) {
+        if (NT == 2 || (!EXACT && A.nterm == 2)) {
             const double d = Lt[0] - Lt[1];
             const double e = exp(-fabs(d));
             s = d >= 0.0 ? fma(Vt[1], e, Vt[0]) : fma(Vt[0], e, Vt[1]);
             return -(fmax(Lt[0], Lt[1]) + log(s));
         }
 #pragma unroll
-        for (int t = 0; t < kMaxTerms; ++t)
-            if (t < A.nterm) s = fma(Vt[t], exp(Lt[t] - Lm), s);
+        for (int t = 0; t < NT; ++t)
+            if (EXACT || t < A.nterm) s = fma(Vt[t], exp(Lt[t] - Lm), s);
         return -(Lm + log(s));
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[NC_],
-                                                    int64_t local, long long* sacc, int nvalid) {
+                                                    int64_t, long long*, int nvalid, bool& bad) {
         bool ok0, ok1;
         double2 t;
         t.x = one(A, x, 0, &ok0);
         t.y = one(A, x, 1, &ok1);
-        if (!ok0) t.x = literal_or_fail(A, local, sacc);
-        if (!ok1 && nvalid > 1) t.y = literal_or_fail(A, local + 1, sacc);
+        bad |= !ok0 || (nvalid > 1 && !ok1);
         return t;
     }
 };
@@ -384,13 +394,12 @@ struct EvDalitz {
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
-                                                    int64_t local, long long* sacc, int nvalid) {
+                                                    int64_t, long long*, int nvalid, bool& bad) {
         bool ok0, ok1;
         double2 t;
         t.x = one(A, x[0].x, x[1].x, &ok0);
         t.y = one(A, x[0].y, x[1].y, &ok1);
-        if (!ok0) t.x = literal_or_fail(A, local, sacc);
-        if (!ok1 && nvalid > 1) t.y = literal_or_fail(A, local + 1, sacc);
+        bad |= !ok0 || (nvalid > 1 && !ok1);
         return t;
     }
 };
@@ -441,13 +450,12 @@ struct EvDalitzCached {
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
-                                                    int64_t local, long long* sacc, int nvalid) {
+                                                    int64_t local, long long*, int nvalid, bool& bad) {
         bool ok0, ok1;
         double2 t;
         t.x = one(A, x[0].x, x[1].x, local, &ok0);
         t.y = one(A, x[0].y, x[1].y, local + 1, &ok1);
-        if (!ok0) t.x = literal_or_fail(A, local, sacc);
-        if (!ok1 && nvalid > 1) t.y = literal_or_fail(A, local + 1, sacc);
+        bad |= !ok0 || (nvalid > 1 && !ok1);
         return t;
     }
 };
@@ -468,8 +476,13 @@ static __device__ __noinline__ double pairwise_serial(const double* a, int n) {
     while (sp >= 0) {
         Frame& f = st[sp];
         if (f.len <= 8) {
-            double s = a[f.start];
-            for (int k = 1; k < f.len; ++k) s = Add(s, a[f.start + k]);
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = k < f.len ? a[f.start + k] : 0.0;
+            double s = v[0];
+#pragma unroll
+            for (int k = 1; k < 8; ++k)
+                if (k < f.len) s = Add(s, v[k]);
             ret = s;
             --sp;
             continue;
@@ -520,12 +533,28 @@ static __device__ __noinline__ double pairwise_warp(const double* a, int n, int 
     return __shfl_sync(0xffffffffu, v, 0);
 }
 
+// Named barrier of one warp group.  Immediate barrier ids, so ptxas reserves
+// only GROUPS+1 of the SM's hardware barriers (a register id reserves all 16
+// and caps the CTAs per SM).
 template <int P>
 __device__ __forceinline__ void group_sync(int grp) {
+    constexpr int n = P * 32;
     if (P == 1) {
         __syncwarp();
+    } else if (P == 8) {
+        asm volatile("bar.sync 1, %0;" ::"n"(n) : "memory");
+    } else if (P == 4) {
+        if (grp == 0)
+            asm volatile("bar.sync 1, %0;" ::"n"(n) : "memory");
+        else
+            asm volatile("bar.sync 2, %0;" ::"n"(n) : "memory");
     } else {
-        asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(P * 32) : "memory");
+        switch (grp) {
+            case 0: asm volatile("bar.sync 1, %0;" ::"n"(n) : "memory"); break;
+            case 1: asm volatile("bar.sync 2, %0;" ::"n"(n) : "memory"); break;
+            case 2: asm volatile("bar.sync 3, %0;" ::"n"(n) : "memory"); break;
+            default: asm volatile("bar.sync 4, %0;" ::"n"(n) : "memory"); break;
+        }
     }
 }
 
@@ -559,23 +588,30 @@ __device__ __forceinline__ void acc_add_shared(long long* sacc, double x) {
                       (unsigned long long)d.d[i]);
 }
 
-// Rounding runs once per launch in one thread: keep its 68-limb working set
-// out of the kernel's register allocation.
-static __device__ __noinline__ int acc_round_dev(const long long* acc, double* out) {
-    return acc_round(acc, out);
-}
-
 // ---------------------------------------------------------------------------
-template <int P, class Ev>
+// Kernel modes.  The fast kernel never takes the literal path: a block that
+// contains an event its evaluator cannot certify is left out of the
+// accumulator and listed; the fix-up launch (LIST = true, literal evaluator)
+// recomputes exactly those blocks -- reporting the reference's errors -- and
+// adds them.  Integer accumulation makes "fast blocks + fixed blocks" exact.
+enum KernelMode : int32_t {
+    MODE_EXPORT = 0,      // last CTA: out = acc, reset; counters -> result
+    MODE_ADD_EXPORT = 1,  // last CTA: out += acc, reset (fix-up after a fast launch)
+    MODE_ACCUM = 2        // chained launches: keep accumulating
+};
+
+template <int P, class Ev, bool LIST>
 __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant__ NllArgs A) {
     constexpr int NC = Ev::NC;
     constexpr int GROUPS = kThreads / (32 * P);
     constexpr int KPT = 64 / P;                       // double2 slots per thread per block
-    constexpr int U = Ev::U < KPT ? Ev::U : KPT;      // slots per streamed chunk
-    constexpr int G = KPT / U;                        // chunks
-    constexpr int LG = Log2<G>::value;
+    constexpr int W = Ev::U < KPT ? Ev::U : KPT;      // slot loads kept in flight
+    constexpr int LK = Log2<KPT>::value;
 
     __shared__ double2 xch[GROUPS][P][32];
+    __shared__ int xbad[GROUPS][P];
+    __shared__ long long s_item[GROUPS];
+    __shared__ double s_tail[kBlock];  // ragged-tail terms (one per launch)
     __shared__ long long sacc[PFB_ACC_WORDS];
     __shared__ unsigned int s_last;
 
@@ -587,14 +623,29 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
     __syncthreads();
 
-    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
-    for (int64_t it = (int64_t)blockIdx.x * GROUPS + grp; it < nitems;
-         it += (int64_t)gridDim.x * GROUPS) {
+    const int64_t nitems = LIST ? (int64_t)(*A.fix_count) : A.nfull + (A.tail ? 1 : 0);
+    // Dynamic item scheduling: groups pull the next block from a global
+    // counter, so fast SMs take more blocks and no SM idles in a last round.
+    // Item 0 is the ragged tail (if any), pulled first.
+    for (;;) {
+        if (wig == 0 && lane == 0) s_item[grp] = (long long)atomicAdd(A.work_counter, 1ull);
+        group_sync<P>(grp);
+        const int64_t it = s_item[grp];
+        group_sync<P>(grp);
+        if (it >= nitems) break;
         double bsum = 0.0;
         int64_t bidx;
-        if (A.tail && it == 0) {
+        bool is_tail;
+        if (LIST) {
+            bidx = A.fix_list[it] - A.block_base;
+            is_tail = A.tail && bidx == A.nfull;
+        } else {
+            is_tail = A.tail && it == 0;
+            bidx = is_tail ? A.nfull : it - (A.tail ? 1 : 0);
+        }
+        bool bad = false;
+        if (is_tail) {
             // ---- ragged tail block: terms to scratch, then split recursion
-            bidx = A.nfull;
             const int64_t lbase = A.nfull * (int64_t)kBlock;  // local index of tail start
             const int n = A.tail;
 #pragma unroll 1
@@ -606,78 +657,92 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
                     const double* p = A.col[c] + A.begin + lbase + e;
                     x[c] = pair ? ld2(p) : make_double2(__ldg(p), __ldg(p));
                 }
-                const double2 t = Ev::eval2(A, x, lbase + e, sacc, pair ? 2 : 1);
-                A.tail_scratch[e] = t.x;
-                if (pair) A.tail_scratch[e + 1] = t.y;
+                const double2 t = Ev::eval2(A, x, lbase + e, sacc, pair ? 2 : 1, bad);
+                s_tail[e] = t.x;
+                if (pair) s_tail[e + 1] = t.y;
             }
-            __threadfence_block();
+            const unsigned anybad = __any_sync(0xffffffffu, bad);
+            if (lane == 0) xbad[grp][wig] = anybad ? 1 : 0;
             group_sync<P>(grp);
-            if (wig == 0) bsum = pairwise_warp(A.tail_scratch, n, lane);
+            bad = false;
+#pragma unroll
+            for (int w = 0; w < P; ++w) bad |= xbad[grp][w] != 0;
+            if (wig == 0 && !bad) bsum = pairwise_warp(s_tail, n, lane);
             group_sync<P>(grp);
         } else {
             // ---- full block, reference half-folding tree
-            bidx = it - (A.tail ? 1 : 0);
             const int64_t lbase = bidx * (int64_t)kBlock;
             const int64_t lthr = lbase + 2 * lane + 64 * wig;
-            double2 lvl[LG > 0 ? LG : 1];
+            // Sliding window: slots are visited in the streaming order
+            // i = 0..KPT-1 (slot k = bitrev(i)), W loads stay in flight, and
+            // a binary counter over i reproduces the half-folding tree (the
+            // tree over i pairs adjacent i first).  One eval2 per kernel body
+            // keeps the code inside the instruction cache.
+            double2 win[W][NC];
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+                const int k = LK ? (int)(__brev((unsigned)q) >> (32 - LK)) : 0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) win[q][c] = ld2(A.col[c] + A.begin + lthr + 64 * P * k);
+            }
+            double2 lvl[LK > 0 ? LK : 1];
             double2 T = make_double2(0.0, 0.0);
 #pragma unroll 1
-            for (int g = 0; g < G; ++g) {
-                const int cidx = LG ? (int)(__brev((unsigned)g) >> (32 - LG)) : 0;
-                double2 x[U][NC];
+            for (int i = 0; i < KPT; ++i) {
+                const int k = LK ? (int)(__brev((unsigned)i) >> (32 - LK)) : 0;
+                double2 cur[NC];
 #pragma unroll
-                for (int q = 0; q < U; ++q) {
-                    const int64_t off = lthr + 64 * P * (int64_t)(cidx + G * q);
+                for (int c = 0; c < NC; ++c) cur[c] = win[0][c];
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) x[q][c] = ld2(A.col[c] + A.begin + off);
+                for (int q = 0; q + 1 < W; ++q)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) win[q][c] = win[q + 1][c];
+                if (i + W < KPT) {
+                    const int kn = (int)(__brev((unsigned)(i + W)) >> (32 - LK));
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        win[W - 1][c] = ld2(A.col[c] + A.begin + lthr + 64 * P * kn);
                 }
-                double2 t[U];
+                double2 v = Ev::eval2(A, cur, lthr + 64 * P * (int64_t)k, sacc, 2, bad);
 #pragma unroll
-                for (int q = 0; q < U; ++q)
-                    t[q] = Ev::eval2(A, x[q], lthr + 64 * P * (int64_t)(cidx + G * q), sacc, 2);
-#pragma unroll
-                for (int h = U / 2; h >= 1; h /= 2) {
-#pragma unroll
-                    for (int q = 0; q < h; ++q) {
-                        t[q].x = Add(t[q].x, t[q + h].x);
-                        t[q].y = Add(t[q].y, t[q + h].y);
-                    }
-                }
-                // binary counter over chunks: chunk g is the right sibling at
-                // every level b where bit b of g is set
-                double2 c = t[0];
-#pragma unroll
-                for (int b = 0; b < LG; ++b) {
-                    if ((g >> b) & 1) {
-                        c.x = Add(lvl[b].x, c.x);
-                        c.y = Add(lvl[b].y, c.y);
+                for (int b = 0; b < LK; ++b) {
+                    if ((i >> b) & 1) {
+                        v.x = Add(lvl[b].x, v.x);
+                        v.y = Add(lvl[b].y, v.y);
                     } else {
-                        lvl[b] = c;
+                        lvl[b] = v;
                         break;
                     }
                 }
-                T = c;  // meaningful after the last chunk (g = G-1: all bits set)
+                T = v;  // the root after the last slot (i = KPT-1: all bits set)
             }
+            const unsigned anybad = __any_sync(0xffffffffu, bad);
             if (P > 1) {
                 xch[grp][wig][lane] = T;
+                if (lane == 0) xbad[grp][wig] = anybad ? 1 : 0;
                 group_sync<P>(grp);
-                if (wig == 0) {
-                    double2 W[P];
+                bad = false;
 #pragma unroll
-                    for (int w = 0; w < P; ++w) W[w] = xch[grp][w][lane];
+                for (int w = 0; w < P; ++w) bad |= xbad[grp][w] != 0;
+                if (wig == 0 && !bad) {
+                    double2 Wv[P];
+#pragma unroll
+                    for (int w = 0; w < P; ++w) Wv[w] = xch[grp][w][lane];
 #pragma unroll
                     for (int h = P / 2; h >= 1; h /= 2) {
 #pragma unroll
                         for (int w = 0; w < h; ++w) {
-                            W[w].x = Add(W[w].x, W[w + h].x);
-                            W[w].y = Add(W[w].y, W[w + h].y);
+                            Wv[w].x = Add(Wv[w].x, Wv[w + h].x);
+                            Wv[w].y = Add(Wv[w].y, Wv[w + h].y);
                         }
                     }
-                    T = W[0];
+                    T = Wv[0];
                 }
                 group_sync<P>(grp);
+            } else {
+                bad = anybad != 0;
             }
-            if (wig == 0) {
+            if (wig == 0 && !bad) {
 #pragma unroll
                 for (int off = 16; off >= 1; off /= 2) {
                     T.x = Add(T.x, __shfl_down_sync(0xffffffffu, T.x, off));
@@ -687,12 +752,17 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
             }
         }
         if (wig == 0 && lane == 0) {
-            if (A.block_sums) A.block_sums[bidx] = bsum;
-            acc_add_shared(sacc, bsum);
+            if (bad) {  // defer the whole block to the exact fix-up launch
+                const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
+                A.fix_list[slot] = A.block_base + bidx;
+            } else {
+                if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
+                acc_add_shared(sacc, bsum);
+            }
         }
     }
 
-    // ---- flush the CTA accumulator, last CTA finalises --------------------
+    // ---- flush the CTA accumulator; the last CTA exports and resets ----------
     __syncthreads();
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x)
         if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
@@ -701,60 +771,64 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
     if (tid == 0) s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!s_last) return;
-    if (A.mode == 2) {  // chained launches: the accumulator and error key stay put
+    if (tid == 0) *A.work_counter = 0ull;
+    if (A.mode == MODE_ACCUM) {
         if (tid == 0) *A.ticket = 0u;
         return;
     }
     __threadfence();
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) {
-        sacc[i] = (long long)atomicExch(A.acc + i, 0ull);
-        if (A.mode == 1) A.acc_out[i] = sacc[i];
+        const long long v = (long long)atomicExch(A.acc + i, 0ull);
+        if (A.mode == MODE_EXPORT)
+            A.acc_out[i] = v;
+        else
+            A.acc_out[i] += v;
     }
-    __syncthreads();
     if (tid == 0) {
-        const unsigned long long key = atomicExch(A.errkey, ~0ull);
         *A.ticket = 0u;
-        A.result[1] = (double)sacc[PFB_ACC_FAILS];
-        A.result[2] = __longlong_as_double((long long)key);
-        if (A.mode == 0) {
-            double r;
-            const int st = acc_round_dev(sacc, &r);
-            A.result[0] = r;
-            A.result[3] = (double)st;
+        if (!LIST) {  // hand the deferred-block count to the fix-up launch
+            A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
         }
+        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
     }
 }
 
 // ---------------------------------------------------------------------------
-// Host-side launch of one instantiation (grid = min(work, resident capacity)).
-template <int P, class Ev>
+// Host-side launch of one instantiation.  Grid: one resident wave (workers
+// pull blocks from the device counter).
+template <int P, class Ev, bool LIST>
 static cudaError_t launch_one(const NllArgs& A, cudaStream_t stream, int sm_count) {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nll_kernel<P, Ev>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nll_kernel<P, Ev, LIST>, kThreads, 0);
         if (occ < 1) occ = 1;
     }
     constexpr int GROUPS = kThreads / (32 * P);
-    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
-    int64_t grid = (nitems + GROUPS - 1) / GROUPS;
+    int64_t grid;
     const int64_t cap = (int64_t)sm_count * occ;
-    if (grid > cap) grid = cap;
+    if (LIST) {
+        grid = sm_count;  // item count lives on the device
+    } else {
+        const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+        grid = (nitems + GROUPS - 1) / GROUPS;
+        if (grid > cap) grid = cap;  // resident workers pull items dynamically
+    }
     if (grid < 1) grid = 1;
-    nll_kernel<P, Ev><<<(unsigned)grid, kThreads, 0, stream>>>(A);
+    nll_kernel<P, Ev, LIST><<<(unsigned)grid, kThreads, 0, stream>>>(A);
     return cudaGetLastError();
 }
 
-template <class Ev>
+template <class Ev, bool LIST = false>
 static cudaError_t launch_p(const NllArgs& A, cudaStream_t stream, int sm_count) {
     switch (A.warps) {
         case 1:
-            return launch_one<1, Ev>(A, stream, sm_count);
+            return launch_one<1, Ev, LIST>(A, stream, sm_count);
         case 2:
-            return launch_one<2, Ev>(A, stream, sm_count);
+            return launch_one<2, Ev, LIST>(A, stream, sm_count);
         case 4:
-            return launch_one<4, Ev>(A, stream, sm_count);
+            return launch_one<4, Ev, LIST>(A, stream, sm_count);
         default:
-            return launch_one<8, Ev>(A, stream, sm_count);
+            return launch_one<8, Ev, LIST>(A, stream, sm_count);
     }
 }
 

@@ -1,18 +1,36 @@
-// pfb_nll_sop.cu -- sum-of-products (log-domain) instantiations: 1, 2 or 4
-// observable columns x P in {1,2,4,8}.
+// pfb_nll_sop.cu -- sum-of-products (log-domain) instantiations.
+// Shape-specialised (exact leaf/term counts and leaf kinds) for the common
+// trees, and a generic instantiation (<= 4 leaves, <= 4 terms) for the rest.
 #include "pfb_nll_kernel.cuh"
 
 namespace pfb {
 
+static constexpr int kG = PFB_GAUSSIAN, kE = PFB_EXPONENTIAL;
+
+static int kinds_of(const NllArgs& A) {
+    int k = 0;
+    for (int l = 0; l < A.nleaf && l < kMaxLeaves; ++l) k |= (A.leaf[l].kind & 3) << (2 * l);
+    return k;
+}
+
 cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
-    switch (nc) {
-        case 1:
-            return launch_p<EvSop<1>>(A, stream, sm_count);
-        case 2:
-            return launch_p<EvSop<2>>(A, stream, sm_count);
-        default:
-            return launch_p<EvSop<4>>(A, stream, sm_count);
+    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
+    if (nc == 1) {
+        // SumPdf(gaussian, exponential): C1 / C5
+        if (nl == 2 && nt == 2 && kinds == (kG | kE << 2))
+            return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);
+        if (nl == 1 && nt == 1 && kinds == kG) return launch_p<EvSop<1, 1, 1, true, kG>>(A, stream, sm_count);
+        if (nl == 1 && nt == 1) return launch_p<EvSop<1, 1, 1, true>>(A, stream, sm_count);
+        if (nl == 2 && nt == 2) return launch_p<EvSop<1, 2, 2, true>>(A, stream, sm_count);
+        return launch_p<EvSop<1>>(A, stream, sm_count);
     }
+    if (nc == 2) {
+        // ProdPdf(gaussian(x), exponential(y)): C2
+        if (nl == 2 && nt == 1 && kinds == (kG | kE << 2))
+            return launch_p<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
+        return launch_p<EvSop<2>>(A, stream, sm_count);
+    }
+    return launch_p<EvSop<4>>(A, stream, sm_count);
 }
 
 }  // namespace pfb

@@ -115,6 +115,7 @@ def partial_nll(sh: Shard, pdf, snap, norms=None, block: int = DEFAULT_BLOCK, ct
     L.check(L.lib().pfb_nll_partial_async(ctx.handle, plan.handle, st, 0, sh.size, sh.begin, L.dptr(vals),
                                           len(vals), L.dptr(nv), len(nv), ctypes.c_void_p(acc.data_ptr())),
             "pfb_nll_partial_async")
+    L.check(L.lib().pfb_ctx_synchronize(ctx.handle), "pfb_ctx_synchronize")
     a = acc.cpu().numpy()
     if a[L.PFB_ACC_FAILS]:
         err = L.PfbErr()
@@ -215,26 +216,34 @@ class ShardedNll:
 
     def _raise_first_error(self):
         """Rare path: gather every rank's first failure, raise the global first."""
-        import torch
-        import torch.distributed as dist
-
         from . import engine
 
         err = L.PfbErr()
         L.check(L.lib().pfb_last_error(self.ctx.handle, ctypes.byref(err)), "pfb_last_error")
-        # reference order: chunk (shard) order first, then the check rank/index
-        mine = torch.tensor([self.rank if err.code else self.world, err.code, err.index, err.node],
-                            dtype=torch.int64, device=self.acc.device)
-        val = torch.tensor([err.value], dtype=torch.float64, device=self.acc.device)
-        if dist.is_initialized() and self.world > 1:
-            allk = [torch.empty_like(mine) for _ in range(self.world)]
-            allv = [torch.empty_like(val) for _ in range(self.world)]
-            dist.all_gather(allk, mine, group=self.group)
-            dist.all_gather(allv, val, group=self.group)
-        else:
-            allk, allv = [mine], [val]
-        best = min(range(len(allk)), key=lambda i: int(allk[i][0]))
-        k = allk[best].cpu().tolist()
+        code, index, node, value = first_error_across_ranks(
+            self.rank, self.world, (err.code, err.index, err.node, err.value), self.group, self.acc.device)
         e = L.PfbErr()
-        e.code, e.index, e.node, e.value = int(k[1]), int(k[2]), int(k[3]), float(allv[best].item())
+        e.code, e.index, e.node, e.value = code, index, node, value
         engine.raise_for(e, e.code, self.pdf, "ShardedNll")
+
+
+def first_error_across_ranks(rank: int, world: int, err: tuple, group=None, device="cpu") -> tuple:
+    """The error the reference would raise: shards are evaluated in order
+    (sharding.py:145), so the lowest failing rank wins.  err = (code, index,
+    node, value); code 0 means this rank had no failure."""
+    import torch
+    import torch.distributed as dist
+
+    code, index, node, value = err
+    mine = torch.tensor([rank if code else world, code, index, node], dtype=torch.int64, device=device)
+    val = torch.tensor([value], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and world > 1:
+        allk = [torch.empty_like(mine) for _ in range(world)]
+        allv = [torch.empty_like(val) for _ in range(world)]
+        dist.all_gather(allk, mine, group=group)
+        dist.all_gather(allv, val, group=group)
+    else:
+        allk, allv = [mine], [val]
+    best = min(range(len(allk)), key=lambda i: int(allk[i][0]))
+    k = allk[best].cpu().tolist()
+    return int(k[1]), int(k[2]), int(k[3]), float(allv[best].item())

@@ -249,6 +249,51 @@ def errors_fixture():
         json.dump(cases, fh, indent=1)
 
 
+def fits_fixture():
+    """Reference FitManager results (values, errors, minimum, call counts)."""
+    from parafit.fitting import FitManager
+
+    out = {}
+    g = np.load(os.path.join(OUT, "c1_sumpdf.npz"))
+    x, pdf, params = c1_model()
+    for v, val in zip(params, (4.8, 0.6, -0.25, 0.35)):
+        v.value = val
+    ds = UnbinnedDataSet([x])
+    ds.extend([g["x"]])
+    r = FitManager(pdf, ds).fit()
+    out["c1"] = {"start": [4.8, 0.6, -0.25, 0.35], "names": list(r.names), "values": r.values.tolist(),
+                 "errors": r.errors.tolist(), "nll_min": r.nll_min, "n_calls": r.n_calls, "status": r.status}
+    g2 = np.load(os.path.join(OUT, "c2_prod.npz"))
+    x = Variable.observable("x", 0.0, 10.0)
+    y = Variable.observable("y", 0.0, 10.0)
+    mu = Variable("mu", 4.9, 0.0, 10.0, step=0.01)
+    sigma = Variable("sigma", 1.1, 0.01, 5.0, step=1e-3)
+    alpha = Variable("alpha", -0.35, -5.0, 5.0, step=1e-3)
+    pdf2 = prod_pdf([gaussian(x, mu, sigma), exponential(y, alpha)])
+    ds2 = UnbinnedDataSet([x, y])
+    ds2.extend([g2["x"], g2["y"]])
+    r = FitManager(pdf2, ds2).fit()
+    out["c2"] = {"start": [4.9, 1.1, -0.35], "names": list(r.names), "values": r.values.tolist(),
+                 "errors": r.errors.tolist(), "nll_min": r.nll_min, "n_calls": r.n_calls, "status": r.status}
+    g3 = np.load(os.path.join(OUT, "c3_dalitz.npz"))
+    terms = c3_terms()
+    start = {"rhom_mag": 0.8, "rhom_ph": 0.05, "rho0_mag": 0.5, "rho0_ph": 0.2, "nr_mag": 18.0, "nr_ph": -0.4}
+    for t in terms:
+        for var in (t.magnitude, t.phase):
+            if var.name in start:
+                var.value = start[var.name]
+    s12 = Variable.observable("s12", *D_CHANNEL.s12_range)
+    s13 = Variable.observable("s13", *D_CHANNEL.s13_range)
+    ds3 = UnbinnedDataSet([s12, s13])
+    ds3.extend([g3["s12"], g3["s13"]])
+    pdf3 = dalitz_pdf(terms, D_CHANNEL, s12_obs=s12, s13_obs=s13, grid=(128, 128))
+    r = FitManager(pdf3, ds3).fit()
+    out["c3"] = {"start": start, "grid": [128, 128], "names": list(r.names), "values": r.values.tolist(),
+                 "errors": r.errors.tolist(), "nll_min": r.nll_min, "n_calls": r.n_calls, "status": r.status}
+    with open(os.path.join(OUT, "fits.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     reduction_fixture()
     c1_fixture()
@@ -256,5 +301,6 @@ if __name__ == "__main__":
     c3_fixture()
     shards_fixture()
     errors_fixture()
+    fits_fixture()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
