@@ -91,6 +91,7 @@ _SIGNATURES = [
     ("pfb_ctx_stream", _PTR, [_PTR]),
     ("pfb_ctx_synchronize", c_int, [_PTR]),
     ("pfb_ctx_set_warps_per_block", c_int, [_PTR, c_int]),
+    ("pfb_ctx_set_pipeline", c_int, [_PTR, c_int]),
     ("pfb_ctx_launch_count", c_int, [_PTR, _I64_P]),
     ("pfb_ctx_enable_timing", c_int, [_PTR, c_int]),
     ("pfb_ctx_last_kernel_ms", c_int, [_PTR, POINTER(c_float)]),

@@ -59,6 +59,7 @@ struct pfb_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     int warps_override = 0;
+    int pipeline = 1;  // 1: TMA bulk-copy pipeline where available
     unsigned long long* acc = nullptr;
     unsigned int* ticket = nullptr;
     unsigned long long* work_counter = nullptr;
@@ -266,6 +267,12 @@ int pfb_ctx_synchronize(pfb_ctx* c) {
 int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
     if (!c || !(w == 0 || w == 1 || w == 2 || w == 4 || w == 8)) return PFB_E_INVALID_ARGUMENT;
     c->warps_override = w;
+    return PFB_OK;
+}
+
+int pfb_ctx_set_pipeline(pfb_ctx* c, int mode) {
+    if (!c || mode < 0 || mode > 1) return PFB_E_INVALID_ARGUMENT;
+    c->pipeline = mode;
     return PFB_OK;
 }
 
@@ -638,6 +645,8 @@ static void build_dal(const pfb_plan* p, const double* values, NllArgs* A) {
         T.mg2 = T.mg * T.mg;
         T.cre = mag * cos(ph);
         T.cim = mag * sin(ph);
+        T.alpha = T.cre * T.m2 - T.cim * T.mg;
+        T.beta = T.cre * T.mg + T.cim * T.m2;
         T.cached = 0;
         if (T.spin == 1) {
             if (T.pair == 12 && D.zc12 != 0.0) D.need12 = 1;
@@ -669,6 +678,7 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     // evaluator at 1M-10M events (scripts/kernel_sweep.py)
     const int warps = c->warps_override ? c->warps_override : 8;
     A->warps = warps;
+    A->tma = c->pipeline;
     A->acc = c->acc;
     A->ticket = c->ticket;
     A->work_counter = c->work_counter;
@@ -1222,6 +1232,7 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->evaluator = 100;
     const int warps = c->warps_override ? c->warps_override : 8;
     A->warps = warps;
+    A->tma = c->pipeline;
     A->acc = c->acc;
     A->ticket = c->ticket;
     A->work_counter = c->work_counter;

@@ -80,6 +80,8 @@ struct DalTerm {
     double mg;        // m*width
     double mg2;       // (m*width)^2
     double cre, cim;  // magnitude*(cos phase, sin phase)
+    double alpha;     // cre*m^2 - cim*m*G
+    double beta;      // cre*m*G + cim*m^2
 };
 
 struct DalDesc {
@@ -102,6 +104,7 @@ struct NllArgs {
     int32_t tail;             // events in the trailing partial block
     int32_t evaluator;
     int32_t warps;            // warps cooperating on one block (1,2,4,8)
+    int32_t tma;              // 1: TMA bulk-copy pipeline for HBM-bound evaluators
     int32_t mode;             // KernelMode: export / add-export / accumulate
     int64_t idx_base;         // added to local event indices in error keys
     int64_t block_base;       // global block index of this range's block 0

@@ -1,7 +1,7 @@
 // pfb_nll.cu -- generic instantiations (literal interpreter, reduction
 // known-answer mode, the list-driven fix-up launch), the accumulator export,
 // the error probe, the FP64 peak microbenchmark and the evaluator dispatch.
-#include "pfb_nll_kernel.cuh"
+#include "pfb_nll_tma.cuh"
 
 namespace pfb {
 
@@ -58,6 +58,7 @@ cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         case EV_DALITZ_CACHED:
             return launch_dalitz(A, stream, sm_count);
         case 100:  // reduction known-answer mode
+            if (A.tma) return launch_tma<EvTerms>(A, stream, sm_count);
             return launch_p<EvTerms>(A, stream, sm_count);
         default:
             return launch_p<EvLiteral<1>>(A, stream, sm_count);

@@ -1,8 +1,22 @@
 // pfb_nll_dal.cu -- Dalitz instantiations: recompute path with K known at
-// compile time (batch-inverted denominators), generic/lineshape-cache path.
+// compile time (batch-inverted denominators), optionally with the term
+// structure (pair, spin per term) fixed at compile time; the generic /
+// lineshape-cache path for everything else.
 #include "pfb_nll_kernel.cuh"
 
 namespace pfb {
+
+// (pair, spin) signature, 3 bits per term (see EvDalitz)
+static constexpr int sig_term(int pair, int spin) { return dal_pair_code(pair) | (spin << 2); }
+// C3 / C4: D0 -> pi+ pi- pi0 with rho+ (13, P-wave), rho- (23), rho0 (12), NR (12, S-wave)
+static constexpr int kSigD0 = sig_term(13, 1) | sig_term(23, 1) << 3 | sig_term(12, 1) << 6 |
+                              sig_term(12, 0) << 9;
+
+static int signature_of(const DalDesc& D) {
+    int sig = 0;
+    for (int k = 0; k < D.K; ++k) sig |= sig_term(D.t[k].pair, D.t[k].spin) << (3 * k);
+    return sig;
+}
 
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.evaluator == EV_DALITZ_CACHED) return launch_p<EvDalitzCached>(A, stream, sm_count);
@@ -12,6 +26,7 @@ cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
         case 3:
             return launch_p<EvDalitz<3>>(A, stream, sm_count);
         case 4:
+            if (signature_of(A.dal) == kSigD0) return launch_p<EvDalitz<4, kSigD0>>(A, stream, sm_count);
             return launch_p<EvDalitz<4>>(A, stream, sm_count);
         default:  // any K: per-term reciprocals, no cache rows
             return launch_p<EvDalitzCached>(A, stream, sm_count);

@@ -168,6 +168,7 @@ __device__ __forceinline__ double literal_or_fail(const NllArgs& A, int64_t loca
 struct EvTerms {
     static constexpr int NC = 1;
     static constexpr int U = 8;
+    static constexpr int MINB = 4;
     __device__ static __forceinline__ double2 eval2(const NllArgs&, const double2 (&x)[1], int64_t,
                                                     long long*, int, bool&) {
         return x[0];
@@ -179,6 +180,7 @@ template <int NC_>
 struct EvLiteral {
     static constexpr int NC = NC_;
     static constexpr int U = 1;
+    static constexpr int MINB = 1;
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&)[NC_],
                                                     int64_t local, long long* sacc, int nvalid, bool&) {
         double2 t;
@@ -202,6 +204,7 @@ template <int NC_, int NL = kMaxLeaves, int NT = kMaxTerms, bool EXACT = false, 
 struct EvSop {
     static constexpr int NC = NC_;
     static constexpr int U = 4;
+    static constexpr int MINB = EXACT ? 3 : 1;
 
     __device__ static __forceinline__ constexpr bool has_value_leaf() {
         if (KINDS == 0) return true;
@@ -231,13 +234,16 @@ struct EvSop {
                 const SopLeaf& L = A.leaf[l];
                 const double xv = pick(x, L.col, which);
                 const int kind = KINDS ? ((KINDS >> (2 * l)) & 3) : L.kind;
+                // With a single term the term budget (sum |u| <= thr < 700)
+                // already bounds every leaf, so the per-leaf check is dropped.
+                constexpr bool kLeafGuard = !(EXACT && NT == 1);
                 if (kind == PFB_GAUSSIAN) {
                     const double z = (xv - A.v[L.voff]) * A.v[L.voff + 1];
                     u[l] = -0.5 * z * z;
-                    good &= (u[l] >= -600.0) || (u[l] < -746.0);
+                    if (kLeafGuard) good &= (u[l] >= -600.0) || (u[l] < -746.0);
                 } else if (kind == PFB_EXPONENTIAL) {
                     u[l] = A.v[L.voff] * xv;
-                    good &= (fabs(u[l]) <= 600.0) || (u[l] < -746.0);
+                    if (kLeafGuard) good &= (fabs(u[l]) <= 600.0) || (u[l] < -746.0);
                 } else if (has_value_leaf()) {  // polynomial (Horner, as polyval)
                     const double* c = A.v + L.voff;
                     double acc = c[L.nv - 1];
@@ -309,29 +315,36 @@ struct EvSop {
 
 // Dalitz coherent sum, recompute path, K terms known at compile time.
 // All K Breit-Wigner denominators and the Zemach 1/s_pair share ONE
-// reciprocal through Montgomery batch inversion.
-template <int K>
+// reciprocal through Montgomery batch inversion.  SIG >= 0 fixes each term's
+// (pair, spin) at compile time -- 3 bits per term: pair code (0: 12, 1: 13,
+// 2: 23) and the spin bit -- removing the per-term selects and branches.
+__host__ __device__ constexpr int dal_pair_code(int pair) { return pair == 12 ? 0 : (pair == 13 ? 1 : 2); }
+
+template <int K, int SIG = -1>
 struct EvDalitz {
     static constexpr int NC = 2;
     static constexpr int U = 2;
+    static constexpr int MINB = 3;
 
     __device__ static __forceinline__ double one(const NllArgs& A, double s12, double s13,
                                                  bool* ok) {
         const DalDesc& D = A.dal;
         constexpr int KK = (K > 0 ? K : 1);
         const double s23 = (D.mss - s12) - s13;
-        double a[KK], d[KK + 3], P[KK + 3];
+        int pc[KK], sp[KK];
+#pragma unroll
+        for (int k = 0; k < KK; ++k) {
+            pc[k] = SIG >= 0 ? ((SIG >> (3 * k)) & 3) : dal_pair_code(D.t[k].pair);
+            sp[k] = SIG >= 0 ? ((SIG >> (3 * k + 2)) & 1) : D.t[k].spin;
+        }
+        double sv[KK], d[KK], P[KK + 3];
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
             const DalTerm& T = D.t[k];
-            const double s = T.pair == 12 ? s12 : (T.pair == 13 ? s13 : s23);
-            a[k] = T.m2 - s;
-            d[k] = fma(a[k], a[k], T.mg2);
+            sv[k] = pc[k] == 0 ? s12 : (pc[k] == 1 ? s13 : s23);
+            const double a = T.m2 - sv[k];
+            d[k] = fma(a, a, T.mg2);
         }
-        int n = KK;
-        d[KK] = s12;
-        d[KK + 1] = s13;
-        d[KK + 2] = s23;
         // prefix products over the used denominators
         P[0] = d[0];
 #pragma unroll
@@ -343,7 +356,6 @@ struct EvDalitz {
         P[KK + 1] = last;
         if (D.need23) last = last * s23;
         P[KK + 2] = last;
-        (void)n;
         double inv = 1.0 / last;
         bool good = (last > 1e-280) && (last < 1e280);
         double r23 = 0.0, r13 = 0.0, r12 = 0.0;
@@ -366,25 +378,26 @@ struct EvDalitz {
             inv = inv * d[k];
         }
         r[0] = inv;
+        // c_k BW_k Z_k = w_k [(alpha_k - cre_k s) + i (beta_k - cim_k s)],
+        // w_k = Z_k / |m_k^2 - s - i m_k G_k|^2, alpha/beta per-call constants
+        const double d12 = s13 - s23, d13 = s12 - s23, d23 = s12 - s13;
         double tr = 0.0, ti = 0.0;
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
             const DalTerm& T = D.t[k];
-            double br = a[k] * r[k];
-            double bi = T.mg * r[k];
-            if (T.spin == 1) {
+            double w = r[k];
+            if (sp[k] == 1) {
                 double z;
-                if (T.pair == 12)
-                    z = fma(D.zc12, r12, s13 - s23);
-                else if (T.pair == 13)
-                    z = fma(D.zc13, r13, s12 - s23);
+                if (pc[k] == 0)
+                    z = fma(D.zc12, r12, d12);
+                else if (pc[k] == 1)
+                    z = fma(D.zc13, r13, d13);
                 else
-                    z = fma(D.zc23, r23, s12 - s13);
-                br *= z;
-                bi *= z;
+                    z = fma(D.zc23, r23, d23);
+                w *= z;
             }
-            tr = fma(T.cre, br, fma(-T.cim, bi, tr));
-            ti = fma(T.cre, bi, fma(T.cim, br, ti));
+            tr = fma(w, fma(-T.cre, sv[k], T.alpha), tr);
+            ti = fma(w, fma(-T.cim, sv[k], T.beta), ti);
         }
         const double I = fma(tr, tr, ti * ti);
         const double p = I * A.inv_norm;
@@ -409,6 +422,7 @@ struct EvDalitz {
 struct EvDalitzCached {
     static constexpr int NC = 2;
     static constexpr int U = 2;
+    static constexpr int MINB = 2;
 
     __device__ static __forceinline__ double one(const NllArgs& A, double s12, double s13,
                                                  int64_t local, bool* ok) {
@@ -601,7 +615,7 @@ enum KernelMode : int32_t {
 };
 
 template <int P, class Ev, bool LIST>
-__global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant__ NllArgs A) {
+__global__ void __launch_bounds__(kThreads, Ev::MINB) nll_kernel(const __grid_constant__ NllArgs A) {
     constexpr int NC = Ev::NC;
     constexpr int GROUPS = kThreads / (32 * P);
     constexpr int KPT = 64 / P;                       // double2 slots per thread per block
@@ -611,7 +625,6 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
     __shared__ double2 xch[GROUPS][P][32];
     __shared__ int xbad[GROUPS][P];
     __shared__ long long s_item[GROUPS];
-    __shared__ double s_tail[kBlock];  // ragged-tail terms (one per launch)
     __shared__ long long sacc[PFB_ACC_WORDS];
     __shared__ unsigned int s_last;
 
@@ -658,8 +671,8 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
                     x[c] = pair ? ld2(p) : make_double2(__ldg(p), __ldg(p));
                 }
                 const double2 t = Ev::eval2(A, x, lbase + e, sacc, pair ? 2 : 1, bad);
-                s_tail[e] = t.x;
-                if (pair) s_tail[e + 1] = t.y;
+                A.tail_scratch[e] = t.x;
+                if (pair) A.tail_scratch[e + 1] = t.y;
             }
             const unsigned anybad = __any_sync(0xffffffffu, bad);
             if (lane == 0) xbad[grp][wig] = anybad ? 1 : 0;
@@ -667,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1) nll_kernel(const __grid_constant_
             bad = false;
 #pragma unroll
             for (int w = 0; w < P; ++w) bad |= xbad[grp][w] != 0;
-            if (wig == 0 && !bad) bsum = pairwise_warp(s_tail, n, lane);
+            if (wig == 0 && !bad) bsum = pairwise_warp(A.tail_scratch, n, lane);
             group_sync<P>(grp);
         } else {
             // ---- full block, reference half-folding tree

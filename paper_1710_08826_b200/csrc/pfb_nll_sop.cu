@@ -1,7 +1,8 @@
 // pfb_nll_sop.cu -- sum-of-products (log-domain) instantiations.
 // Shape-specialised (exact leaf/term counts and leaf kinds) for the common
-// trees, and a generic instantiation (<= 4 leaves, <= 4 terms) for the rest.
-#include "pfb_nll_kernel.cuh"
+// trees -- streamed through the TMA pipeline -- and a generic instantiation
+// (<= 4 leaves, <= 4 terms) on the SIMT kernel for the rest.
+#include "pfb_nll_tma.cuh"
 
 namespace pfb {
 
@@ -13,13 +14,22 @@ static int kinds_of(const NllArgs& A) {
     return k;
 }
 
+template <class Ev>
+static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    if (A.tma) return launch_tma<Ev>(A, stream, sm_count);
+    return launch_p<Ev>(A, stream, sm_count);
+}
+
 cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
     const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
     if (nc == 1) {
-        // SumPdf(gaussian, exponential): C1 / C5
+        // SumPdf(gaussian, exponential): C1 / C5.  FP64-bound (one exp and
+        // one log per event): the SIMT kernel's 24 warps/SM beat the TMA
+        // pipeline's 16 consumer warps (kernel_sweep, round 1).
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2))
             return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);
-        if (nl == 1 && nt == 1 && kinds == kG) return launch_p<EvSop<1, 1, 1, true, kG>>(A, stream, sm_count);
+        if (nl == 1 && nt == 1 && kinds == kG)
+            return launch_stream<EvSop<1, 1, 1, true, kG>>(A, stream, sm_count);
         if (nl == 1 && nt == 1) return launch_p<EvSop<1, 1, 1, true>>(A, stream, sm_count);
         if (nl == 2 && nt == 2) return launch_p<EvSop<1, 2, 2, true>>(A, stream, sm_count);
         return launch_p<EvSop<1>>(A, stream, sm_count);
@@ -27,7 +37,7 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
     if (nc == 2) {
         // ProdPdf(gaussian(x), exponential(y)): C2
         if (nl == 2 && nt == 1 && kinds == (kG | kE << 2))
-            return launch_p<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
+            return launch_stream<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
         return launch_p<EvSop<2>>(A, stream, sm_count);
     }
     return launch_p<EvSop<4>>(A, stream, sm_count);

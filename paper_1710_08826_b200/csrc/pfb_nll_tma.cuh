@@ -1,0 +1,284 @@
+// pfb_nll_tma.cuh -- TMA-pipelined NLL kernel for the HBM-bound evaluators.
+//
+// One CTA per SM: a producer warp streams whole 4096-event column blocks
+// into an S-stage shared-memory ring with cp.async.bulk (the TMA bulk-copy
+// engine; completion tracked by mbarrier transaction counts), and sixteen
+// consumer warps evaluate -ln p from shared memory and fold each block with
+// the same reference-order tree as nll_kernel (element e = 2*lane + {0,1} +
+// 64*w + 64*16*k; slots k streamed in bit-reversed order through a binary
+// counter, then warps, lanes, x+y).  Stages are released as soon as the
+// consumers have read them, so the copy engine always has S-1 blocks of
+// prefetch in flight and no thread spends registers or issue slots on loads.
+//
+// Blocks are handed out by the producer from the device work counter; the
+// ragged tail (item 0) is copied like any block and its terms are written in
+// place before the split recursion.  Blocks holding an event the fast
+// evaluator cannot certify are deferred to the exact fix-up launch, exactly
+// as in nll_kernel.
+#pragma once
+
+#include "pfb_nll_kernel.cuh"
+
+namespace pfb {
+
+constexpr int kTmaConsumers = 16;                  // consumer warps = one block tree
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "PFB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra PFB_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kTmaConsumers) : "memory");
+}
+
+template <class Ev, int S>
+__global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_constant__ NllArgs A) {
+    constexpr int NC = Ev::NC;
+    constexpr int KPT = 64 / kTmaConsumers;  // 4 double2 slots per consumer thread
+    constexpr int LK = Log2<KPT>::value;
+    extern __shared__ __align__(128) double stage[];  // S x NC x 4096 doubles
+
+    __shared__ unsigned long long full_bar[S], empty_bar[S];
+    __shared__ long long s_blk[S];
+    __shared__ double2 xch[kTmaConsumers][32];
+    __shared__ int xbad[kTmaConsumers];
+    __shared__ long long sacc[PFB_ACC_WORDS];
+    __shared__ unsigned int s_last;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kTmaConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
+    __syncthreads();
+
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    if (warp == kTmaConsumers) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            for (int u = 0;; ++u) {
+                const int s = u % S;
+                mbar_wait(&empty_bar[s], ((u / S) & 1) ^ 1);
+                const int64_t it = (int64_t)atomicAdd(A.work_counter, 1ull);
+                if (it >= nitems) {
+                    s_blk[s] = -1;
+                    mbar_arrive(&full_bar[s]);
+                    break;
+                }
+                const bool is_tail = A.tail && it == 0;
+                const int64_t bidx = is_tail ? A.nfull : it - (A.tail ? 1 : 0);
+                s_blk[s] = bidx;
+                // bulk copies move multiples of 16 B: an odd tail's last event
+                // is read from global memory by the consumers
+                const unsigned bytes = is_tail ? (unsigned)(8 * (A.tail & ~1)) : (unsigned)(8 * kBlock);
+                mbar_arrive_expect_tx(&full_bar[s], bytes * NC);
+                if (bytes) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        bulk_g2s(stage + ((int64_t)s * NC + c) * kBlock,
+                                 A.col[c] + A.begin + bidx * (int64_t)kBlock, bytes, &full_bar[s]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ consumers
+        const int w = warp;
+        for (int u = 0;; ++u) {
+            const int s = u % S;
+            mbar_wait(&full_bar[s], (u / S) & 1);
+            const int64_t bidx = s_blk[s];
+            if (bidx < 0) break;
+            const double* sx = stage + (int64_t)s * NC * kBlock;
+            bool bad = false;
+            double bsum = 0.0;
+            if (A.tail && bidx == A.nfull) {
+                // ragged tail: terms in place (column 0), then the split recursion
+                const int n = A.tail;
+                const int64_t lbase = A.nfull * (int64_t)kBlock;
+                double* t0 = stage + (int64_t)s * NC * kBlock;
+                for (int e = 2 * (w * 32 + lane); e < n; e += 64 * kTmaConsumers) {
+                    const bool pair = e + 1 < n;
+                    double2 x[NC];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        if (pair) {
+                            x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
+                        } else {
+                            const double v = __ldg(A.col[c] + A.begin + lbase + e);
+                            x[c] = make_double2(v, v);
+                        }
+                    }
+                    const double2 t = Ev::eval2(A, x, lbase + e, sacc, pair ? 2 : 1, bad);
+                    t0[e] = t.x;
+                    if (pair) t0[e + 1] = t.y;
+                }
+                const unsigned anybad = __any_sync(0xffffffffu, bad);
+                if (lane == 0) xbad[w] = anybad ? 1 : 0;
+                consumer_sync();
+                bad = false;
+#pragma unroll
+                for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
+                if (w == 0 && !bad) bsum = pairwise_warp(t0, n, lane);
+                consumer_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+            } else {
+                const int64_t lthr = bidx * (int64_t)kBlock + 2 * lane + 64 * w;
+                const int base = 2 * lane + 64 * w;
+                double2 lvl[LK];
+                double2 T = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < KPT; ++i) {
+                    const int k = (int)(__brev((unsigned)i) >> (32 - LK));
+                    double2 cur[NC];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        cur[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + base + 64 * kTmaConsumers * k);
+                    double2 v = Ev::eval2(A, cur, lthr + 64 * kTmaConsumers * (int64_t)k, sacc, 2, bad);
+#pragma unroll
+                    for (int b = 0; b < LK; ++b) {
+                        if ((i >> b) & 1) {
+                            v.x = Add(lvl[b].x, v.x);
+                            v.y = Add(lvl[b].y, v.y);
+                        } else {
+                            lvl[b] = v;
+                            break;
+                        }
+                    }
+                    T = v;
+                }
+                // this warp is done with the stage: hand it back to the producer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+                const unsigned anybad = __any_sync(0xffffffffu, bad);
+                xch[w][lane] = T;
+                if (lane == 0) xbad[w] = anybad ? 1 : 0;
+                consumer_sync();
+                bad = false;
+#pragma unroll
+                for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
+                if (w == 0 && !bad) {
+                    double2 Wv[kTmaConsumers];
+#pragma unroll
+                    for (int q = 0; q < kTmaConsumers; ++q) Wv[q] = xch[q][lane];
+#pragma unroll
+                    for (int h = kTmaConsumers / 2; h >= 1; h /= 2) {
+#pragma unroll
+                        for (int q = 0; q < h; ++q) {
+                            Wv[q].x = Add(Wv[q].x, Wv[q + h].x);
+                            Wv[q].y = Add(Wv[q].y, Wv[q + h].y);
+                        }
+                    }
+                    T = Wv[0];
+#pragma unroll
+                    for (int off = 16; off >= 1; off /= 2) {
+                        T.x = Add(T.x, __shfl_down_sync(0xffffffffu, T.x, off));
+                        T.y = Add(T.y, __shfl_down_sync(0xffffffffu, T.y, off));
+                    }
+                    bsum = Add(T.x, T.y);
+                }
+                consumer_sync();
+            }
+            if (w == 0 && lane == 0) {
+                if (bad) {
+                    const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
+                    A.fix_list[slot] = A.block_base + bidx;
+                } else {
+                    if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
+                    acc_add_shared(sacc, bsum);
+                }
+            }
+        }
+    }
+
+    // ---- flush the CTA accumulator; the last CTA exports and resets ----------
+    __syncthreads();
+    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x)
+        if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    if (tid == 0) *A.work_counter = 0ull;
+    if (A.mode == MODE_ACCUM) {
+        if (tid == 0) *A.ticket = 0u;
+        return;
+    }
+    __threadfence();
+    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) {
+        const long long v = (long long)atomicExch(A.acc + i, 0ull);
+        if (A.mode == MODE_EXPORT)
+            A.acc_out[i] = v;
+        else
+            A.acc_out[i] += v;
+    }
+    if (tid == 0) {
+        *A.ticket = 0u;
+        A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
+        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
+    }
+}
+
+// Stages: as many NC x 32 KB stages as fit the 227 KB opt-in shared memory.
+template <class Ev>
+static cudaError_t launch_tma(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    constexpr int NC = Ev::NC;
+    constexpr int S = NC == 1 ? 6 : (NC == 2 ? 3 : 1);
+    const size_t smem = (size_t)S * NC * kBlock * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(nll_tma_kernel<Ev, S>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    int64_t grid = sm_count;
+    if (grid > nitems) grid = nitems > 0 ? nitems : 1;
+    nll_tma_kernel<Ev, S><<<(unsigned)grid, kTmaThreads, smem, stream>>>(A);
+    return cudaGetLastError();
+}
+
+}  // namespace pfb
