@@ -45,25 +45,40 @@ CONFIGS = {
     "c1": dict(workload="C1 SumPdf 1-D (gauss+exp), 1M events", n=1_000_000, ncols=1),
     "c2": dict(workload="C2 ProductPdf 2-D (gauss(x) x exp(y)), 10M events", n=10_000_000, ncols=2),
     "c3": dict(workload="C3 Dalitz D0->pi+pi-pi0 (rho+, rho-, rho0, NR), 10M events", n=10_000_000, ncols=2),
+    "c4": dict(workload="C4 Dalitz D0->pi+pi-pi0, 100M events sharded over the GPUs (strong scaling)",
+               n=100_000_000, ncols=2),
     "c5": dict(workload="C5 toy unit: SumPdf 1-D, 10M events", n=10_000_000, ncols=1),
 }
+
+
+# SURVEY.md 8(d) algorithmic figures (each + - x / = 1 flop, exp/log = 1):
+# 4 terms x 20 + s23 2 + |T|^2 3 + /norm 1 + -log 2 + accumulate 1 (rounded to 84)
+FLOPS_PER_EVENT = {"c3": 84, "c4": 84}
 
 
 def log(msg: str) -> None:
     print(msg, file=sys.stderr, flush=True)
 
 
-def make_data(cfg: str, n: int, seed: int):
+def make_data(cfg: str, n: int, seed: int, device: bool = True):
+    """Synthetic events of the configuration's model: generated on the GPU
+    (pfb_gen_*) when one is available, else with the host numpy samplers."""
     from paper_1710_08826_b200 import mcgen
 
     if cfg in ("c1", "c5"):
+        if device:
+            return [mcgen.device_sumpdf_1d(n, 5.0, 0.5, -0.3, 0.3, 0.0, 10.0, seed)]
         return [mcgen.sumpdf_1d(n, 5.0, 0.5, -0.3, 0.3, 0.0, 10.0, seed)]
     if cfg == "c2":
+        if device:
+            return list(mcgen.device_prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, seed))
         return list(mcgen.prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, seed))
-    if cfg == "c3":
+    if cfg in ("c3", "c4"):
         from tests import models
 
         terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
+        if device:
+            return list(mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, seed))
         return list(mcgen.dalitz(n, terms, models.D_CHANNEL_T, seed))
     raise ValueError(cfg)
 
@@ -172,11 +187,20 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = args.config
     n_per = args.n or CONFIGS[cfg]["n"]
+    scaling = "weak"
+    if cfg == "c4" and not args.n:
+        # strong scaling: the 100M events are sharded over the ranks
+        # with the reference's shard() bounds
+        from paper_1710_08826_b200.sharding import shard_bounds
+
+        b = shard_bounds(CONFIGS[cfg]["n"], world)
+        n_per = b[rank + 1] - b[rank]
+        scaling = "strong"
 
     if args.impl == "reference":
         if rank != 0:
             return
-        cols = make_data(cfg, n_per, seed=1000)
+        cols = make_data(cfg, n_per, seed=1000, device=False)
         steps = max(1, args.steps)
         rates = []
         from oracle import parafit_oracle as O
@@ -194,7 +218,7 @@ def main():
         line = {
             "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIGS[cfg]["workload"], "n_events": n_per},
             "nll_evals_per_s": steps / dt,
             "cpu_baseline": {"value": value, "unit": "events/s", "cores": threads, "kind": "port",
@@ -222,8 +246,7 @@ def main():
     cols = make_data(cfg, n_per, seed=1000 + rank)
     log(f"[rank {rank}] generated {n_per} events for {cfg} in {time.perf_counter() - t_gen:.1f}s")
     obs, pdf = build_model(cfg)
-    ds = pf.UnbinnedDataSet(obs)
-    ds.extend(cols)
+    ds = pf.UnbinnedDataSet.from_columns(obs, cols, copy=False)  # keeps the generated HBM copy
     ctx = pf.device_context(dev)
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     ctx.enable_timing(True)
@@ -331,6 +354,18 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_event": 8 * len(arrays)}
+    if cfg in ("c3", "c4"):
+        # The Dalitz coherent sum is FP64-bound (~84 flop per
+        # event against 16 B).  Denominator: the FP64 DFMA-chain peak measured
+        # on this GPU in this run (pfb_fp64_peak; MEASURED_PEAKS.json has none).
+        fp64_peak = ctx.fp64_peak_tflops()
+        flops = FLOPS_PER_EVENT[cfg] * n_per
+        achieved_tf = flops / (ms_per_step * 1e-3) / 1e12
+        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": achieved_tf / fp64_peak, "traffic": traffic,
+                    "peak_source": "measured in this run (pfb_fp64_peak: DFMA chains, 2 flop each)",
+                    "algorithmic_flops_per_event": FLOPS_PER_EVENT[cfg],
+                    "hbm": {"achieved_GBps": achieved, "peak_GBps": peak, "frac": achieved / peak}}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -339,7 +374,7 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[cfg]["workload"], "n_events_per_gpu": n_per,
                    "evaluator": plan.evaluator, "l2": "flushed (256 MB read) before every step",

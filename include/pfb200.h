@@ -228,6 +228,21 @@ int pfb_grid_integrals(pfb_ctx* ctx, pfb_grid* g, int32_t nterms, const int32_t*
                        const uint8_t* stale, double* inout_matrix);
 int pfb_grid_destroy(pfb_grid* g);
 
+/* ---- synthetic events (toy MC; mcgen.generate_1d / generate_dalitz, mcgen.py:105-257) */
+/* Dalitz accept-reject into store columns 0 (s12) and 1 (s13): candidates
+ * uniform in the (s12, s13) box (Philox4x32-10, counter = candidate index),
+ * kept inside the kinematic boundary when u*envelope < |sum c_k A_k|^2, written in
+ * candidate order (deterministic per seed).  term_values: [mass, width,
+ * magnitude, phase] per term. */
+int pfb_gen_dalitz(pfb_ctx* ctx, const pfb_dalitz_desc* channel, const double* term_values,
+                   double envelope, uint64_t seed, int64_t n_events, pfb_store* out,
+                   int64_t* out_candidates);
+/* kind 0: f*Gauss(mu,sigma) + (1-f)*Exp(alpha) on [lo,hi] into column 0;
+ * kind 1: Gauss(mu,sigma) on [lo,hi] into column 0 x Exp(alpha) into column 1. */
+int pfb_gen_1d(pfb_ctx* ctx, int32_t kind, double mu, double sigma, double alpha, double f,
+               double lo, double hi, uint64_t seed, int64_t n_events, pfb_store* out);
+int pfb_store_download(pfb_store* st, int32_t col, double* host, int64_t offset, int64_t count);
+
 /* ---- microbenchmarks used for the roofline denominators ------------------------ */
 int pfb_fp64_peak(pfb_ctx* ctx, double* out_tflops);
 

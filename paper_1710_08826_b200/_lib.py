@@ -121,6 +121,9 @@ _SIGNATURES = [
     ("pfb_grid_mask", c_int, [_PTR, POINTER(c_uint8)]),
     ("pfb_grid_integrals", c_int, [_PTR, _PTR, c_int32, POINTER(c_int32), POINTER(c_int32), _DBL_P, POINTER(c_uint8), POINTER(c_uint8), _DBL_P]),
     ("pfb_grid_destroy", c_int, [_PTR]),
+    ("pfb_gen_dalitz", c_int, [_PTR, POINTER(PfbDalitzDesc), _DBL_P, c_double, ctypes.c_uint64, c_int64, _PTR, _I64_P]),
+    ("pfb_gen_1d", c_int, [_PTR, c_int32, c_double, c_double, c_double, c_double, c_double, c_double, ctypes.c_uint64, c_int64, _PTR]),
+    ("pfb_store_download", c_int, [_PTR, c_int32, _DBL_P, c_int64, c_int64]),
     ("pfb_fp64_peak", c_int, [_PTR, _DBL_P]),
 ]
 

@@ -30,6 +30,9 @@ cudaError_t launch_grid_overlap(const double2* amps, int64_t n, const int2* pair
 cudaError_t launch_lineshape_cache(const DalDesc& D, const DalTerm& T, const double* s12,
                                    const double* s13, int64_t n, double2* row, cudaStream_t st,
                                    int sm_count);
+cudaError_t launch_gen_1d(const Gen1D& G, int64_t n, double* x, double* y, cudaStream_t st, int sm);
+cudaError_t run_gen_dalitz(const GenDalitz& G, int64_t n, double* s12, double* s13, cudaStream_t st,
+                           int sm, int64_t* candidates_used);
 }  // namespace pfb
 
 using namespace pfb;
@@ -1461,6 +1464,94 @@ int pfb_grid_destroy(pfb_grid* g) {
     cudaFree(g->p13);
     cudaFree(g->amps);
     delete g;
+    return PFB_OK;
+}
+
+// ---- synthetic event generation (toy MC) -------------------------------------------
+
+static void fill_daldesc(const pfb_dalitz_desc& d, const double* raw, DalDesc* D) {
+    memset(D, 0, sizeof(DalDesc));
+    const double M = d.mother_mass;
+    const double M2 = M * M, m1sq = d.m1 * d.m1, m2sq = d.m2 * d.m2, m3sq = d.m3 * d.m3;
+    D->K = d.nterms;
+    D->mss = ((M2 + m1sq) + m2sq) + m3sq;
+    D->zc12 = (M2 - m3sq) * (m2sq - m1sq);
+    D->zc13 = (M2 - m2sq) * (m3sq - m1sq);
+    D->zc23 = (M2 - m1sq) * (m3sq - m2sq);
+    for (int k = 0; k < d.nterms; ++k) {
+        DalTerm& T = D->t[k];
+        const double m = raw[4 * k], w = raw[4 * k + 1], mag = raw[4 * k + 2], ph = raw[4 * k + 3];
+        T.pair = d.pair[k];
+        T.spin = d.spin[k];
+        T.m2 = m * m;
+        T.mg = m * w;
+        T.mg2 = T.mg * T.mg;
+        T.cre = mag * cos(ph);
+        T.cim = mag * sin(ph);
+        T.alpha = T.cre * T.m2 - T.cim * T.mg;
+        T.beta = T.cre * T.mg + T.cim * T.m2;
+    }
+}
+
+int pfb_gen_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term_values, double envelope,
+                   uint64_t seed, int64_t n, pfb_store* out, int64_t* candidates) {
+    if (!c || !d || !term_values || !out || n < 0 || out->ncols < 2 || out->n < n || !(envelope > 0.0) ||
+        d->nterms < 1 || d->nterms > kMaxDal)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    GenDalitz G;
+    memset(&G, 0, sizeof(G));
+    fill_daldesc(*d, term_values, &G.D);
+    const double a12 = d->m1 + d->m2, b12 = d->mother_mass - d->m3;
+    const double a13 = d->m1 + d->m3, b13 = d->mother_mass - d->m2;
+    G.lo12 = a12 * a12;
+    G.hi12 = b12 * b12;
+    G.lo13 = a13 * a13;
+    G.hi13 = b13 * b13;
+    G.m1sq = d->m1 * d->m1;
+    G.m2sq = d->m2 * d->m2;
+    G.m3sq = d->m3 * d->m3;
+    G.M2 = d->mother_mass * d->mother_mass;
+    G.envelope = envelope;
+    G.seed_lo = (uint32_t)seed;
+    G.seed_hi = (uint32_t)(seed >> 32);
+    if (n == 0) return PFB_OK;
+    CK(run_gen_dalitz(G, n, out->cols[0], out->cols[1], c->stream, c->sm_count, candidates));
+    c->launches += 3;
+    CK(cudaStreamSynchronize(c->stream));
+    return PFB_OK;
+}
+
+int pfb_gen_1d(pfb_ctx* c, int32_t kind, double mu, double sigma, double alpha, double f, double lo,
+               double hi, uint64_t seed, int64_t n, pfb_store* out) {
+    if (!c || !out || n < 0 || out->n < n || (kind != 0 && kind != 1) || out->ncols < (kind == 1 ? 2 : 1) ||
+        !(sigma > 0.0) || !(hi > lo))
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    Gen1D G;
+    G.kind = kind;
+    G.mu = mu;
+    G.sigma = sigma;
+    G.alpha = alpha;
+    G.f = f;
+    G.lo = lo;
+    G.hi = hi;
+    G.seed_lo = (uint32_t)seed;
+    G.seed_hi = (uint32_t)(seed >> 32);
+    if (n == 0) return PFB_OK;
+    CK(launch_gen_1d(G, n, out->cols[0], kind == 1 ? out->cols[1] : nullptr, c->stream, c->sm_count));
+    ++c->launches;
+    CK(cudaStreamSynchronize(c->stream));
+    return PFB_OK;
+}
+
+int pfb_store_download(pfb_store* st, int32_t col, double* host, int64_t offset, int64_t count) {
+    if (!st || !host || col < 0 || col >= st->ncols || offset < 0 || count < 0 || offset + count > st->n)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(st->ctx->device));
+    CK(cudaMemcpyAsync(host, st->cols[col] + offset, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                       st->ctx->stream));
+    CK(cudaStreamSynchronize(st->ctx->stream));
     return PFB_OK;
 }
 

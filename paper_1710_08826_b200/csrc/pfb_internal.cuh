@@ -134,6 +134,19 @@ struct NllArgs {
     DalDesc dal;
 };
 
+// Synthetic-event generators (pfb_gen.cu).
+struct GenDalitz {
+    DalDesc D;
+    double lo12, hi12, lo13, hi13, m1sq, m2sq, m3sq, M2;
+    double envelope;
+    uint32_t seed_lo, seed_hi;
+};
+struct Gen1D {
+    int kind;  // 0: f*Gauss + (1-f)*Exp on [lo,hi] (1 column); 1: Gauss(x) x Exp(y) (2 columns)
+    double mu, sigma, alpha, f, lo, hi;
+    uint32_t seed_lo, seed_hi;
+};
+
 // Dalitz integration grid constants (dalitz.py:246-264).
 struct GridConsts {
     int nx, ny;

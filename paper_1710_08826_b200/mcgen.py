@@ -109,3 +109,87 @@ def dalitz(n: int, terms, channel, seed: int, chunk: int = 1 << 22):
         a13[got:got + take] = c13[:take]
         got += take
     return a12, a13
+
+
+# --- device generation (libpfb200: pfb_gen_1d / pfb_gen_dalitz) -------------------------
+
+
+def _device_store(ctx, ncols: int, n: int):
+    import ctypes
+
+    from . import _lib as L
+
+    st = ctypes.c_void_p()
+    L.check(L.lib().pfb_store_create(ctx.handle, ncols, n, ctypes.byref(st)), "pfb_store_create")
+    return st
+
+
+def _adopt(ctx, st, ncols: int, n: int):
+    """Download the generated columns and register the device store as the
+    HBM copy of those host arrays (no re-upload when the NLL runs)."""
+    from . import _lib as L
+
+    cols = []
+    for c in range(ncols):
+        a = np.empty(n, dtype=np.float64)
+        L.check(L.lib().pfb_store_download(st, c, L.dptr(a), 0, n), "pfb_store_download")
+        cols.append(a)
+    ctx._stores[tuple(id(a) for a in cols) + (0, n)] = (st, tuple(cols))
+    return cols
+
+
+def device_sumpdf_1d(n, mu, sigma, alpha, f, lo, hi, seed, ctx=None):
+    """C1 / C5 events generated on the GPU: f * Gauss + (1 - f) * Exp on [lo, hi]."""
+    from . import _lib as L
+    from .engine import device_context
+
+    ctx = ctx or device_context(0)
+    st = _device_store(ctx, 1, n)
+    L.check(L.lib().pfb_gen_1d(ctx.handle, 0, mu, sigma, alpha, f, lo, hi, seed, n, st), "pfb_gen_1d")
+    return _adopt(ctx, st, 1, n)[0]
+
+
+def device_prod_2d(n, mu, sigma, alpha, lo, hi, seed, ctx=None):
+    """C2 events generated on the GPU: Gauss(x) x Exp(y) on [lo, hi]^2."""
+    from . import _lib as L
+    from .engine import device_context
+
+    ctx = ctx or device_context(0)
+    st = _device_store(ctx, 2, n)
+    L.check(L.lib().pfb_gen_1d(ctx.handle, 1, mu, sigma, alpha, 0.0, lo, hi, seed, n, st), "pfb_gen_1d")
+    return tuple(_adopt(ctx, st, 2, n))
+
+
+def dalitz_envelope(terms, channel, safety: float = 1.2, points: int = 512) -> float:
+    """safety x the largest intensity on a points^2 midpoint scan (reference mcgen.py:180-181)."""
+    M, m1, m2, m3 = channel
+    lo12, hi12 = (m1 + m2) ** 2, (M - m3) ** 2
+    lo13, hi13 = (m1 + m3) ** 2, (M - m2) ** 2
+    g12 = lo12 + (np.arange(points) + 0.5) * (hi12 - lo12) / points
+    g13 = lo13 + (np.arange(points) + 0.5) * (hi13 - lo13) / points
+    G12, G13 = np.meshgrid(g12, g13, indexing="ij")
+    inside = _boundary(G12, G13, M, m1, m2, m3)
+    return safety * float(_intensity(terms, G12[inside], G13[inside], M, m1, m2, m3).max())
+
+
+def device_dalitz(n, terms, channel, seed, ctx=None, envelope=None):
+    """Dalitz events generated on the GPU; terms = [(pair, spin, m, w, mag, phase)]."""
+    import ctypes
+
+    from . import _lib as L
+    from .engine import device_context
+
+    ctx = ctx or device_context(0)
+    d = L.PfbDalitzDesc()
+    d.mother_mass, d.m1, d.m2, d.m3 = channel
+    d.nterms = len(terms)
+    vals = np.zeros(4 * len(terms))
+    for k, (pair, spin, m, w, mag, ph) in enumerate(terms):
+        d.pair[k], d.spin[k] = int(pair), int(spin)
+        vals[4 * k:4 * k + 4] = (m, w, mag, ph)
+    env = envelope if envelope is not None else dalitz_envelope(terms, channel)
+    st = _device_store(ctx, 2, n)
+    cand = ctypes.c_int64()
+    L.check(L.lib().pfb_gen_dalitz(ctx.handle, ctypes.byref(d), L.dptr(vals), env, seed, n, st, ctypes.byref(cand)),
+            "pfb_gen_dalitz")
+    return tuple(_adopt(ctx, st, 2, n))
