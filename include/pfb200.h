@@ -180,6 +180,17 @@ int pfb_nll_block_sums(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, 
                        int64_t end, int64_t index_offset, const double* values, int32_t nvalues,
                        const double* norms, int32_t nnorms, double* out_block_sums,
                        int64_t n_out, pfb_err* out_err);
+/* Batched objective: the NLL at `npts` <= 16 parameter
+ * points -- e.g. the 2P finite-difference points of fitting.fd_gradient
+ * (fitting.py:140-151) or the Hesse stencil (fitting.py:180-213) -- each
+ * bitwise equal to its own pfb_nll.  HBM-bound plans evaluate all points in
+ * ONE pass over the events (the stage stays in shared memory while every point
+ * is folded); others run one fused launch per point.  values: npts rows of
+ * nvalues; norms: npts rows of nnorms; out_nll / out_err: npts entries.
+ * Returns the first failing point's status (in point order) or PFB_OK. */
+int pfb_nll_batch(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin, int64_t end,
+                  int64_t index_offset, const double* values, int32_t npts, int32_t nvalues,
+                  const double* norms, int32_t nnorms, double* out_nll, pfb_err* out_err);
 /* Enqueue (no host sync) the exact partial of [begin,end) into `dev_acc`
  * (PFB_ACC_WORDS int64 on the device, overwritten).  Sum these across ranks with
  * one allreduce, then pfb_finalize.  The local error record is kept in the

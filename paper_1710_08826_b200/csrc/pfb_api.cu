@@ -14,6 +14,7 @@
 namespace pfb {
 cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
 cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count);
+bool sop_batched_in_kernel(const NllArgs& A, int nc);
 cudaError_t launch_export(unsigned long long* acc, long long* out, long long* result_i,
                           unsigned long long* fix_counter, unsigned long long* errkey,
                           cudaStream_t stream);
@@ -52,7 +53,8 @@ static int cuda_fail(cudaError_t e) {
 
 static constexpr int kStoreMaxCols = 16;
 // result words: [0, 72) exported accumulator, [72] deferred-block count, [73] error key
-static constexpr int kResWords = PFB_ACC_WORDS + 2;
+static constexpr int kResHead = 2;  // [0] deferred-block count, [1] error key
+static constexpr int kResWords = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
 enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
 struct pfb_ctx {
@@ -206,8 +208,8 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
-    CK(cudaMalloc(&c->acc, sizeof(unsigned long long) * PFB_ACC_WORDS));
-    CK(cudaMemset(c->acc, 0, sizeof(unsigned long long) * PFB_ACC_WORDS));
+    CK(cudaMalloc(&c->acc, sizeof(unsigned long long) * kMaxPts * PFB_ACC_WORDS));
+    CK(cudaMemset(c->acc, 0, sizeof(unsigned long long) * kMaxPts * PFB_ACC_WORDS));
     CK(cudaMalloc(&c->ticket, sizeof(unsigned int)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned int)));
     CK(cudaMalloc(&c->work_counter, sizeof(unsigned long long)));
@@ -659,6 +661,68 @@ static void build_dal(const pfb_plan* p, const double* values, NllArgs* A) {
     }
 }
 
+// Sum-of-products tables for parameter point m: the structural leaf/term
+// layout (A->leaf, A->term masks) and the point's row A->ptv[m] = leaf values
+// (mu, 1/sigma, alpha, coefficients) then (log coef, threshold) per term.  A
+// zero weight keeps its term with log coef -inf (exactly 0 in the reference).
+// Returns false when the leaf values do not fit a row.
+static bool fill_sop_point(const pfb_plan* p, const double* values, const double* norms, NllArgs* A,
+                           int m) {
+    double* row = A->ptv[m];
+    int vo = 0;
+    A->nleaf = (int)p->leaf_nodes.size();
+    for (int l = 0; l < A->nleaf; ++l) {
+        const int ni = p->leaf_nodes[l];
+        const pfb_node& n = p->nodes[ni];
+        SopLeaf& L = A->leaf[l];
+        L.kind = n.kind;
+        L.col = p->node_slot0[ni];
+        L.voff = vo;
+        L.nv = n.kind == PFB_GAUSSIAN ? 2 : (n.kind == PFB_EXPONENTIAL ? 1 : n.nparam);
+        if (vo + L.nv > kPtLeafWords) return false;
+        const double* raw = values + p->raw_off[ni];
+        if (n.kind == PFB_GAUSSIAN) {
+            row[vo] = raw[0];
+            row[vo + 1] = 1.0 / raw[1];
+        } else {
+            for (int k = 0; k < L.nv; ++k) row[vo + k] = raw[k];
+        }
+        vo += L.nv;
+    }
+    A->nterm = (int)p->terms.size();
+    for (int t = 0; t < A->nterm; ++t) {
+        const TermStruct& ts = p->terms[t];
+        double logc = 0.0, budget = 0.0;
+        bool zero = false;
+        for (const auto& f : ts.factors) {
+            double v;
+            if (f.type == 0) {  // weight f.child of add node f.node (pdf._fractions)
+                const double* raw = values + p->raw_off[f.node];
+                const int nf = p->nodes[f.node].nchild - 1;
+                v = f.child < nf ? raw[f.child] : 1.0 - numpy_sum(raw, nf);
+            } else {
+                v = 1.0 / norms[f.node];
+            }
+            if (!(v > 0.0) || !isfinite(v)) {
+                zero = true;
+                break;
+            }
+            const double lv = log(v);
+            logc += lv;
+            budget += fabs(lv);
+        }
+        SopTerm& T = A->term[t];
+        T.emask = ts.emask;
+        T.vmask = ts.vmask;
+        T.logcoef = zero ? -INFINITY : logc;
+        T.coef = zero ? 0.0 : exp(logc);
+        T.thr = 690.0 - budget;
+        row[kPtLeafWords + 2 * t] = T.logcoef;
+        row[kPtLeafWords + 2 * t + 1] = T.thr;
+    }
+    return true;
+}
+
 // Fills A from the plan and this call's raw values/norms.  Returns the rank of
 // a failing fraction check (host-side, FractionOutOfRange) or -1.
 static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end,
@@ -687,11 +751,11 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     A->work_counter = c->work_counter;
     A->errkey = c->errkey;
     A->tail_scratch = c->tail_scratch;
-    A->acc_out = c->res_dev;
-    A->result_i = c->res_dev + PFB_ACC_WORDS;
+    A->acc_out = c->res_dev + kResHead;
+    A->result_i = c->res_dev;
     A->fix_counter = c->fix_counter;
     A->fix_list = c->fix_list;
-    A->fix_count = c->res_dev + PFB_ACC_WORDS;
+    A->fix_count = c->res_dev;
     A->block_base = 0;
     A->mode = MODE_EXPORT;
     A->nops = (int)p->nodes.size();
@@ -742,60 +806,9 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     build_dal(p, values, A);
     A->inv_norm = 1.0 / norms[A->nops - 1];
     // sum of products
-    if (p->evaluator == EV_SOP) {
-        int vo = p->nder;
-        A->nleaf = (int)p->leaf_nodes.size();
-        for (int l = 0; l < A->nleaf; ++l) {
-            const int ni = p->leaf_nodes[l];
-            const pfb_node& n = p->nodes[ni];
-            SopLeaf& L = A->leaf[l];
-            L.kind = n.kind;
-            L.col = p->node_slot0[ni];
-            L.voff = vo;
-            const double* raw = values + p->raw_off[ni];
-            if (n.kind == PFB_GAUSSIAN) {
-                A->v[vo] = raw[0];
-                A->v[vo + 1] = 1.0 / raw[1];
-                L.nv = 2;
-            } else if (n.kind == PFB_EXPONENTIAL) {
-                A->v[vo] = raw[0];
-                L.nv = 1;
-            } else {
-                for (int k = 0; k < n.nparam; ++k) A->v[vo + k] = raw[k];
-                L.nv = n.nparam;
-            }
-            vo += L.nv;
-        }
-        if (vo > kMaxVals) A->evaluator = EV_LITERAL;
-        int nt = 0;
-        for (const auto& ts : p->terms) {
-            double logc = 0.0, budget = 0.0;
-            bool zero = false;
-            for (const auto& f : ts.factors) {
-                double v;
-                if (f.type == 0) {
-                    v = A->v[p->der_off[f.node] + f.child];
-                } else {
-                    v = 1.0 / norms[f.node];
-                }
-                if (!(v > 0.0) || !isfinite(v)) {
-                    zero = true;
-                    break;
-                }
-                const double lv = log(v);
-                logc += lv;
-                budget += fabs(lv);
-            }
-            if (zero) continue;
-            SopTerm& T = A->term[nt++];
-            T.emask = ts.emask;
-            T.vmask = ts.vmask;
-            T.logcoef = logc;
-            T.coef = exp(logc);
-            T.thr = 690.0 - budget;
-        }
-        A->nterm = nt;
-    }
+    A->npts = 1;
+    A->fix_point = 0;
+    if (p->evaluator == EV_SOP && !fill_sop_point(p, values, norms, A, 0)) A->evaluator = EV_LITERAL;
     return frac_fail;
 }
 
@@ -937,8 +950,8 @@ static int decode_error(pfb_ctx* c, const pfb_plan* p, const NllArgs& A, unsigne
     return e.code;
 }
 
-static int read_result(pfb_ctx* c) {
-    CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * kResWords,
+static int read_result(pfb_ctx* c, int npts = 1) {
+    CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * (kResHead + npts * PFB_ACC_WORDS),
                        cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
@@ -960,16 +973,16 @@ static int launch_fixup(pfb_ctx* c, const NllArgs& A, long long* out) {
     NllArgs F = A;
     F.mode = MODE_ADD_EXPORT;
     F.acc_out = out;
-    F.fix_count = c->res_dev + PFB_ACC_WORDS;
+    F.fix_count = c->res_dev;
     CK(launch_fix(F, c->stream, c->sm_count));
     ++c->launches;
     return PFB_OK;
 }
 
 // Host rounding of the exported accumulator words in res_host[0..72).
-static int round_result(pfb_ctx* c, double* out) {
+static int round_result(pfb_ctx* c, double* out, int point = 0) {
     double r = 0.0;
-    const int st = acc_round(c->res_host, &r);
+    const int st = acc_round(c->res_host + kResHead + point * PFB_ACC_WORDS, &r);
     if (out) *out = r;
     return st;
 }
@@ -1027,15 +1040,15 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
     if (rc) return rc;
     rc = read_result(c);
     if (rc) return rc;
-    if (c->res_host[PFB_ACC_WORDS] > 0) {  // deferred blocks: exact fix-up
-        rc = launch_fixup(c, *A, c->res_dev);
+    if (c->res_host[0] > 0) {  // deferred blocks: exact fix-up
+        rc = launch_fixup(c, *A, c->res_dev + kResHead);
         if (rc) return rc;
         const float fast_ms = c->last_ms;
         rc = read_result(c);
         if (rc) return rc;
         c->last_ms = fast_ms;
     }
-    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
+    const unsigned long long key = (unsigned long long)c->res_host[1];
     const int code = decode_error(c, p, *A, key, frac, index_offset, out_err);
     if (code) return code;
     if (block_sums_host)
@@ -1061,6 +1074,89 @@ int pfb_nll_block_sums(pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int64
     if (!out_block_sums) return PFB_E_INVALID_ARGUMENT;
     return nll_common(c, p, st, begin, end, index_offset, values, nvalues, norms, nnorms,
                       out_block_sums, n_out, nullptr, out_err);
+}
+
+int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin, int64_t end,
+                  int64_t index_offset, const double* values, int32_t npts, int32_t nvalues,
+                  const double* norms, int32_t nnorms, double* out_nll, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || !out_nll || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (npts < 1 || npts > kMaxPts) return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    for (int m = 0; m < npts; ++m) clear_err(out_err ? out_err + m : nullptr);
+    if (end == begin) {
+        for (int m = 0; m < npts; ++m)
+            if (out_err) out_err[m].code = PFB_E_EMPTY_DATASET;
+        return PFB_E_EMPTY_DATASET;
+    }
+    CK(cudaSetDevice(c->device));
+    pfb_store staged;
+    if (!range_aligned(p, st, begin)) {
+        const int rs = restage(c, p, st, begin, end, &staged);
+        if (rs) return rs;
+        st = &staged;
+        end -= begin;
+        begin = 0;
+    }
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
+    if (rc) return rc;
+    auto A = std::make_unique<NllArgs>();
+    int frac0 = pack_args(p, st, begin, end, values, norms, A.get());
+    const bool in_kernel = A->evaluator == EV_SOP && sop_batched_in_kernel(*A, sop_ncols(p));
+    int first = PFB_OK;
+    if (in_kernel) {
+        // one pass over the data for all points (TMA pipeline kernel)
+        for (int m = 1; m < npts; ++m)
+            fill_sop_point(p, values + (int64_t)m * nvalues, norms + (int64_t)m * nnorms, A.get(), m);
+        A->npts = npts;
+        rc = launch_eval(p, st, begin, end, A.get(), false);
+        if (rc) return rc;
+        rc = read_result(c, npts);
+        if (rc) return rc;
+        const bool deferred = c->res_host[0] > 0;
+        std::vector<long long> accs(c->res_host + kResHead, c->res_host + kResHead + npts * PFB_ACC_WORDS);
+        for (int m = 0; m < npts; ++m) {
+            // point m's literal tables (weights, norms) for the fix-up and errors
+            auto Am = std::make_unique<NllArgs>();
+            const int frac = m == 0 ? frac0
+                                    : pack_args(p, st, begin, end, values + (int64_t)m * nvalues,
+                                                norms + (int64_t)m * nnorms, Am.get());
+            const NllArgs& Ap = m == 0 ? *A : *Am;
+            unsigned long long key = ~0ull;
+            if (deferred) {
+                NllArgs F = Ap;
+                F.fix_point = m;
+                rc = launch_fixup(c, F, c->res_dev + kResHead + m * PFB_ACC_WORDS);
+                if (rc) return rc;
+                rc = read_result(c, npts);
+                if (rc) return rc;
+                key = (unsigned long long)c->res_host[1];
+                std::copy(c->res_host + kResHead + m * PFB_ACC_WORDS,
+                          c->res_host + kResHead + (m + 1) * PFB_ACC_WORDS, accs.begin() + m * PFB_ACC_WORDS);
+            }
+            pfb_err e;
+            int code = decode_error(c, p, Ap, key, frac, index_offset, &e);
+            double r = 0.0;
+            if (!code) code = acc_round(accs.data() + m * PFB_ACC_WORDS, &r);
+            out_nll[m] = r;
+            e.code = code;
+            if (out_err) out_err[m] = e;
+            if (code && !first) first = code;
+        }
+        return first;
+    }
+    // other evaluators: one fused launch per point, back to back in C++
+    for (int m = 0; m < npts; ++m) {
+        pfb_err e;
+        const int code = nll_common(c, p, st, begin, end, index_offset, values + (int64_t)m * nvalues,
+                                    nvalues, norms + (int64_t)m * nnorms, nnorms, nullptr, 0, out_nll + m, &e);
+        if (code >= PFB_E_INVALID_ARGUMENT) return code;
+        if (out_err) out_err[m] = e;
+        if (code && !first) first = code;
+    }
+    return first;
 }
 
 int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin,
@@ -1090,8 +1186,8 @@ int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, i
     c->last_index_offset = index_offset;
     if (end == begin) {  // empty shard: a zero partial (sharding.partial_nll, sharding.py:110-111)
         CK(cudaMemsetAsync(dev_acc, 0, sizeof(int64_t) * PFB_ACC_WORDS, c->stream));
-        CK(cudaMemsetAsync(c->res_dev + PFB_ACC_WORDS, 0, sizeof(long long), c->stream));
-        CK(cudaMemsetAsync(c->res_dev + PFB_ACC_WORDS + 1, 0xff, sizeof(long long), c->stream));
+        CK(cudaMemsetAsync(c->res_dev, 0, sizeof(long long), c->stream));
+        CK(cudaMemsetAsync(c->res_dev + 1, 0xff, sizeof(long long), c->stream));
         return PFB_OK;
     }
     A->acc_out = (long long*)dev_acc;
@@ -1119,7 +1215,7 @@ int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
     CK(cudaSetDevice(c->device));
     int rc = read_result(c);
     if (rc) return rc;
-    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
+    const unsigned long long key = (unsigned long long)c->res_host[1];
     decode_error(c, c->last_plan, *c->last_args, key, c->last_frac_rank, c->last_index_offset,
                  out_err);
     return PFB_OK;
@@ -1188,18 +1284,18 @@ int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols,
         rc = launch_eval(p, &st, b, e, A.get(), /*allow_cache=*/false);
         if (rc) return rc;
     }
-    CK(launch_export(c->acc, c->res_dev, c->res_dev + PFB_ACC_WORDS, c->fix_counter, c->errkey,
+    CK(launch_export(c->acc, c->res_dev + kResHead, c->res_dev, c->fix_counter, c->errkey,
                      c->stream));
     ++c->launches;
     rc = read_result(c);
     if (rc) return rc;
-    if (c->res_host[PFB_ACC_WORDS] > 0) {
-        rc = launch_fixup(c, A0, c->res_dev);
+    if (c->res_host[0] > 0) {
+        rc = launch_fixup(c, A0, c->res_dev + kResHead);
         if (rc) return rc;
         rc = read_result(c);
         if (rc) return rc;
     }
-    const unsigned long long key = (unsigned long long)c->res_host[PFB_ACC_WORDS + 1];
+    const unsigned long long key = (unsigned long long)c->res_host[1];
     const int code = decode_error(c, p, A0, key, frac, 0, out_err);
     if (code) return code;
     const int st_round = round_result(c, out_nll);
@@ -1233,6 +1329,7 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->nfull = n / kBlock;
     A->tail = (int32_t)(n % kBlock);
     A->evaluator = 100;
+    A->npts = 1;
     const int warps = c->warps_override ? c->warps_override : 8;
     A->warps = warps;
     A->tma = c->pipeline;
@@ -1241,8 +1338,8 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->work_counter = c->work_counter;
     A->errkey = c->errkey;
     A->tail_scratch = c->tail_scratch;
-    A->acc_out = c->res_dev;
-    A->result_i = c->res_dev + PFB_ACC_WORDS;
+    A->acc_out = c->res_dev + kResHead;
+    A->result_i = c->res_dev;
     A->fix_counter = c->fix_counter;
     A->fix_list = c->fix_list;
     A->mode = MODE_EXPORT;

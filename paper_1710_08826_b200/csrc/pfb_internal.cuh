@@ -38,6 +38,9 @@ constexpr int kMaxLeaves = 4;            // sum-of-products leaves (fast path)
 constexpr int kMaxTerms = 4;             // sum-of-products terms (fast path)
 constexpr int kMaxDal = PFB_MAX_DALITZ_TERMS;
 constexpr int kThreads = 256;            // CTA size of the NLL kernels
+constexpr int kMaxPts = 16;              // parameter points evaluated in one pass
+constexpr int kPtLeafWords = 16;         // per-point leaf values (mu, 1/sigma, alpha, coeffs)
+constexpr int kPtWords = kPtLeafWords + 2 * kMaxTerms;  // + (log coef, threshold) per term
 
 enum Evaluator : int32_t { EV_LITERAL = 0, EV_SOP = 1, EV_DALITZ = 2, EV_DALITZ_CACHED = 3 };
 
@@ -127,8 +130,12 @@ struct NllArgs {
     double v[kMaxVals];       // derived per-call values
     // sum-of-products
     int32_t nleaf, nterm;
-    SopLeaf leaf[kMaxLeaves];
+    SopLeaf leaf[kMaxLeaves];  // voff indexes a ptv row
     SopTerm term[kMaxTerms];
+    // batched objective: npts parameter points per pass over the data
+    int32_t npts;
+    int32_t fix_point;         // fix-up launch: the point whose deferred blocks it redoes
+    double ptv[kMaxPts][kPtWords];
     // dalitz
     double inv_norm;          // 1/norm_root (fast paths)
     DalDesc dal;

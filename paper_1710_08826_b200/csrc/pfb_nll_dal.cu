@@ -9,13 +9,14 @@ namespace pfb {
 // (pair, spin) signature, 3 bits per term (see EvDalitz)
 static constexpr int sig_term(int pair, int spin) { return dal_pair_code(pair) | (spin << 2); }
 // C3 / C4: D0 -> pi+ pi- pi0 with rho+ (13, P-wave), rho- (23), rho0 (12), NR (12, S-wave)
+// pi+ pi- equal masses: the 12 Zemach term has no 1/s12 part (need 13, 23 only)
 static constexpr int kSigD0 = sig_term(13, 1) | sig_term(23, 1) << 3 | sig_term(12, 1) << 6 |
-                              sig_term(12, 0) << 9;
+                              sig_term(12, 0) << 9 | 1 << 13 | 1 << 14;
 
 static int signature_of(const DalDesc& D) {
     int sig = 0;
     for (int k = 0; k < D.K; ++k) sig |= sig_term(D.t[k].pair, D.t[k].spin) << (3 * k);
-    return sig;
+    return sig | (D.need12 ? 1 << 12 : 0) | (D.need13 ? 1 << 13 : 0) | (D.need23 ? 1 << 14 : 0);
 }
 
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {

@@ -170,7 +170,7 @@ struct EvTerms {
     static constexpr int U = 8;
     static constexpr int MINB = 4;
     __device__ static __forceinline__ double2 eval2(const NllArgs&, const double2 (&x)[1], int64_t,
-                                                    long long*, int, bool&) {
+                                                    long long*, int, bool&, int = 0) {
         return x[0];
     }
 };
@@ -182,7 +182,7 @@ struct EvLiteral {
     static constexpr int U = 1;
     static constexpr int MINB = 1;
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&)[NC_],
-                                                    int64_t local, long long* sacc, int nvalid, bool&) {
+                                                    int64_t local, long long* sacc, int nvalid, bool&, int = 0) {
         double2 t;
         t.x = literal_or_fail(A, local, sacc);
         t.y = nvalid > 1 ? literal_or_fail(A, local + 1, sacc) : 0.0;
@@ -222,7 +222,7 @@ struct EvSop {
     }
 
     __device__ static __forceinline__ double one(const NllArgs& A, const double2 (&x)[NC_],
-                                                 int which, bool* ok) {
+                                                 int which, bool* ok, int m) {
         double u[NL];
         double lv[NL];  // |log| budget of value leaves
         bool good = true;
@@ -238,14 +238,14 @@ struct EvSop {
                 // already bounds every leaf, so the per-leaf check is dropped.
                 constexpr bool kLeafGuard = !(EXACT && NT == 1);
                 if (kind == PFB_GAUSSIAN) {
-                    const double z = (xv - A.v[L.voff]) * A.v[L.voff + 1];
+                    const double z = (xv - A.ptv[m][L.voff]) * A.ptv[m][L.voff + 1];
                     u[l] = -0.5 * z * z;
                     if (kLeafGuard) good &= (u[l] >= -600.0) || (u[l] < -746.0);
                 } else if (kind == PFB_EXPONENTIAL) {
-                    u[l] = A.v[L.voff] * xv;
+                    u[l] = A.ptv[m][L.voff] * xv;
                     if (kLeafGuard) good &= (fabs(u[l]) <= 600.0) || (u[l] < -746.0);
                 } else if (has_value_leaf()) {  // polynomial (Horner, as polyval)
-                    const double* c = A.v + L.voff;
+                    const double* c = A.ptv[m] + L.voff;
                     double acc = c[L.nv - 1];
                     for (int i = 2; i <= L.nv; ++i) acc = fma(acc, xv, c[L.nv - i]);
                     u[l] = acc;
@@ -264,8 +264,11 @@ struct EvSop {
             Vt[t] = 1.0;
             if (EXACT || t < A.nterm) {
                 const SopTerm& T = A.term[t];
-                double lsum = T.logcoef, budget = 0.0, vprod = 1.0;
-                bool dead = false;  // a leaf underflows to exactly 0 in the reference
+                const double lc = A.ptv[m][kPtLeafWords + 2 * t];
+                double lsum = lc, budget = 0.0, vprod = 1.0;
+                // dead: a zero weight (lc = -inf) or a leaf that underflows to
+                // exactly 0 in the reference -- the term contributes exactly 0
+                bool dead = !(lc > -1e300);
 #pragma unroll
                 for (int l = 0; l < NL; ++l) {
                     if ((T.emask >> l) & 1u) {
@@ -278,7 +281,7 @@ struct EvSop {
                         budget += lv[l];
                     }
                 }
-                good &= dead || (budget <= T.thr);
+                good &= dead || (budget <= A.ptv[m][kPtLeafWords + 2 * t + 1]);
                 live |= !dead;
                 Lt[t] = dead ? -1e300 : lsum;
                 Vt[t] = vprod;
@@ -303,11 +306,11 @@ struct EvSop {
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[NC_],
-                                                    int64_t, long long*, int nvalid, bool& bad) {
+                                                    int64_t, long long*, int nvalid, bool& bad, int m = 0) {
         bool ok0, ok1;
         double2 t;
-        t.x = one(A, x, 0, &ok0);
-        t.y = one(A, x, 1, &ok1);
+        t.x = one(A, x, 0, &ok0, m);
+        t.y = one(A, x, 1, &ok1, m);
         bad |= !ok0 || (nvalid > 1 && !ok1);
         return t;
     }
@@ -317,7 +320,10 @@ struct EvSop {
 // All K Breit-Wigner denominators and the Zemach 1/s_pair share ONE
 // reciprocal through Montgomery batch inversion.  SIG >= 0 fixes each term's
 // (pair, spin) at compile time -- 3 bits per term: pair code (0: 12, 1: 13,
-// 2: 23) and the spin bit -- removing the per-term selects and branches.
+// 2: 23) and the spin bit -- and, in bits 12..14, which Zemach 1/s_pair
+// factors the batch inversion carries (need12/13/23: a P-wave on that pair
+// with a nonzero mass-difference coefficient), removing the per-term selects
+// and branches.
 __host__ __device__ constexpr int dal_pair_code(int pair) { return pair == 12 ? 0 : (pair == 13 ? 1 : 2); }
 
 template <int K, int SIG = -1>
@@ -349,25 +355,28 @@ struct EvDalitz {
         P[0] = d[0];
 #pragma unroll
         for (int k = 1; k < KK; ++k) P[k] = P[k - 1] * d[k];
+        const bool n12 = SIG >= 0 ? ((SIG >> 12) & 1) : D.need12;
+        const bool n13 = SIG >= 0 ? ((SIG >> 13) & 1) : D.need13;
+        const bool n23 = SIG >= 0 ? ((SIG >> 14) & 1) : D.need23;
         double last = P[KK - 1];
-        if (D.need12) last = last * s12;
+        if (n12) last = last * s12;
         P[KK] = last;
-        if (D.need13) last = last * s13;
+        if (n13) last = last * s13;
         P[KK + 1] = last;
-        if (D.need23) last = last * s23;
+        if (n23) last = last * s23;
         P[KK + 2] = last;
         double inv = 1.0 / last;
         bool good = (last > 1e-280) && (last < 1e280);
         double r23 = 0.0, r13 = 0.0, r12 = 0.0;
-        if (D.need23) {
+        if (n23) {
             r23 = inv * P[KK + 1];
             inv = inv * s23;
         }
-        if (D.need13) {
+        if (n13) {
             r13 = inv * P[KK];
             inv = inv * s13;
         }
-        if (D.need12) {
+        if (n12) {
             r12 = inv * P[KK - 1];
             inv = inv * s12;
         }
@@ -407,7 +416,7 @@ struct EvDalitz {
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
-                                                    int64_t, long long*, int nvalid, bool& bad) {
+                                                    int64_t, long long*, int nvalid, bool& bad, int = 0) {
         bool ok0, ok1;
         double2 t;
         t.x = one(A, x[0].x, x[1].x, &ok0);
@@ -464,7 +473,7 @@ struct EvDalitzCached {
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
-                                                    int64_t local, long long*, int nvalid, bool& bad) {
+                                                    int64_t local, long long*, int nvalid, bool& bad, int = 0) {
         bool ok0, ok1;
         double2 t;
         t.x = one(A, x[0].x, x[1].x, local, &ok0);
@@ -650,7 +659,9 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_kernel(const __grid_co
         int64_t bidx;
         bool is_tail;
         if (LIST) {
-            bidx = A.fix_list[it] - A.block_base;
+            const int64_t entry = A.fix_list[it];
+            if ((int)(entry % kMaxPts) != A.fix_point) continue;  // another point's block
+            bidx = entry / kMaxPts - A.block_base;
             is_tail = A.tail && bidx == A.nfull;
         } else {
             is_tail = A.tail && it == 0;
@@ -767,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_kernel(const __grid_co
         if (wig == 0 && lane == 0) {
             if (bad) {  // defer the whole block to the exact fix-up launch
                 const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
-                A.fix_list[slot] = A.block_base + bidx;
+                A.fix_list[slot] = (A.block_base + bidx) * kMaxPts + A.fix_point;
             } else {
                 if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
                 acc_add_shared(sacc, bsum);

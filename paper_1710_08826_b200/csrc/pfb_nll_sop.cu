@@ -14,6 +14,16 @@ static int kinds_of(const NllArgs& A) {
     return k;
 }
 
+// True when launch_sop runs the TMA pipeline kernel for this plan -- the
+// kernel that evaluates A.npts parameter points per pass over the data.
+bool sop_batched_in_kernel(const NllArgs& A, int nc) {
+    if (!A.tma) return false;
+    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
+    if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
+    if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
+    return false;
+}
+
 template <class Ev>
 static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.tma) return launch_tma<Ev>(A, stream, sm_count);

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
     __shared__ long long s_blk[S];
     __shared__ double2 xch[kTmaConsumers][32];
     __shared__ int xbad[kTmaConsumers];
-    __shared__ long long sacc[PFB_ACC_WORDS];
+    __shared__ long long sacc[kMaxPts][PFB_ACC_WORDS];
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
+    for (int i = tid; i < kMaxPts * PFB_ACC_WORDS; i += blockDim.x) (&sacc[0][0])[i] = 0;
     __syncthreads();
 
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
         }
     } else {
         // ------------------------------------------------------------ consumers
+        // Batched objective: the stage stays resident while every parameter
+        // point is folded, so HBM traffic is one pass whatever npts is.
         const int w = warp;
         for (int u = 0;; ++u) {
             const int s = u % S;
@@ -130,112 +132,120 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
             const int64_t bidx = s_blk[s];
             if (bidx < 0) break;
             const double* sx = stage + (int64_t)s * NC * kBlock;
-            bool bad = false;
-            double bsum = 0.0;
-            if (A.tail && bidx == A.nfull) {
-                // ragged tail: terms in place (column 0), then the split recursion
-                const int n = A.tail;
-                const int64_t lbase = A.nfull * (int64_t)kBlock;
-                double* t0 = stage + (int64_t)s * NC * kBlock;
-                for (int e = 2 * (w * 32 + lane); e < n; e += 64 * kTmaConsumers) {
-                    const bool pair = e + 1 < n;
-                    double2 x[NC];
+            for (int m = 0; m < A.npts; ++m) {
+                bool bad = false;
+                double bsum = 0.0;
+                const bool last_pt = m == A.npts - 1;
+                if (A.tail && bidx == A.nfull) {
+                    // ragged tail: terms to global scratch, then the split recursion
+                    const int n = A.tail;
+                    const int64_t lbase = A.nfull * (int64_t)kBlock;
+                    for (int e = 2 * (w * 32 + lane); e < n; e += 64 * kTmaConsumers) {
+                        const bool pair = e + 1 < n;
+                        double2 x[NC];
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) {
-                        if (pair) {
-                            x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
-                        } else {
-                            const double v = __ldg(A.col[c] + A.begin + lbase + e);
-                            x[c] = make_double2(v, v);
+                        for (int c = 0; c < NC; ++c) {
+                            if (pair) {
+                                x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
+                            } else {
+                                const double v = __ldg(A.col[c] + A.begin + lbase + e);
+                                x[c] = make_double2(v, v);
+                            }
                         }
+                        const double2 t = Ev::eval2(A, x, lbase + e, sacc[0], pair ? 2 : 1, bad, m);
+                        A.tail_scratch[e] = t.x;
+                        if (pair) A.tail_scratch[e + 1] = t.y;
                     }
-                    const double2 t = Ev::eval2(A, x, lbase + e, sacc, pair ? 2 : 1, bad);
-                    t0[e] = t.x;
-                    if (pair) t0[e + 1] = t.y;
-                }
-                const unsigned anybad = __any_sync(0xffffffffu, bad);
-                if (lane == 0) xbad[w] = anybad ? 1 : 0;
-                consumer_sync();
-                bad = false;
-#pragma unroll
-                for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
-                if (w == 0 && !bad) bsum = pairwise_warp(t0, n, lane);
-                consumer_sync();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[s]);
-            } else {
-                const int64_t lthr = bidx * (int64_t)kBlock + 2 * lane + 64 * w;
-                const int base = 2 * lane + 64 * w;
-                double2 lvl[LK];
-                double2 T = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int i = 0; i < KPT; ++i) {
-                    const int k = (int)(__brev((unsigned)i) >> (32 - LK));
-                    double2 cur[NC];
-#pragma unroll
-                    for (int c = 0; c < NC; ++c)
-                        cur[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + base + 64 * kTmaConsumers * k);
-                    double2 v = Ev::eval2(A, cur, lthr + 64 * kTmaConsumers * (int64_t)k, sacc, 2, bad);
-#pragma unroll
-                    for (int b = 0; b < LK; ++b) {
-                        if ((i >> b) & 1) {
-                            v.x = Add(lvl[b].x, v.x);
-                            v.y = Add(lvl[b].y, v.y);
-                        } else {
-                            lvl[b] = v;
-                            break;
-                        }
+                    if (last_pt) {  // the stage is no longer read
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty_bar[s]);
                     }
-                    T = v;
-                }
-                // this warp is done with the stage: hand it back to the producer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[s]);
-                const unsigned anybad = __any_sync(0xffffffffu, bad);
-                xch[w][lane] = T;
-                if (lane == 0) xbad[w] = anybad ? 1 : 0;
-                consumer_sync();
-                bad = false;
+                    const unsigned anybad = __any_sync(0xffffffffu, bad);
+                    if (lane == 0) xbad[w] = anybad ? 1 : 0;
+                    consumer_sync();
+                    bad = false;
 #pragma unroll
-                for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
-                if (w == 0 && !bad) {
-                    double2 Wv[kTmaConsumers];
-#pragma unroll
-                    for (int q = 0; q < kTmaConsumers; ++q) Wv[q] = xch[q][lane];
-#pragma unroll
-                    for (int h = kTmaConsumers / 2; h >= 1; h /= 2) {
-#pragma unroll
-                        for (int q = 0; q < h; ++q) {
-                            Wv[q].x = Add(Wv[q].x, Wv[q + h].x);
-                            Wv[q].y = Add(Wv[q].y, Wv[q + h].y);
-                        }
-                    }
-                    T = Wv[0];
-#pragma unroll
-                    for (int off = 16; off >= 1; off /= 2) {
-                        T.x = Add(T.x, __shfl_down_sync(0xffffffffu, T.x, off));
-                        T.y = Add(T.y, __shfl_down_sync(0xffffffffu, T.y, off));
-                    }
-                    bsum = Add(T.x, T.y);
-                }
-                consumer_sync();
-            }
-            if (w == 0 && lane == 0) {
-                if (bad) {
-                    const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
-                    A.fix_list[slot] = A.block_base + bidx;
+                    for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
+                    if (w == 0 && !bad) bsum = pairwise_warp(A.tail_scratch, n, lane);
+                    consumer_sync();
                 } else {
-                    if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
-                    acc_add_shared(sacc, bsum);
+                    const int64_t lthr = bidx * (int64_t)kBlock + 2 * lane + 64 * w;
+                    const int base = 2 * lane + 64 * w;
+                    double2 lvl[LK];
+                    double2 T = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int i = 0; i < KPT; ++i) {
+                        const int k = (int)(__brev((unsigned)i) >> (32 - LK));
+                        double2 cur[NC];
+#pragma unroll
+                        for (int c = 0; c < NC; ++c)
+                            cur[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + base +
+                                                                       64 * kTmaConsumers * k);
+                        double2 v = Ev::eval2(A, cur, lthr + 64 * kTmaConsumers * (int64_t)k, sacc[0], 2, bad, m);
+#pragma unroll
+                        for (int b = 0; b < LK; ++b) {
+                            if ((i >> b) & 1) {
+                                v.x = Add(lvl[b].x, v.x);
+                                v.y = Add(lvl[b].y, v.y);
+                            } else {
+                                lvl[b] = v;
+                                break;
+                            }
+                        }
+                        T = v;
+                    }
+                    if (last_pt) {  // this warp is done with the stage: hand it back
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty_bar[s]);
+                    }
+                    const unsigned anybad = __any_sync(0xffffffffu, bad);
+                    xch[w][lane] = T;
+                    if (lane == 0) xbad[w] = anybad ? 1 : 0;
+                    consumer_sync();
+                    bad = false;
+#pragma unroll
+                    for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
+                    if (w == 0 && !bad) {
+                        double2 Wv[kTmaConsumers];
+#pragma unroll
+                        for (int q = 0; q < kTmaConsumers; ++q) Wv[q] = xch[q][lane];
+#pragma unroll
+                        for (int h = kTmaConsumers / 2; h >= 1; h /= 2) {
+#pragma unroll
+                            for (int q = 0; q < h; ++q) {
+                                Wv[q].x = Add(Wv[q].x, Wv[q + h].x);
+                                Wv[q].y = Add(Wv[q].y, Wv[q + h].y);
+                            }
+                        }
+                        T = Wv[0];
+#pragma unroll
+                        for (int off = 16; off >= 1; off /= 2) {
+                            T.x = Add(T.x, __shfl_down_sync(0xffffffffu, T.x, off));
+                            T.y = Add(T.y, __shfl_down_sync(0xffffffffu, T.y, off));
+                        }
+                        bsum = Add(T.x, T.y);
+                    }
+                    consumer_sync();
+                }
+                if (w == 0 && lane == 0) {
+                    if (bad) {  // defer (block, point) to the exact fix-up launch
+                        const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
+                        A.fix_list[slot] = (A.block_base + bidx) * kMaxPts + m;
+                    } else {
+                        if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
+                        acc_add_shared(sacc[m], bsum);
+                    }
                 }
             }
         }
     }
 
-    // ---- flush the CTA accumulator; the last CTA exports and resets ----------
+    // ---- flush the CTA accumulators; the last CTA exports and resets ----------
+    const int nwords = A.npts * PFB_ACC_WORDS;
+    long long* sflat = &sacc[0][0];
     __syncthreads();
-    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x)
-        if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
+    for (int i = tid; i < nwords; i += blockDim.x)
+        if (sflat[i]) atomicAdd(A.acc + i, (unsigned long long)sflat[i]);
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
         return;
     }
     __threadfence();
-    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) {
+    for (int i = tid; i < nwords; i += blockDim.x) {
         const long long v = (long long)atomicExch(A.acc + i, 0ull);
         if (A.mode == MODE_EXPORT)
             A.acc_out[i] = v;

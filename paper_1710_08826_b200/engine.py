@@ -292,6 +292,47 @@ class DeviceBackend:
                              index_offset + start, lineshape_cache=self.lineshape_cache)
         return self._evaluate_multi(pdf, arrays, names, snap, norms, start, stop, index_offset)
 
+    MAX_BATCH = 16
+
+    def evaluate_batch(self, pdf, columns: Mapping[str, np.ndarray], snaps, norms_list, start: int, stop: int,
+                       index_offset: int = 0) -> list:
+        """NLL at several parameter points.  Returns one
+        entry per point: the float, or the exception that point's own
+        evaluation would raise.  HBM-bound plans read the events once per
+        group of up to 16 points; each value is bitwise its single-point NLL."""
+        names = tuple(columns.keys())
+        arrays = [columns[k] for k in names]
+        if len(self.contexts) > 1:
+            return [self._try(lambda s=s, n=n: self.evaluate(pdf, columns, s, n, start, stop, index_offset))
+                    for s, n in zip(snaps, norms_list)]
+        ctx = self.contexts[0]
+        plan = ctx.plan_for(pdf, names)
+        st = ctx.store_for(arrays)
+        out: list = []
+        for g0 in range(0, len(snaps), self.MAX_BATCH):
+            sn, nl = snaps[g0:g0 + self.MAX_BATCH], norms_list[g0:g0 + self.MAX_BATCH]
+            vals, nv = plan.pack_batch(sn, nl)
+            m = len(sn)
+            res = np.empty(m, dtype=np.float64)
+            errs = (L.PfbErr * m)()
+            code = L.lib().pfb_nll_batch(ctx.handle, plan.handle, st, start, stop, index_offset + start,
+                                         L.dptr(vals), m, vals.shape[1], L.dptr(nv), nv.shape[1], L.dptr(res), errs)
+            if code >= L.E_INVALID_ARGUMENT:
+                raise L.NativeError(code, "pfb_nll_batch")
+            for k in range(m):
+                if errs[k].code:
+                    out.append(self._try(lambda e=errs[k]: raise_for(e, e.code, pdf, "pfb_nll_batch")))
+                else:
+                    out.append(float(res[k]))
+        return out
+
+    @staticmethod
+    def _try(fn):
+        try:
+            return fn()
+        except Exception as exc:  # returned, raised by the caller in call order
+            return exc
+
     def block_sums(self, pdf, columns, snap, norms, start: int, stop: int, index_offset: int = 0):
         names = tuple(columns.keys())
         arrays = [columns[k] for k in names]

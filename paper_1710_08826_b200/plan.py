@@ -132,6 +132,16 @@ class Plan:
             nv[i] = norms[node.id]
         return vals, nv
 
+    def pack_batch(self, snaps, norms_list) -> tuple[np.ndarray, np.ndarray]:
+        """Rows of raw values and norms for several parameter points."""
+        vals = np.empty((len(snaps), self.nvalues), dtype=np.float64)
+        nv = np.empty((len(snaps), self.nnodes), dtype=np.float64)
+        for m, (snap, norms) in enumerate(zip(snaps, norms_list)):
+            v, n = self.pack(snap, norms)
+            vals[m] = v
+            nv[m] = n
+        return vals, nv
+
     def close(self) -> None:
         if self.handle:
             L.lib().pfb_plan_destroy(self.handle)

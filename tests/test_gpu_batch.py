@@ -1,0 +1,127 @@
+"""Batched objective: several parameter points per pass.
+
+Each batched value must be bitwise its own single-point NLL, errors must be
+attributed to the right point, and a fit driven through the batched objective
+must follow exactly the trajectory (values, n_calls) of point-by-point calls.
+"""
+
+import numpy as np
+import pytest
+
+from tests import models
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import paper_1710_08826_b200 as pf
+    from paper_1710_08826_b200 import _lib as L
+
+    if L.device_count() < 1:
+        pytest.fail("GPU test run without a CUDA device")
+    return pf
+
+
+def points_eval(pf, pdf, ds, params, pts):
+    """(snaps, norms) per point the way the fitter builds them."""
+    store = pf.NormalizationStore()
+    snaps, norms = [], []
+    for pt in pts:
+        for v, val in zip(params, pt):
+            pf.set_value(v, float(val))
+        snap = pf.snapshot(pdf.param_closure())
+        snaps.append(snap)
+        norms.append(pf.resolve_norms(pdf, snap, store))
+    return snaps, norms
+
+
+def single(pf, pdf, ds, params, pt):
+    for v, val in zip(params, pt):
+        pf.set_value(v, float(val))
+    try:
+        return pf.nll(pdf, ds)
+    except Exception as exc:  # the batched call returns the exception in this slot
+        return exc
+
+
+def outcome(r):
+    """Comparable form: floats bitwise, errors by type and event index."""
+    if isinstance(r, Exception):
+        return (type(r).__name__, getattr(r, "index", None))
+    return ("ok", float(r).hex())
+
+
+@pytest.mark.parametrize("config", ["c2", "c1"])
+def test_batch_equals_single_bitwise(pf, config):
+    rng = np.random.default_rng(4)
+    n = 9 * 4096 + 777
+    if config == "c2":
+        (x, y), pdf, params = models.c2()
+        xs = np.clip(rng.normal(5, 1, n), 0, 10)
+        xs[::5000] = 0.2  # far tail: defers to the exact fix-up at the "wide tail" point below
+        ds = models.dataset([x, y], [xs, np.clip(rng.exponential(2.5, n), 0, 10)])
+        base = np.array([5.0, 1.0, -0.4])
+    else:
+        x, pdf, params = models.c1()
+        xs = np.clip(np.concatenate([rng.normal(5, 0.5, n // 2), rng.exponential(3.0, n - n // 2)]), 0, 10)
+        ds = models.dataset([x], [xs])
+        base = np.array([5.0, 0.5, -0.3, 0.3])
+    pts = [base]
+    for k in range(len(base)):
+        for s in (+1, -1):
+            p = base.copy()
+            p[k] += s * 0.01
+            pts.append(p)
+    # a point whose gaussian is so narrow that most events defer to the exact fix-up
+    # (for the product model it underflows to zero: NonPositiveDensity, as in the reference)
+    narrow = base.copy()
+    narrow[1] = 0.011
+    pts.append(narrow)
+    if config == "c2":
+        tail = base.copy()
+        tail[1] = 0.1336  # u ~ -645 at x = 0.2: guard-deferred yet positive
+        pts.append(tail)
+    want = [outcome(single(pf, pdf, ds, params, p)) for p in pts]
+    snaps, norms = points_eval(pf, pdf, ds, params, pts)
+    backend = pf.DeviceBackend()
+    names = tuple(sorted({o.name for node in pdf.walk() for o in node.observables}))
+    cols = {k: ds.column(k) for k in names}
+    got = backend.evaluate_batch(pdf, cols, snaps, norms, 0, ds.n_events)
+    assert [outcome(r) for r in got] == want
+    assert any(w[0] == "ok" for w in want)
+
+
+def test_batch_error_attributed_to_its_point(pf):
+    x = pf.Variable.observable("x", 0.0, 1.0)
+    c0 = pf.Variable("c0", 0.5, -1.0, 2.0)
+    c1 = pf.Variable("c1", 1.0, -2.0, 2.0)
+    pdf = pf.polynomial(x, [c0, c1])
+    vals = np.linspace(0.0, 1.0, 9000)
+    ds = models.dataset([x], [vals])
+    pts = [(0.5, 1.0), (0.0, 1.0), (0.6, 1.0)]  # point 1: p(0) = 0 -> NonPositiveDensity at index 0
+    snaps, norms = points_eval(pf, pdf, ds, [c0, c1], pts)
+    got = pf.DeviceBackend().evaluate_batch(pdf, {"x": ds.column("x")}, snaps, norms, 0, ds.n_events)
+    assert isinstance(got[1], pf.errors.NonPositiveDensity) and got[1].index == 0
+    assert got[0] == single(pf, pdf, ds, [c0, c1], pts[0])
+    assert got[2] == single(pf, pdf, ds, [c0, c1], pts[2])
+
+
+def test_batched_fit_equals_unbatched_fit(pf, golden_dir):
+    import os
+
+    from paper_1710_08826_b200.fitting import FcnHandle, FitManager, minimize
+
+    g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
+    (x, y), pdf, params = models.c2((4.9, 1.1, -0.35))
+    ds = models.dataset([x, y], [g["x"], g["y"]])
+    batched = FitManager(pdf, ds).fit()
+    for v, val in zip(params, (4.9, 1.1, -0.35)):
+        pf.set_value(v, val)
+    fm = FitManager(pdf, ds)
+    plain = fm.fcn()
+    unbatched = minimize(FcnHandle(plain._objective), fm.free_parameters(), fm.options)
+    assert batched.n_calls == unbatched.n_calls
+    assert np.array_equal(batched.values, unbatched.values)
+    assert batched.nll_min == unbatched.nll_min
+    np.testing.assert_array_equal(batched.covariance, unbatched.covariance)
