@@ -2,7 +2,7 @@
 // compile time (batch-inverted denominators), optionally with the term
 // structure (pair, spin per term) fixed at compile time; the generic /
 // lineshape-cache path for everything else.
-#include "pfb_nll_kernel.cuh"
+#include "pfb_nll_prod.cuh"
 
 namespace pfb {
 
@@ -19,16 +19,24 @@ static int signature_of(const DalDesc& D) {
     return sig | (D.need12 ? 1 << 12 : 0) | (D.need13 ? 1 << 13 : 0) | (D.need23 ? 1 << 14 : 0);
 }
 
+// Recompute-path evaluators run in product mode (one log per 16 events,
+// pfb_nll_prod.cuh) unless the pipeline is switched off (log-domain kernel).
+template <class Ev>
+static cudaError_t launch_dal(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    if (A.tma) return launch_prod<Ev>(A, stream, sm_count);
+    return launch_p<Ev>(A, stream, sm_count);
+}
+
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.evaluator == EV_DALITZ_CACHED) return launch_p<EvDalitzCached>(A, stream, sm_count);
     switch (A.dal.K) {
         case 2:
-            return launch_p<EvDalitz<2>>(A, stream, sm_count);
+            return launch_dal<EvDalitz<2>>(A, stream, sm_count);
         case 3:
-            return launch_p<EvDalitz<3>>(A, stream, sm_count);
+            return launch_dal<EvDalitz<3>>(A, stream, sm_count);
         case 4:
-            if (signature_of(A.dal) == kSigD0) return launch_p<EvDalitz<4, kSigD0>>(A, stream, sm_count);
-            return launch_p<EvDalitz<4>>(A, stream, sm_count);
+            if (signature_of(A.dal) == kSigD0) return launch_dal<EvDalitz<4, kSigD0>>(A, stream, sm_count);
+            return launch_dal<EvDalitz<4>>(A, stream, sm_count);
         default:  // any K: per-term reciprocals, no cache rows
             return launch_p<EvDalitzCached>(A, stream, sm_count);
     }

@@ -332,8 +332,9 @@ struct EvDalitz {
     static constexpr int U = 2;
     static constexpr int MINB = 3;
 
-    __device__ static __forceinline__ double one(const NllArgs& A, double s12, double s13,
-                                                 bool* ok) {
+    // p = |sum_k c_k BW_k Z_k|^2 / norm; *ok = the batch inversion stayed in range
+    __device__ static __forceinline__ double prob(const NllArgs& A, double s12, double s13,
+                                                  bool* ok) {
         const DalDesc& D = A.dal;
         constexpr int KK = (K > 0 ? K : 1);
         const double s23 = (D.mss - s12) - s13;
@@ -409,9 +410,14 @@ struct EvDalitz {
             ti = fma(w, fma(-T.cim, sv[k], T.beta), ti);
         }
         const double I = fma(tr, tr, ti * ti);
-        const double p = I * A.inv_norm;
-        good &= (p > 1e-300) && (p < 1e300);
         *ok = good;
+        return I * A.inv_norm;
+    }
+
+    __device__ static __forceinline__ double one(const NllArgs& A, double s12, double s13,
+                                                 bool* ok) {
+        const double p = prob(A, s12, s13, ok);
+        *ok = *ok && (p > 1e-300) && (p < 1e300);
         return -log(p);
     }
 
@@ -423,6 +429,15 @@ struct EvDalitz {
         t.y = one(A, x[0].y, x[1].y, &ok1);
         bad |= !ok0 || (nvalid > 1 && !ok1);
         return t;
+    }
+
+    // product-mode interface (pfb_nll_prod.cuh)
+    __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[2], bool& okx,
+                                                    bool& oky) {
+        double2 p;
+        p.x = prob(A, x[0].x, x[1].x, &okx);
+        p.y = prob(A, x[0].y, x[1].y, &oky);
+        return p;
     }
 };
 
@@ -623,6 +638,40 @@ enum KernelMode : int32_t {
     MODE_ACCUM = 2        // chained launches: keep accumulating
 };
 
+// Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and
+// resets the launch-scoped counters.  Shared by every fast kernel.
+template <bool LIST>
+__device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc, unsigned int* s_last) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x)
+        if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!*s_last) return;
+    if (threadIdx.x == 0) *A.work_counter = 0ull;
+    if (A.mode == MODE_ACCUM) {
+        if (threadIdx.x == 0) *A.ticket = 0u;
+        return;
+    }
+    __threadfence();
+    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) {
+        const long long v = (long long)atomicExch(A.acc + i, 0ull);
+        if (A.mode == MODE_EXPORT)
+            A.acc_out[i] = v;
+        else
+            A.acc_out[i] += v;
+    }
+    if (threadIdx.x == 0) {
+        *A.ticket = 0u;
+        if (!LIST) {  // hand the deferred-block count to the fix-up launch
+            A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
+        }
+        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
+    }
+}
+
 template <int P, class Ev, bool LIST>
 __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_kernel(const __grid_constant__ NllArgs A) {
     constexpr int NC = Ev::NC;
@@ -786,35 +835,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_kernel(const __grid_co
         }
     }
 
-    // ---- flush the CTA accumulator; the last CTA exports and resets ----------
-    __syncthreads();
-    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x)
-        if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-    __syncthreads();
-    if (!s_last) return;
-    if (tid == 0) *A.work_counter = 0ull;
-    if (A.mode == MODE_ACCUM) {
-        if (tid == 0) *A.ticket = 0u;
-        return;
-    }
-    __threadfence();
-    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) {
-        const long long v = (long long)atomicExch(A.acc + i, 0ull);
-        if (A.mode == MODE_EXPORT)
-            A.acc_out[i] = v;
-        else
-            A.acc_out[i] += v;
-    }
-    if (tid == 0) {
-        *A.ticket = 0u;
-        if (!LIST) {  // hand the deferred-block count to the fix-up launch
-            A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
-        }
-        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
-    }
+    finish_launch<LIST>(A, sacc, &s_last);
 }
 
 // ---------------------------------------------------------------------------

@@ -2,6 +2,7 @@
 // Shape-specialised (exact leaf/term counts and leaf kinds) for the common
 // trees -- streamed through the TMA pipeline -- and a generic instantiation
 // (<= 4 leaves, <= 4 terms) on the SIMT kernel for the rest.
+#include "pfb_nll_prod.cuh"
 #include "pfb_nll_tma.cuh"
 
 namespace pfb {
@@ -24,6 +25,16 @@ bool sop_batched_in_kernel(const NllArgs& A, int nc) {
     return false;
 }
 
+// EvSum2GE's fixed layout (leaf 0 gaussian, leaf 1 exponential, term t =
+// leaf t alone) and |ln c_t| < 200 (see EvSum2GE).
+static bool sum2ge_ok(const NllArgs& A) {
+    if (A.leaf[0].voff != 0 || A.leaf[1].voff != 2) return false;
+    if (A.term[0].emask != 1u || A.term[1].emask != 2u || A.term[0].vmask || A.term[1].vmask) return false;
+    for (int t = 0; t < 2; ++t)
+        if (!(fabs(A.term[t].logcoef) < 200.0)) return false;
+    return true;
+}
+
 template <class Ev>
 static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.tma) return launch_tma<Ev>(A, stream, sm_count);
@@ -33,9 +44,12 @@ static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_c
 cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
     const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
     if (nc == 1) {
-        // SumPdf(gaussian, exponential): C1 / C5.  FP64-bound (one exp and
-        // one log per event): the SIMT kernel's 24 warps/SM beat the TMA
-        // pipeline's 16 consumer warps (kernel_sweep, round 1).
+        // SumPdf(gaussian, exponential): C1 / C5.  FP64-bound: product mode
+        // (two exp per event, one log per 16 events) on the SIMT streaming
+        // kernel; the log-domain kernel (one exp + one log per event) when
+        // the pipeline is off or the shape's preconditions do not hold.
+        if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A))
+            return launch_prod<EvSum2GE>(A, stream, sm_count);
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2))
             return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);
         if (nl == 1 && nt == 1 && kinds == kG)
