@@ -433,7 +433,7 @@ struct EvDalitz {
 
     // product-mode interface (pfb_nll_prod.cuh)
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[2], bool& okx,
-                                                    bool& oky) {
+                                                    bool& oky, const double*, double2&) {
         double2 p;
         p.x = prob(A, x[0].x, x[1].x, &okx);
         p.y = prob(A, x[0].y, x[1].y, &oky);

@@ -4,22 +4,24 @@
 // costs exponentials anyway (SumPdf C1/C5, Dalitz C3/C4) the kernel evaluates
 // p_i in the linear domain -- the reference's own formula, pdf.py:205-227 /
 // dalitz.py:217-230 -- and multiplies: one log per 16 events instead of one
-// per event.
+// per event.  An evaluator may factor p_i = exp(l_i) q_i; then q_i enters the
+// product and l_i a plain sum (C1: l = alpha x, one exponential per event).
 //
 // Canonical structure of one 4096-event block (independent of warps per
 // block P, of grid size and of GPU count, so every invariance the reference
 // tests -- serial == pool == shards -- holds bit for bit):
 //   row r = e / 64 (64 rows), column = e % 64, thread column = 2*lane + {0,1};
 //   unit u = rows [8u, 8u+8) x one lane's 2 columns = 16 events;
-//   unit value  v(u, lane) = -(ln m + ex ln 2)  with  m 2^ex = prod p  (rows in
-//   ascending order, x then y, renormalised to m in [1, 2) after every row);
+//   unit value  v(u, lane) = -(ln m + L + ex ln 2)  with  m 2^ex = prod q
+//   and L = sum l (rows in ascending order, x then y; m renormalised to
+//   [1, 2) after every row);
 //   block value = lane tree (shuffle-down 16..1) of the unit tree
 //   ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)).
-// A ragged tail block uses the same structure with p = 1 for absent events.
+// A ragged tail block uses the same structure with q = 1 for absent events.
 //
-// Guard: an event is certified when its p lies in [2^-500, 2^500] (so every
-// partial product is a normal double and the reference's p is far from 0 and
-// inf) and the evaluator reports no out-of-range intermediate.  A block with
+// Guard: an event is certified when its q lies in [2^-500, 2^500] (so every
+// partial product is a normal double) and the evaluator's own conditions
+// hold (p far from 0 and inf, no out-of-range intermediate).  A block with
 // any uncertified event is deferred to the exact fix-up launch (literal
 // reference arithmetic, reference errors) exactly like the log-domain kernel.
 //
@@ -35,7 +37,7 @@ namespace pfb {
 static constexpr double kLn2Hi = 6.93147180369123816490e-01;
 static constexpr double kLn2Lo = 1.90821492927058770002e-10;
 
-// p in [2^-500, 2^500]: biased exponent in [523, 1523]; 0, subnormal, negative,
+// q in [2^-500, 2^500]: biased exponent in [523, 1523]; 0, subnormal, negative,
 // inf and NaN all fail.
 __device__ __forceinline__ bool p_in_range(double p) {
     const int hi = __double2hiint(p);
@@ -49,29 +51,76 @@ __device__ __forceinline__ void renorm(double& m, int& ex) {
     m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(m));
 }
 
-// SumPdf(gaussian, exponential) on one column (C1 / C5), linear domain:
-//   p = c0 exp((-0.5 z) z) + c1 exp(alpha x),  z = (x - mu) / sigma,
-//   c_t = weight_t / (norm_t * norm_root)  (pdf.py:122-127, 141-144, 205-219).
+// 2^(j/16), j = 0..15, correctly rounded.  Kept in shared memory: 16 doubles
+// fill the 32 banks once, so any lane pattern reads conflict-free.
+__constant__ static double kExp2Tab[16] = {
+    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
+    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
+    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
+// 16/ln2, ln2/16 split hi (32 significant bits: kd * hi exact) + lo, and the
+// Taylor coefficients 1/n! (read as constant-bank operands, no per-use moves).
+__constant__ static double kExpK[9] = {
+    23.083120654223414, 0x1.62e42fee00000p-5, 0x1.a39ef35793c76p-37,
+    1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
+
+// exp(x) for x in [-707, 707] (callers clamp): x = k ln2/16 + r, |r| <= ln2/32;
+// exp(r) by its degree-6 Taylor polynomial (truncation < 2^-52), times
+// 2^(k mod 16 / 16) from the table, times 2^(k div 16) by exponent addition.
+// <= 3 ulp; 11 FP64 operations against ~17 plus a range branch for exp().
+__device__ __forceinline__ double exp_tab(double x, const double* tab) {
+    const double t = fma(x, kExpK[0], 0x1.8p52);
+    const int k = __double2loint(t);
+    const double kd = t - 0x1.8p52;
+    double r = fma(kd, -kExpK[1], x);
+    r = fma(kd, -kExpK[2], r);
+    double q = fma(r, kExpK[3], kExpK[4]);
+    q = fma(q, r, kExpK[5]);
+    q = fma(q, r, kExpK[6]);
+    q = fma(q, r, kExpK[7]);
+    q = fma(q, r, kExpK[8]);
+    q = fma(q, r, 1.0);
+    const double v = q * tab[k & 15];
+    return __hiloint2double(__double2hiint(v) + ((k >> 4) << 20), __double2loint(v));
+}
+
+// SumPdf(gaussian, exponential) on one column (C1 / C5):
+//   p = c0 exp(u0) + c1 exp(u1),  u0 = (-0.5 z) z,  z = (x - mu) / sigma,
+//   u1 = alpha x,  c_t = weight_t / (norm_t * norm_root)
+//   (pdf.py:122-127, 141-144, 205-219), factored as
+//   p = exp(u1) * q,  q = c1 + c0 exp(u0 - u1):
+// one exponential per event; u1 goes into the unit's sum, q into its product.
 // Leaf/term layout fixed by the dispatcher: leaf 0 gaussian (ptv[0][0..1] =
-// mu, 1/sigma), leaf 1 exponential (ptv[0][2] = alpha), term t = leaf t.
-// A subnormal term is negligible next to a certified p when |ln c_t| < 200
-// (checked by the dispatcher), so no per-leaf guard is needed.
+// mu, 1/sigma), leaf 1 exponential (ptv[0][2] = alpha), term t = leaf t, and
+// |ln c_t| < 200.
+// Certification: |u1| <= 250 and q in [2^-500, 2^500] (kernel check) put p
+// in [2^-861, 2^861] and keep the reference's exp(u1) finite and normal; a
+// subnormal exp(u0) in the reference is then below 2^-84 p (negligible).
+// d = u0 - u1 <= -u1 <= 250 for a certified event (u0 <= 0) and is clamped
+// below at -707 (then c0 e^d < 2^-700 c1, negligible); whatever exp_tab
+// returns for an uncertified event (NaN d, d > 707) is discarded.
 struct EvSum2GE {
     static constexpr int NC = 1;
     static constexpr int U = 4;
     static constexpr int MINB = 3;
 
-    __device__ static __forceinline__ double one(const NllArgs& A, double x) {
+    __device__ static __forceinline__ double one(const NllArgs& A, double x, const double* tab, bool& ok,
+                                                 double& l) {
         const double z = (x - A.ptv[0][0]) * A.ptv[0][1];
-        const double g = exp((-0.5 * z) * z);
-        const double e = exp(A.ptv[0][2] * x);
-        return fma(A.term[0].coef, g, A.term[1].coef * e);
+        const double u1 = A.ptv[0][2] * x;
+        double d = (-0.5 * z) * z - u1;
+        d = d < -707.0 ? -707.0 : d;
+        ok = fabs(u1) <= 250.0;  // certified => d <= 250: no upper clamp
+        l = u1;
+        return fma(A.term[0].coef, exp_tab(d, tab), A.term[1].coef);
     }
 
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[1], bool& okx,
-                                                    bool& oky) {
-        okx = oky = true;
-        return make_double2(one(A, x[0].x), one(A, x[0].y));
+                                                    bool& oky, const double* tab, double2& l) {
+        double2 q;
+        q.x = one(A, x[0].x, tab, okx, l.x);
+        q.y = one(A, x[0].y, tab, oky, l.y);
+        return q;
     }
 };
 
@@ -82,12 +131,12 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
     constexpr int GROUPS = kThreads / (32 * P);
     constexpr int ROWS = 64 / P;  // rows per warp
     constexpr int W = Ev::U;      // row loads kept in flight
-    static_assert(W <= ROWS, "window");
+    static_assert(W <= ROWS && 8 % W == 0, "window");
 
-    __shared__ double xch[GROUPS][8][32];
-    __shared__ int xbad[GROUPS][P];
-    __shared__ long long s_item[GROUPS];
+    __shared__ double xch[2][GROUPS][8][32];  // unit values, double-buffered by item parity
+    __shared__ int xbad[2][GROUPS][P];
     __shared__ long long sacc[PFB_ACC_WORDS];
+    __shared__ double s_tab[16];
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
@@ -96,104 +145,164 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
     const int grp = warp / P;
     const int wig = warp % P;
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
+    if (tid < 16) s_tab[tid] = kExp2Tab[tid];
     __syncthreads();
 
+    // Static round-robin items (every block costs the same): the next item is
+    // known in advance, so its first rows stream in while the current item's
+    // last rows compute, and one group barrier per item suffices.  Item 0 is
+    // the ragged tail (if any).
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    const int64_t stride = (int64_t)gridDim.x * GROUPS;
     const int r0 = wig * ROWS;
-    for (;;) {
-        if (wig == 0 && lane == 0) s_item[grp] = (long long)atomicAdd(A.work_counter, 1ull);
-        group_sync<P>(grp);
-        const int64_t it = s_item[grp];
-        group_sync<P>(grp);
-        if (it >= nitems) break;
-        const bool is_tail = A.tail && it == 0;
-        const int64_t bidx = is_tail ? A.nfull : it - (A.tail ? 1 : 0);
-        const int64_t lbase = bidx * (int64_t)kBlock;
-        const int n = is_tail ? A.tail : kBlock;
-        const double* col[NC];
+    struct Item {
+        int64_t off;  // A.begin + first event of the block
+        int64_t bidx;
+        int n;
+        bool tail;
+    };
+    auto item_of = [&](int64_t it, Item& I) {
+        I.tail = A.tail && it == 0;
+        I.bidx = I.tail ? A.nfull : it - (A.tail ? 1 : 0);
+        I.n = I.tail ? A.tail : kBlock;
+        I.off = A.begin + I.bidx * (int64_t)kBlock;
+    };
+    auto load_full = [&](const Item& I, int row, double2 (&dst)[NC]) {
+        const int64_t e = I.off + row * 64 + 2 * lane;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) col[c] = A.col[c] + A.begin + lbase;
-
-        auto load = [&](int row, double2 (&dst)[NC]) {
-            const int e = row * 64 + 2 * lane;
-            if (!is_tail || e + 1 < n) {
+        for (int c = 0; c < NC; ++c) dst[c] = ld2(A.col[c] + e);
+    };
+    auto load = [&](const Item& I, int row, double2 (&dst)[NC]) {
+        if (!I.tail || row * 64 + 2 * lane + 1 < I.n) {
+            load_full(I, row, dst);
+        } else {  // ragged tail: a lone last event, or a stand-in (masked below)
+            const int64_t e = I.off + row * 64 + 2 * lane;
+            const int64_t j = row * 64 + 2 * lane < I.n ? e : I.off;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) dst[c] = ld2(col[c] + e);
-            } else {  // ragged tail: a lone last event, or a stand-in (masked below)
-                const int j = e < n ? e : 0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    const double v = __ldg(col[c] + j);
-                    dst[c] = make_double2(v, v);
-                }
+            for (int c = 0; c < NC; ++c) {
+                const double v = __ldg(A.col[c] + j);
+                dst[c] = make_double2(v, v);
             }
-        };
+        }
+    };
 
-        double2 win[W][NC];
+    int64_t it = (int64_t)blockIdx.x * GROUPS + grp;
+    Item cur_item, next_item;
+    double2 win[W][NC];
+    if (it < nitems) {
+        item_of(it, cur_item);
 #pragma unroll
-        for (int q = 0; q < W; ++q) load(r0 + q, win[q]);
-        double m = 1.0;
-        int ex = 0;
+        for (int q = 0; q < W; ++q) load(cur_item, r0 + q, win[q]);
+    }
+    int par = 0;
+    for (; it < nitems; it += stride, par ^= 1) {
+        const bool has_next = it + stride < nitems;
+        if (has_next) item_of(it + stride, next_item);
         bool bad = false;
-#pragma unroll 1
-        for (int i = 0; i < ROWS; ++i) {
-            double2 cur[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) cur[c] = win[0][c];
-#pragma unroll
-            for (int q = 0; q + 1 < W; ++q)
-#pragma unroll
-                for (int c = 0; c < NC; ++c) win[q][c] = win[q + 1][c];
-            if (i + W < ROWS) load(r0 + i + W, win[W - 1]);
+        // One row: evaluate, mask absent tail events (TAIL only), certify,
+        // multiply.  p = exp(l) * q: q goes into the product, l into a sum.
+        // (TAIL is a literal at both call sites; inlining folds it)
+        auto row = [&](const double2 (&x)[NC], int i, double& m, int& ex, double& ls, const bool TAIL) {
             bool okx, oky;
-            double2 p = Ev::prob2(A, cur, okx, oky);
-            if (is_tail) {
+            double2 l = make_double2(0.0, 0.0);
+            double2 q = Ev::prob2(A, x, okx, oky, s_tab, l);
+            if (TAIL) {
                 const int e = (r0 + i) * 64 + 2 * lane;
-                if (e >= n) {
-                    p.x = 1.0;
+                if (e >= cur_item.n) {
+                    q.x = 1.0;
+                    l.x = 0.0;
                     okx = true;
                 }
-                if (e + 1 >= n) {
-                    p.y = 1.0;
+                if (e + 1 >= cur_item.n) {
+                    q.y = 1.0;
+                    l.y = 0.0;
                     oky = true;
                 }
             }
-            bad |= !(okx && oky && p_in_range(p.x) && p_in_range(p.y));
-            m = (m * p.x) * p.y;
+            ls = (ls + l.x) + l.y;
+            bad |= !(okx && oky && p_in_range(q.x) && p_in_range(q.y));
+            m = (m * q.x) * q.y;
             renorm(m, ex);
-            if ((i & 7) == 7) {
-                const double fe = (double)ex;
-                xch[grp][(r0 + i) >> 3][lane] = -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(m)));
-                m = 1.0;
-                ex = 0;
+        };
+        auto unit_value = [&](double m, int ex, double ls) {
+            const double fe = (double)ex;
+            return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(m) + ls));
+        };
+        if (!cur_item.tail) {
+            // 8-row units; rows unrolled so the load window rotates by
+            // register naming (slot r % W holds row r until consumed/refilled)
+#pragma unroll 1
+            for (int ju = 0; ju < ROWS / 8; ++ju) {
+                double m = 1.0, ls = 0.0;
+                int ex = 0;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int i = 8 * ju + r;
+                    double2 cur[NC];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) cur[c] = win[r % W][c];
+                    if (i + W < ROWS)
+                        load_full(cur_item, r0 + i + W, win[r % W]);
+                    else if (has_next)
+                        load_full(next_item, r0 + i + W - ROWS, win[r % W]);
+                    row(cur, i, m, ex, ls, false);
+                }
+                xch[par][grp][(r0 >> 3) + ju][lane] = unit_value(m, ex, ls);
+            }
+        } else {
+            // the ragged tail block (once per launch): same structure, rolled
+            double m = 1.0, ls = 0.0;
+            int ex = 0;
+#pragma unroll 1
+            for (int i = 0; i < ROWS; ++i) {
+                double2 cur[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) cur[c] = win[0][c];
+#pragma unroll
+                for (int q = 0; q + 1 < W; ++q)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) win[q][c] = win[q + 1][c];
+                if (i + W < ROWS)
+                    load(cur_item, r0 + i + W, win[W - 1]);
+                else if (has_next)
+                    load_full(next_item, r0 + i + W - ROWS, win[W - 1]);
+                row(cur, i, m, ex, ls, true);
+                if ((i & 7) == 7) {
+                    xch[par][grp][(r0 + i) >> 3][lane] = unit_value(m, ex, ls);
+                    m = 1.0;
+                    ls = 0.0;
+                    ex = 0;
+                }
             }
         }
         const unsigned anybad = __any_sync(0xffffffffu, bad);
-        if (lane == 0) xbad[grp][wig] = anybad ? 1 : 0;
-        group_sync<P>(grp);
-        bad = false;
+        if (lane == 0) xbad[par][grp][wig] = anybad ? 1 : 0;
+        group_sync<P>(grp);  // the only barrier per item (buffers alternate)
+        if (wig == 0) {
+            bad = false;
 #pragma unroll
-        for (int w = 0; w < P; ++w) bad |= xbad[grp][w] != 0;
-        double bsum = 0.0;
-        if (wig == 0 && !bad) {
-            double v[8];
+            for (int w = 0; w < P; ++w) bad |= xbad[par][grp][w] != 0;
+            double bsum = 0.0;
+            if (!bad) {
+                double v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = xch[grp][u][lane];
-            double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+                for (int u = 0; u < 8; ++u) v[u] = xch[par][grp][u][lane];
+                double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
 #pragma unroll
-            for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
-            bsum = T;
-        }
-        group_sync<P>(grp);  // xch / xbad reused by the next item
-        if (wig == 0 && lane == 0) {
-            if (bad) {  // defer the whole block to the exact fix-up launch
-                const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
-                A.fix_list[slot] = (A.block_base + bidx) * kMaxPts + A.fix_point;
-            } else {
-                if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
-                acc_add_shared(sacc, bsum);
+                for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
+                bsum = T;
+            }
+            if (lane == 0) {
+                if (bad) {  // defer the whole block to the exact fix-up launch
+                    const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
+                    A.fix_list[slot] = (A.block_base + cur_item.bidx) * kMaxPts + A.fix_point;
+                } else {
+                    if (A.block_sums) A.block_sums[A.block_base + cur_item.bidx] = bsum;
+                    acc_add_shared(sacc, bsum);
+                }
             }
         }
+        if (has_next) cur_item = next_item;
     }
     finish_launch<false>(A, sacc, &s_last);
 }

@@ -1,0 +1,3 @@
+set -x
+timeout 600 python scripts/kernel_sweep.py --configs c1 --warps 0 --n 100000000 --reps 5 > gpurun_out/sweep15_100m.log 2>&1; cat gpurun_out/sweep15_100m.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:nll_prod -s 3 -c 1 -o gpurun_out/prof_c1q python scripts/kernel_sweep.py --configs c1 --warps 0 --reps 2 > gpurun_out/ncu_c1q.log 2>&1; echo "ncu rc=$?"
