@@ -295,7 +295,7 @@ def main():
             flush.sum()  # evict L2 (126 MB, clean lines) so every step streams from HBM
             # keep the stream busy while the host prepares the launch, so the
             # CUDA events around the kernel time the kernel, not launch latency
-            torch.cuda._sleep(200_000)
+            torch.cuda._sleep(2_000_000)
             ms, nll_value = step_local()
             kernel_ms.append(ms)
         torch.cuda.synchronize()

@@ -135,8 +135,12 @@ void* pfb_ctx_stream(pfb_ctx* ctx);
 int pfb_ctx_synchronize(pfb_ctx* ctx);
 /* Tuning: warps cooperating on one 4096-event block (0 = automatic; 1,2,4,8). */
 int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
-/* Kernel structure for HBM-bound evaluators: 1 (default) the TMA bulk-copy
- * pipeline (producer warp + shared-memory ring), 0 the SIMT streaming kernel. */
+/* Kernel structure: 1 (default) bulk-copy pipelines where available (the
+ * TMA producer/consumer kernel for HBM-bound evaluators, the product-mode
+ * kernel for exponential- and Dalitz-bound ones, with per-warp bulk
+ * prefetch for single-column models); 2 as 1 with per-warp bulk prefetch
+ * for every product-mode evaluator; 0 the SIMT log-domain streaming kernel.
+ * Results are identical within each mode's documented block structure. */
 int pfb_ctx_set_pipeline(pfb_ctx* ctx, int mode);
 /* Number of engine kernels launched on this context since creation. */
 int pfb_ctx_launch_count(pfb_ctx* ctx, int64_t* out);

@@ -276,7 +276,7 @@ int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
 }
 
 int pfb_ctx_set_pipeline(pfb_ctx* c, int mode) {
-    if (!c || mode < 0 || mode > 1) return PFB_E_INVALID_ARGUMENT;
+    if (!c || mode < 0 || mode > 2) return PFB_E_INVALID_ARGUMENT;
     c->pipeline = mode;
     return PFB_OK;
 }
@@ -743,8 +743,7 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     A->evaluator = p->evaluator;
     // one 4096-event block per 8-warp group: measured fastest for every
     // evaluator at 1M-10M events (scripts/kernel_sweep.py)
-    const int warps = c->warps_override ? c->warps_override : 8;
-    A->warps = warps;
+    A->warps = c->warps_override;  // 0: the evaluator's default kernel shape
     A->tma = c->pipeline;
     A->acc = c->acc;
     A->ticket = c->ticket;
@@ -1330,8 +1329,7 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->tail = (int32_t)(n % kBlock);
     A->evaluator = 100;
     A->npts = 1;
-    const int warps = c->warps_override ? c->warps_override : 8;
-    A->warps = warps;
+    A->warps = c->warps_override;  // 0: the evaluator's default kernel shape
     A->tma = c->pipeline;
     A->acc = c->acc;
     A->ticket = c->ticket;

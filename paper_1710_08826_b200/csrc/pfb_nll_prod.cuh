@@ -29,7 +29,7 @@
 // <= 16 u, i.e. an absolute error <= 4e-15 in each unit's -ln -- orders of
 // magnitude inside the 1e-10 relative NLL tolerance.
 #pragma once
-#include "pfb_nll_kernel.cuh"
+#include "pfb_nll_tma.cuh"
 
 namespace pfb {
 
@@ -124,6 +124,37 @@ struct EvSum2GE {
     }
 };
 
+// One row of a unit: evaluate two events (local block indices e, e+1),
+// mask absent tail events (TAIL), certify, multiply q into m * 2^ex, add l.
+template <class Ev, bool TAIL>
+__device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev::NC], int e, int n, double& m,
+                                         int& ex, double& ls, bool& bad, const double* tab) {
+    bool okx, oky;
+    double2 l = make_double2(0.0, 0.0);
+    double2 q = Ev::prob2(A, x, okx, oky, tab, l);
+    if (TAIL) {
+        if (e >= n) {
+            q.x = 1.0;
+            l.x = 0.0;
+            okx = true;
+        }
+        if (e + 1 >= n) {
+            q.y = 1.0;
+            l.y = 0.0;
+            oky = true;
+        }
+    }
+    bad |= !(okx && oky && p_in_range(q.x) && p_in_range(q.y));
+    ls = (ls + l.x) + l.y;
+    m = (m * q.x) * q.y;
+    renorm(m, ex);
+}
+
+__device__ __forceinline__ double unit_value(double m, int ex, double ls) {
+    const double fe = (double)ex;
+    return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(m) + ls));
+}
+
 template <int P, class Ev>
 __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __grid_constant__ NllArgs A) {
     static_assert(P == 1 || P == 2 || P == 4 || P == 8, "P");
@@ -199,35 +230,6 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
         const bool has_next = it + stride < nitems;
         if (has_next) item_of(it + stride, next_item);
         bool bad = false;
-        // One row: evaluate, mask absent tail events (TAIL only), certify,
-        // multiply.  p = exp(l) * q: q goes into the product, l into a sum.
-        // (TAIL is a literal at both call sites; inlining folds it)
-        auto row = [&](const double2 (&x)[NC], int i, double& m, int& ex, double& ls, const bool TAIL) {
-            bool okx, oky;
-            double2 l = make_double2(0.0, 0.0);
-            double2 q = Ev::prob2(A, x, okx, oky, s_tab, l);
-            if (TAIL) {
-                const int e = (r0 + i) * 64 + 2 * lane;
-                if (e >= cur_item.n) {
-                    q.x = 1.0;
-                    l.x = 0.0;
-                    okx = true;
-                }
-                if (e + 1 >= cur_item.n) {
-                    q.y = 1.0;
-                    l.y = 0.0;
-                    oky = true;
-                }
-            }
-            ls = (ls + l.x) + l.y;
-            bad |= !(okx && oky && p_in_range(q.x) && p_in_range(q.y));
-            m = (m * q.x) * q.y;
-            renorm(m, ex);
-        };
-        auto unit_value = [&](double m, int ex, double ls) {
-            const double fe = (double)ex;
-            return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(m) + ls));
-        };
         if (!cur_item.tail) {
             // 8-row units; rows unrolled so the load window rotates by
             // register naming (slot r % W holds row r until consumed/refilled)
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                         load_full(cur_item, r0 + i + W, win[r % W]);
                     else if (has_next)
                         load_full(next_item, r0 + i + W - ROWS, win[r % W]);
-                    row(cur, i, m, ex, ls, false);
+                    prod_row<Ev, false>(A, cur, 0, kBlock, m, ex, ls, bad, s_tab);
                 }
                 xch[par][grp][(r0 >> 3) + ju][lane] = unit_value(m, ex, ls);
             }
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                     load(cur_item, r0 + i + W, win[W - 1]);
                 else if (has_next)
                     load_full(next_item, r0 + i + W - ROWS, win[W - 1]);
-                row(cur, i, m, ex, ls, true);
+                prod_row<Ev, true>(A, cur, (r0 + i) * 64 + 2 * lane, cur_item.n, m, ex, ls, bad, s_tab);
                 if ((i & 7) == 7) {
                     xch[par][grp][(r0 + i) >> 3][lane] = unit_value(m, ex, ls);
                     m = 1.0;
@@ -307,6 +309,199 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
     finish_launch<false>(A, sacc, &s_last);
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy variant (single-column evaluators).  Same canonical block
+// structure with P = 8 (warp w owns unit w = rows [8w, 8w+8), i.e. the
+// contiguous 4 KB [512w, 512w+512) of every block).  Each warp streams its
+// next item's 4 KB with one cp.async.bulk into a private double buffer in
+// shared memory (own mbarrier per buffer), so a whole item of prefetch is in
+// flight per warp without spending registers on it, and reads its rows back
+// with conflict-free 16-byte shared loads.
+constexpr int kBulkWarps = 8;
+constexpr int kUnitEvents = 512;  // events per warp per item
+constexpr int kRing = 4;          // block-fold slots (warps may drift this many items)
+
+template <class T>
+__device__ __forceinline__ T ld_volatile(const T* p) {
+    return *reinterpret_cast<const volatile T*>(p);
+}
+template <class T>
+__device__ __forceinline__ void st_volatile(T* p, T v) {
+    *reinterpret_cast<volatile T*>(p) = v;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <class Ev>
+__global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid_constant__ NllArgs A) {
+    constexpr int NC = Ev::NC;
+    static_assert(kThreads == 32 * kBulkWarps, "one item per CTA");
+    extern __shared__ __align__(128) double sbuf[];  // [8 warps][2 buffers][NC][512]
+    __shared__ unsigned long long bar[kBulkWarps][2];
+    __shared__ double xch[kRing][8][32];
+    __shared__ int xbad[kRing][kBulkWarps];
+    __shared__ unsigned int s_cnt[kRing];
+    __shared__ int s_done[kRing];  // folds completed per slot
+    __shared__ long long sacc[PFB_ACC_WORDS];
+    __shared__ double s_tab[16];
+    __shared__ unsigned int s_last;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int w = tid >> 5;
+    for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
+    if (tid < 16) s_tab[tid] = kExp2Tab[tid];
+    if (tid < kRing) {
+        s_cnt[tid] = 0u;
+        s_done[tid] = 0;
+    }
+    if (lane == 0) {
+        mbar_init(&bar[w][0], 1);
+        mbar_init(&bar[w][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    const int64_t stride = gridDim.x;
+    double* mybuf = sbuf + (int64_t)w * 2 * NC * kUnitEvents;
+    // geometry of item `it` for this warp: first event offset, events present
+    auto issue = [&](int64_t it, int b) {
+        const bool tail = A.tail && it == 0;
+        const int64_t bidx = tail ? A.nfull : it - (A.tail ? 1 : 0);
+        const int n = tail ? A.tail : kBlock;
+        int nw = n - kUnitEvents * w;
+        nw = nw < 0 ? 0 : (nw > kUnitEvents ? kUnitEvents : nw);
+        const unsigned bytes = 8u * (unsigned)(nw & ~1);  // bulk copies move 16 B multiples
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&bar[w][b], bytes * NC);
+            if (bytes) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    bulk_g2s(mybuf + (b * NC + c) * kUnitEvents,
+                             A.col[c] + A.begin + bidx * (int64_t)kBlock + kUnitEvents * w, bytes, &bar[w][b]);
+            }
+        }
+    };
+
+    int64_t it = blockIdx.x;
+    if (it < nitems) issue(it, 0);
+    int j = 0;  // items processed by this CTA
+    for (; it < nitems; it += stride, ++j) {
+        const int b = j & 1;
+        const bool has_next = it + stride < nitems;
+        if (has_next) {
+            // buffer b^1 was last read in item j-1 (program order, all lanes)
+            __syncwarp();
+            fence_proxy_async_smem();
+            issue(it + stride, b ^ 1);
+        }
+        mbar_wait(&bar[w][b], (j >> 1) & 1);
+        const double* xb = mybuf + b * NC * kUnitEvents;
+        const bool tail = A.tail && it == 0;
+        const int64_t bidx = tail ? A.nfull : it - (A.tail ? 1 : 0);
+        double m = 1.0, ls = 0.0;
+        int ex = 0;
+        bool bad = false;
+        if (!tail) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double2 x[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    x[c] = *reinterpret_cast<const double2*>(xb + c * kUnitEvents + r * 64 + 2 * lane);
+                prod_row<Ev, false>(A, x, 0, kBlock, m, ex, ls, bad, s_tab);
+            }
+        } else {
+            const int n = A.tail;
+            const int64_t gbase = A.begin + bidx * (int64_t)kBlock;
+#pragma unroll 1
+            for (int r = 0; r < 8; ++r) {
+                const int le = r * 64 + 2 * lane;          // within the warp's 512
+                const int e = kUnitEvents * w + le;        // within the block
+                double2 x[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (e + 1 < n) {
+                        x[c] = *reinterpret_cast<const double2*>(xb + c * kUnitEvents + le);
+                    } else {  // odd last event (not bulk-copied) or a stand-in
+                        const double v = __ldg(A.col[c] + gbase + (e < n ? e : 0));
+                        x[c] = make_double2(v, v);
+                    }
+                }
+                prod_row<Ev, true>(A, x, e, n, m, ex, ls, bad, s_tab);
+            }
+        }
+        // No barrier: every warp posts its unit value into ring slot j % R and
+        // the last of the 8 to arrive folds the block (warps never wait for
+        // each other; a warp R items ahead waits for the slot to be folded).
+        const int slot = j % kRing;
+        if (lane == 0)
+            while (ld_volatile(&s_done[slot]) < j / kRing) __nanosleep(32);
+        __syncwarp();
+        xch[slot][w][lane] = unit_value(m, ex, ls);
+        const unsigned anybad = __any_sync(0xffffffffu, bad);
+        unsigned arrived = 0;
+        if (lane == 0) {
+            xbad[slot][w] = anybad ? 1 : 0;
+            __threadfence_block();
+            arrived = atomicAdd(&s_cnt[slot], 1u);
+        }
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (arrived == kBulkWarps - 1) {
+            __threadfence_block();
+            bad = false;
+#pragma unroll
+            for (int q = 0; q < kBulkWarps; ++q) bad |= ld_volatile(&xbad[slot][q]) != 0;
+            double bsum = 0.0;
+            if (!bad) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = ld_volatile(&xch[slot][u][lane]);
+                double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+#pragma unroll
+                for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
+                bsum = T;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (bad) {
+                    const unsigned long long fs = atomicAdd(A.fix_counter, 1ull);
+                    A.fix_list[fs] = (A.block_base + bidx) * kMaxPts + A.fix_point;
+                } else {
+                    if (A.block_sums) A.block_sums[A.block_base + bidx] = bsum;
+                    acc_add_shared(sacc, bsum);
+                }
+                s_cnt[slot] = 0u;
+                __threadfence_block();
+                st_volatile(&s_done[slot], j / kRing + 1);
+            }
+        }
+    }
+    finish_launch<false>(A, sacc, &s_last);
+}
+
+template <class Ev>
+static cudaError_t launch_prod_bulk(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    constexpr int NC = Ev::NC;
+    const size_t smem = (size_t)kBulkWarps * 2 * NC * kUnitEvents * sizeof(double);
+    static int occ = 0;
+    if (!occ) {
+        cudaError_t e = cudaFuncSetAttribute(nll_prod_bulk_kernel<Ev>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nll_prod_bulk_kernel<Ev>, kThreads, smem);
+        if (occ < 1) occ = 1;
+    }
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    int64_t grid = (int64_t)sm_count * occ;
+    if (grid > nitems) grid = nitems > 0 ? nitems : 1;
+    nll_prod_bulk_kernel<Ev><<<(unsigned)grid, kThreads, smem, stream>>>(A);
+    return cudaGetLastError();
+}
+
 template <int P, class Ev>
 static cudaError_t launch_prod_one(const NllArgs& A, cudaStream_t stream, int sm_count) {
     static int occ = 0;
@@ -328,6 +523,8 @@ static cudaError_t launch_prod_one(const NllArgs& A, cudaStream_t stream, int sm
 // tuning knob here too.
 template <class Ev>
 static cudaError_t launch_prod(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    // pipeline 1: bulk-copy variant for single-column evaluators; 2: for all
+    if (A.warps == 0 && (A.tma == 2 || (Ev::NC == 1 && A.tma == 1))) return launch_prod_bulk<Ev>(A, stream, sm_count);
     switch (A.warps) {
         case 1:
             return launch_prod_one<1, Ev>(A, stream, sm_count);

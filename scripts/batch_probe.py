@@ -61,7 +61,7 @@ def main():
         times = []
         for r in range(3 + args.reps):
             flush.sum()
-            torch.cuda._sleep(200_000)
+            torch.cuda._sleep(2_000_000)
             L.check(L.lib().pfb_nll_batch(ctx.handle, plan.handle, store, 0, args.n, 0, L.dptr(vals), M,
                                           vals.shape[1], L.dptr(nv), nv.shape[1], L.dptr(out), errs),
                     "pfb_nll_batch")

@@ -60,7 +60,8 @@ def main():
                 ctx.set_warps_per_block(w)
                 times = []
                 for r in range(3 + args.reps):
-                    flush.sum()  # keeps the stream busy: no host-launch gap inside the events
+                    flush.sum()
+                    torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work: the host has enqueued the launch before ev0 runs
                     L.check(L.lib().pfb_terms_block_sums(ctx.handle, L.dptr(terms), n, L.dptr(out),
                                                          ctypes.byref(total)), "terms")
                     if r >= 3:
@@ -89,7 +90,8 @@ def main():
             times = []
             val = None
             for r in range(3 + args.reps):
-                flush.sum()  # keeps the stream busy: no host-launch gap inside the events
+                flush.sum()
+                torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work: the host has enqueued the launch before ev0 runs
                 val = pf.nll(pdf, ds, backend=backend)
                 if r >= 3:
                     times.append(ctx.last_kernel_ms())
