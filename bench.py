@@ -10,7 +10,7 @@ all-reduce of the 72-word integer accumulator).
 
 * value   -- events/s with the events resident in HBM: per-step device time
              of the fused NLL kernel (CUDA events on its stream), L2 flushed
-             (256 MB read) before every step.
+             (256 MB read, pfb_ctx_spin) before every step.
 * e2e     -- the same metric through the C ABI with host (pinned) columns:
              every step copies the events host->device (chunked, overlapped
              with the kernels) and reads the result back.
@@ -292,10 +292,12 @@ def main():
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            flush.sum()  # evict L2 (126 MB, clean lines) so every step streams from HBM
-            # keep the stream busy while the host prepares the launch, so the
-            # CUDA events around the kernel time the kernel, not launch latency
-            torch.cuda._sleep(2_000_000)
+            # evict L2 (256 MB streaming read > 126 MB L2) and keep every SM
+            # busy ~0.5 ms while the host prepares the launch, so the CUDA
+            # events around the kernel time the kernel, not launch latency
+            # (pfb_ctx_spin: same shared-memory carveout as the NLL kernels,
+            # as in a fit loop where only NLL launches reach the GPU)
+            ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * flush.element_size())
             ms, nll_value = step_local()
             kernel_ms.append(ms)
         torch.cuda.synchronize()

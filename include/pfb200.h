@@ -62,6 +62,7 @@ enum pfb_status {
     PFB_E_NONPOSITIVE_NORM = 6,    /* NonPositiveNorm                    errors.py:71 */
     PFB_E_DEGENERATE_GRID = 7,     /* DegenerateGrid                     errors.py:111 */
     PFB_E_INVALID_SUM = 8,         /* math.fsum ValueError (inf + -inf)  */
+    PFB_E_NONPOSITIVE_EXPECTATION = 9, /* NonPositiveExpectation(bin, value) errors.py:102 */
     PFB_E_INVALID_ARGUMENT = 20,
     PFB_E_UNSUPPORTED_PLAN = 21,
     PFB_E_CUDA = 30,
@@ -222,6 +223,25 @@ int pfb_acc_round(const int64_t* acc, double* out);
 /* Add values to a host accumulator (same digit split as the device). */
 int pfb_acc_add_host(int64_t* acc, const double* values, int64_t n);
 
+/* ---- binned data -------------------------------------------- */
+/* BinnedDataSet.fill (core.py:370-379): histogram events [begin, end) of the
+ * store columns cols[0..naxes) into contents[prod(nbins)] (host, row-major,
+ * last axis fastest), adding each bin's count.  Per event and axis the bin is
+ * clip(int64(floor((x - lower) / width)), 0, nbins - 1) with numpy's cast
+ * semantics (NaN / inf -> INT64_MIN -> bin 0): bit-exact. */
+int pfb_bin_fill(pfb_ctx* ctx, const pfb_store* store, int64_t begin, int64_t end, int32_t naxes,
+                 const int32_t* cols, const double* lower, const double* width, const int64_t* nbins,
+                 double* inout_contents);
+/* binned_nll (engine.py:246-276): sum_b [nu_b - n_b ln nu_b] (observed bins;
+ * nu_b otherwise), nu_b = (total * p(centre_b)) * volume, with p from the
+ * literal interpreter on `centers` (one row per bin, the plan's column order)
+ * and the sum exact (math.fsum).  Errors: the node kernels' (as pfb_nll, index
+ * = bin), FractionOutOfRange, then PFB_E_NONPOSITIVE_EXPECTATION (index = first
+ * observed bin with nu <= 0, value = nu). */
+int pfb_binned_nll(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* centers, const double* contents,
+                   int64_t nbins, double total, double volume, const double* values, int32_t nvalues,
+                   const double* norms, int32_t nnorms, double* out_nll, pfb_err* out_err);
+
 /* ---- sharding ------------------------------------------------------------------ */
 /* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */
 int pfb_shard_bounds(int64_t n, int32_t workers, int64_t block, int64_t* bounds);
@@ -260,6 +280,11 @@ int pfb_store_download(pfb_store* st, int32_t col, double* host, int64_t offset,
 
 /* ---- microbenchmarks used for the roofline denominators ------------------------ */
 int pfb_fp64_peak(pfb_ctx* ctx, double* out_tflops);
+/* Timing support (not on the NLL path): on the context stream, read
+ * flush_bytes of flush_buf (a device buffer; L2 eviction) and keep every SM
+ * busy for `cycles` clocks, so that a launch queued behind it is timed
+ * without host-launch latency.  Uses the NLL kernels' shared-memory carveout. */
+int pfb_ctx_spin(pfb_ctx* ctx, int64_t cycles, const double* flush_buf, int64_t flush_bytes);
 
 #ifdef __cplusplus
 }

@@ -386,3 +386,59 @@ def sharded_nll(spec, cols, workers: int, block: int = BLOCK) -> float:
         sh = {name: c[b[k]:b[k + 1]] for name, c in cols.items()}
         sums.extend(block_sums(nll_terms(spec, sh, 0, size, b[k], cache), block).tolist())
     return math.fsum(sums)
+
+
+# --- binned data (core.py:312-379, engine.py:246-276) ---------------------------------
+
+
+def bin_width(lower: float, upper: float, n_bins: int) -> float:
+    """core.py:334-336."""
+    return (upper - lower) / n_bins
+
+
+def bin_centers(axes):
+    """core.py:345-362: axes = [(name, lower, upper, n_bins)], row-major grid."""
+    grids = [np.array([lo + (b + 0.5) * (hi - lo) / nb for b in range(nb)]) for _, lo, hi, nb in axes]
+    mesh = np.meshgrid(*grids, indexing="ij")
+    return {a[0]: m.reshape(-1) for a, m in zip(axes, mesh)}
+
+
+def bin_volume(axes) -> float:
+    """core.py:338-342."""
+    vol = 1.0
+    for _, lo, hi, nb in axes:
+        vol *= bin_width(lo, hi, nb)
+    return vol
+
+
+def fill(axes, cols, contents=None):
+    """core.py:370-379: clip(int64(floor((x - lower) / width)), 0, nb - 1),
+    row-major flat index, np.add.at of 1.0."""
+    total_bins = int(np.prod([a[3] for a in axes]))
+    contents = np.zeros(total_bins) if contents is None else contents
+    n = len(cols[axes[0][0]])
+    idx = np.zeros(n, dtype=np.int64)
+    for name, lo, hi, nb in axes:
+        k = np.floor((cols[name] - lo) / bin_width(lo, hi, nb)).astype(np.int64)
+        np.clip(k, 0, nb - 1, out=k)
+        idx = idx * nb + k
+    np.add.at(contents, idx, 1.0)
+    return contents
+
+
+def binned_nll(spec, axes, contents) -> float:
+    """engine.py:246-276: sum_b nu_b - n_b ln nu_b over the bin centres."""
+    total = float(contents.sum())
+    if total <= 0:
+        raise OracleDensityError("EmptyDataSet")
+    cache: dict = {}
+    dens = spec_eval(spec, bin_centers(axes), cache) / spec_norm_cached(spec, cache)
+    nu = total * dens * bin_volume(axes)
+    observed = contents > 0
+    bad = observed & ~(nu > 0.0)
+    if bad.any():
+        b = int(np.argmax(bad))
+        raise OracleDensityError("NonPositiveExpectation", b, float(nu[b]))
+    terms = nu.copy()
+    terms[observed] -= contents[observed] * np.log(nu[observed])
+    return math.fsum(terms.tolist())

@@ -4,7 +4,8 @@ Public surface mirrors the reference package's names for this path:
 Variable / set_value / snapshot / UnbinnedDataSet (core), gaussian /
 exponential / polynomial / add_pdf / prod_pdf (pdf), DecayChannel /
 ResonanceTerm / dalitz_pdf / compute_integrals / dalitz_norm (dalitz),
-NormalizationStore / resolve_norms / nll (engine), shard / partial_nll /
+NormalizationStore / resolve_norms / nll / binned_nll (engine), BinnedDataSet
+(core), shard / partial_nll /
 reduce_partials / sharded_nll (sharding) -- plus :class:`DeviceBackend`, a
 drop-in ``Backend`` for the reference's own ``nll`` / ``FitManager``.
 
@@ -13,6 +14,7 @@ CPU fallback.
 """
 
 from .core import (
+    BinnedDataSet,
     ParameterRegistry,
     ParameterSnapshot,
     UnbinnedDataSet,
@@ -32,6 +34,7 @@ from .dalitz import (
 from .engine import (
     DeviceBackend,
     NormalizationStore,
+    binned_nll,
     cached_norm,
     device_context,
     nll,
@@ -46,7 +49,7 @@ from .sharding import PartialSum, Shard, ShardedNll, partial_nll, reduce_partial
 __version__ = "0.1.0"
 
 __all__ = [
-    "DecayChannel", "DeviceBackend", "IntegralCache", "NormalizationStore", "NormalizationValue",
+    "BinnedDataSet", "binned_nll", "DecayChannel", "DeviceBackend", "IntegralCache", "NormalizationStore", "NormalizationValue",
     "ParafitError", "ParameterRegistry", "ParameterSnapshot", "PartialSum", "PdfNode", "ResonanceTerm",
     "Shard", "ShardedNll", "UnbinnedDataSet", "Variable", "add_pdf", "cached_norm", "compute_integrals",
     "dalitz_norm", "dalitz_pdf", "device_context", "exponential", "gaussian", "integration_grid", "nll",

@@ -30,6 +30,7 @@ E_EMPTY_DATASET = 5
 E_NONPOSITIVE_NORM = 6
 E_DEGENERATE_GRID = 7
 E_INVALID_SUM = 8
+E_NONPOSITIVE_EXPECTATION = 9
 E_INVALID_ARGUMENT = 20
 E_UNSUPPORTED_PLAN = 21
 E_CUDA = 30
@@ -126,6 +127,10 @@ _SIGNATURES = [
     ("pfb_gen_1d", c_int, [_PTR, c_int32, c_double, c_double, c_double, c_double, c_double, c_double, ctypes.c_uint64, c_int64, _PTR]),
     ("pfb_store_download", c_int, [_PTR, c_int32, _DBL_P, c_int64, c_int64]),
     ("pfb_fp64_peak", c_int, [_PTR, _DBL_P]),
+    ("pfb_ctx_spin", c_int, [_PTR, c_int64, _PTR, c_int64]),
+    ("pfb_bin_fill", c_int, [_PTR, _PTR, c_int64, c_int64, c_int32, _PTR, _PTR, _PTR, _PTR, _PTR]),
+    ("pfb_binned_nll", c_int, [_PTR, _PTR, _PTR, _PTR, c_int64, c_double, c_double, _PTR, c_int32, _PTR, c_int32,
+                               _DBL_P, _PTR]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

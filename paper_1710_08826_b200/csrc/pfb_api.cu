@@ -19,7 +19,15 @@ cudaError_t launch_export(unsigned long long* acc, long long* out, long long* re
                           unsigned long long* fix_counter, unsigned long long* errkey,
                           cudaStream_t stream);
 cudaError_t launch_probe(const NllArgs& A, int64_t j, double* out, cudaStream_t stream);
+cudaError_t launch_bin_fill(const BinAxes& B, int64_t begin, int64_t n, unsigned long long* counts,
+                            cudaStream_t stream, int sm_count);
+cudaError_t launch_binned_nll(const NllArgs& A, const double* contents, int64_t nbins, double total,
+                              double volume, unsigned long long* expkey, cudaStream_t stream, int sm_count);
+cudaError_t launch_binned_probe(const NllArgs& A, int64_t b, double total, double volume, double* out,
+                                cudaStream_t stream);
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
+cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
+                              cudaStream_t stream);
 cudaError_t launch_grid_mask(const GridConsts& g, uint8_t* mask, int* row_count, cudaStream_t st);
 cudaError_t launch_grid_compact(const GridConsts& g, const uint8_t* mask, const int* row_offset,
                                 double* p12, double* p13, cudaStream_t st);
@@ -91,6 +99,10 @@ struct pfb_ctx {
     double* e2e_dev[kMaxCols] = {nullptr, nullptr, nullptr, nullptr};
     int64_t e2e_cap = 0;
     std::vector<cudaEvent_t> chunk_events;
+    // binned data scratch
+    void* bin_dev = nullptr;  // bin counts / contents
+    int64_t bin_cap = 0;      // bytes
+    unsigned long long* bin_key = nullptr;
 };
 
 struct pfb_store {
@@ -243,6 +255,8 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaFree(c->fix_list);
     cudaFree(c->probe_dev);
     cudaFree(c->bsums);
+    cudaFree(c->bin_dev);
+    cudaFree(c->bin_key);
     for (auto& p : c->e2e_dev) cudaFree(p);
     for (auto& e : c->chunk_events) cudaEventDestroy(e);
     cudaFreeHost(c->res_host);
@@ -1665,6 +1679,130 @@ int pfb_fp64_peak(pfb_ctx* c, double* out) {
     const double flops = 2.0 * 16.0 * 8.0 * (double)iters * (double)blocks * threads;
     *out = flops / (ms * 1e-3) / 1e12;
     return PFB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Binned data.
+
+static int ensure_bin(pfb_ctx* c, int64_t bytes) {
+    if (!c->bin_key) CK(cudaMalloc(&c->bin_key, sizeof(unsigned long long)));
+    if (c->bin_cap >= bytes) return PFB_OK;
+    cudaFree(c->bin_dev);
+    c->bin_dev = nullptr;
+    c->bin_cap = 0;
+    CK(cudaMalloc(&c->bin_dev, (size_t)bytes));
+    c->bin_cap = bytes;
+    return PFB_OK;
+}
+
+extern "C" {
+
+int pfb_ctx_spin(pfb_ctx* c, int64_t cycles, const double* flush_buf, int64_t flush_bytes) {
+    if (!c || cycles < 0 || flush_bytes < 0 || (flush_bytes && !flush_buf)) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    CK(launch_spin_flush(cycles, flush_buf, flush_bytes, c->probe_dev, c->sm_count, c->stream));
+    return PFB_OK;
+}
+
+int pfb_bin_fill(pfb_ctx* c, const pfb_store* st, int64_t begin, int64_t end, int32_t naxes,
+                 const int32_t* cols, const double* lower, const double* width, const int64_t* nbins,
+                 double* contents) {
+    if (!c || !st || st->ctx != c || !cols || !lower || !width || !nbins || !contents) return PFB_E_INVALID_ARGUMENT;
+    if (naxes < 1 || naxes > kMaxCols || begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    BinAxes B;
+    memset(&B, 0, sizeof(B));
+    B.naxes = naxes;
+    int64_t total_bins = 1;
+    for (int a = 0; a < naxes; ++a) {
+        if (cols[a] < 0 || cols[a] >= st->ncols || nbins[a] < 1) return PFB_E_INVALID_ARGUMENT;
+        if (total_bins > ((int64_t)1 << 40) / nbins[a]) return PFB_E_INVALID_ARGUMENT;
+        total_bins *= nbins[a];
+        B.col[a] = st->cols[cols[a]];
+        B.lower[a] = lower[a];
+        B.width[a] = width[a];
+        B.nbins[a] = nbins[a];
+    }
+    if (end == begin) return PFB_OK;
+    CK(cudaSetDevice(c->device));
+    int rc = ensure_bin(c, (int64_t)sizeof(unsigned long long) * total_bins);
+    if (rc) return rc;
+    auto* counts = static_cast<unsigned long long*>(c->bin_dev);
+    CK(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * total_bins, c->stream));
+    CK(launch_bin_fill(B, begin, end - begin, counts, c->stream, c->sm_count));
+    ++c->launches;
+    std::vector<unsigned long long> h(total_bins);
+    CK(cudaMemcpyAsync(h.data(), counts, sizeof(unsigned long long) * total_bins, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    // np.add.at adds 1.0 once per event: integral contents (< 2^53) take the
+    // count in one exact addition; anything else repeats the reference's adds.
+    for (int64_t i = 0; i < total_bins; ++i) {
+        if (!h[i]) continue;
+        const double v = contents[i];
+        if (v == floor(v) && fabs(v) < 9007199254740992.0 && h[i] < (1ull << 53)) {
+            contents[i] = v + (double)h[i];
+        } else {
+            double x = v;
+            for (unsigned long long k = 0; k < h[i]; ++k) x += 1.0;
+            contents[i] = x;
+        }
+    }
+    return PFB_OK;
+}
+
+int pfb_binned_nll(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, const double* contents, int64_t nbins,
+                   double total, double volume, const double* values, int32_t nvalues, const double* norms,
+                   int32_t nnorms, double* out_nll, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !contents || !values || !norms || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (nbins < 1 || nbins > st->n) return PFB_E_INVALID_ARGUMENT;
+    for (int s = 0; s < p->nslots; ++s)
+        if (p->slot_col[s] >= st->ncols) return PFB_E_INVALID_ARGUMENT;
+    clear_err(out_err);
+    if (!(total > 0.0)) {
+        if (out_err) out_err->code = PFB_E_EMPTY_DATASET;
+        return PFB_E_EMPTY_DATASET;
+    }
+    CK(cudaSetDevice(c->device));
+    int rc = ensure_bin(c, (int64_t)sizeof(double) * nbins);
+    if (rc) return rc;
+    auto A = std::make_unique<NllArgs>();
+    const int frac = pack_args(p, st, 0, nbins, values, norms, A.get());
+    auto* dcont = static_cast<double*>(c->bin_dev);
+    CK(cudaMemcpyAsync(dcont, contents, sizeof(double) * nbins, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->bin_key, 0xff, sizeof(unsigned long long), c->stream));
+    if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
+    CK(launch_binned_nll(*A, dcont, nbins, total, volume, c->bin_key, c->stream, c->sm_count));
+    ++c->launches;
+    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
+    unsigned long long expkey = ~0ull;
+    CK(cudaMemcpyAsync(&expkey, c->bin_key, sizeof(expkey), cudaMemcpyDeviceToHost, c->stream));
+    rc = read_result(c);
+    if (rc) return rc;
+    pfb_err e;
+    int code = decode_error(c, p, *A, (unsigned long long)c->res_host[1], frac, 0, &e);
+    if (!code && expkey != ~0ull) {
+        CK(launch_binned_probe(*A, (int64_t)expkey, total, volume, c->probe_dev, c->stream));
+        ++c->launches;
+        double nu = 0.0;
+        CK(cudaMemcpyAsync(&nu, c->probe_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        code = PFB_E_NONPOSITIVE_EXPECTATION;
+        e.code = code;
+        e.node = -1;
+        e.index = (int64_t)expkey;
+        e.value = nu;
+    }
+    double r = 0.0;
+    if (!code) code = acc_round(c->res_host + kResHead, &r);
+    e.code = code;
+    if (out_nll) *out_nll = r;
+    if (out_err) *out_err = e;
+    return code;
 }
 
 }  // extern "C"

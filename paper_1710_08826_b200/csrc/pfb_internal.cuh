@@ -154,6 +154,15 @@ struct Gen1D {
     uint32_t seed_lo, seed_hi;
 };
 
+// BinnedDataSet axes for bin_fill_kernel (core.py:339-379).
+struct BinAxes {
+    int32_t naxes;
+    const double* col[kMaxCols];
+    double lower[kMaxCols];
+    double width[kMaxCols];
+    long long nbins[kMaxCols];
+};
+
 // Dalitz integration grid constants (dalitz.py:246-264).
 struct GridConsts {
     int nx, ny;

@@ -84,6 +84,36 @@ cudaError_t launch_probe(const NllArgs& A, int64_t j, double* out, cudaStream_t 
     return cudaGetLastError();
 }
 
+// Measurement support: keeps every SM busy for ~cycles clocks (so a timed
+// launch queued behind it starts without a host-launch gap) and reads `bytes`
+// of a scratch buffer (L2 eviction).  Configured for the maximum shared-memory
+// carveout like the bulk-copy NLL kernels, so no L1/shared reconfiguration
+// separates it from the launch being timed.
+__global__ void spin_flush_kernel(long long cycles, const double2* buf, int64_t n2, double* sink) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = __ldcs(buf + i);
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles) {
+    }
+    if (acc.x + acc.y == 12345.0) sink[0] = acc.x;
+}
+
+cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
+                              cudaStream_t stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(spin_flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        configured = true;
+    }
+    spin_flush_kernel<<<sm_count * 4, 256, 0, stream>>>(cycles, reinterpret_cast<const double2*>(buf),
+                                                         bytes / 16, sink);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream) {
     fp64_peak_kernel<<<blocks, threads, 0, stream>>>(out, iters);
     return cudaGetLastError();

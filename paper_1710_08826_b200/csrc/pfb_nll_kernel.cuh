@@ -66,8 +66,10 @@ __device__ __forceinline__ double dalitz_intensity_literal(const DalDesc& D, dou
 // Literal interpreter: the exact reference evaluation of one event.  Used for
 // trees without a fast evaluator and, per event, whenever a fast evaluator's
 // guard cannot prove that the reference computation is free of underflow,
-// overflow and density errors.  Returns -ln p, or NaN with `rank` set.
-static __device__ __noinline__ double literal_event(const NllArgs& A, int64_t j, int* rank, double* val) {
+// overflow and density errors.  literal_density returns p = root / norm_root
+// (eval_batch(...) / norms[pdf.id], engine.py:181, 265), or NaN with `rank`
+// set when a node kernel raises; literal_event adds the p > 0 check and -ln.
+static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t j, int* rank, double* val) {
     double st[kMaxNodes];
     int sid[kMaxNodes];
     int sp = 0;
@@ -141,7 +143,12 @@ static __device__ __noinline__ double literal_event(const NllArgs& A, int64_t j,
         sid[sp] = o;
         ++sp;
     }
-    const double p = Div(st[0], A.norm[A.nops - 1]);
+    return Div(st[0], A.norm[A.nops - 1]);
+}
+
+static __device__ __forceinline__ double literal_event(const NllArgs& A, int64_t j, int* rank, double* val) {
+    const double p = literal_density(A, j, rank, val);
+    if (*rank >= 0) return p;
     if (!(p > 0.0)) {
         *rank = A.final_rank;
         *val = p;

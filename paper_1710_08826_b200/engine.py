@@ -159,6 +159,12 @@ class DeviceContext:
         L.check(L.lib().pfb_fp64_peak(self.handle, ctypes.byref(out)), "pfb_fp64_peak")
         return out.value
 
+    def spin(self, cycles: int, flush_ptr: int = 0, flush_bytes: int = 0) -> None:
+        """Timing support: L2-evicting read of a device buffer + an SM-wide spin
+        on the context stream (pfb_ctx_spin)."""
+        L.check(L.lib().pfb_ctx_spin(self.handle, int(cycles), ctypes.c_void_p(flush_ptr), int(flush_bytes)),
+                "pfb_ctx_spin")
+
     def close(self) -> None:
         for plan in self._plans.values():
             plan.close()
@@ -206,6 +212,8 @@ def raise_for(err: L.PfbErr, code: int, node, where: str) -> None:
         raise E.EmptyDataSet("cannot evaluate an NLL over zero events")
     if code == L.E_INVALID_SUM:
         raise ValueError("-inf + inf in exact NLL sum")
+    if code == L.E_NONPOSITIVE_EXPECTATION:
+        raise E.NonPositiveExpectation(int(err.index), float(err.value))
     raise L.NativeError(code, where)
 
 
@@ -427,3 +435,37 @@ def nll_block_sums(pdf, columns, snap, norms, start, stop, block=DEFAULT_BLOCK, 
     if block != DEFAULT_BLOCK:
         raise ValueError(f"the device reduction block is fixed at {DEFAULT_BLOCK}")
     return backend.block_sums(pdf, columns, snap, norms, start, stop, offset)
+
+
+def binned_nll(pdf, ds, snap=None, backend=None, store: NormalizationStore | None = None) -> float:
+    """Poisson NLL over bins, sum_b [nu_b - n_b ln nu_b] (reference engine.binned_nll,
+    engine.py:246-276): densities at the bin centres and the exact sum on the GPU
+    (pfb_binned_nll), nu_b = total * p_b * bin volume as the reference computes it."""
+    from .core import snapshot
+
+    total = ds.total
+    if total <= 0:
+        raise error_module_for(pdf).EmptyDataSet("binned dataset has no content")
+    store = store if store is not None else NormalizationStore()
+    if snap is None:
+        snap = snapshot(pdf.param_closure())
+    norms = resolve_norms(pdf, snap, store)
+    device = backend.devices[0] if isinstance(backend, DeviceBackend) else 0
+    ctx = device_context(device)
+    centers = ds.device_centers()
+    needed = sorted({name for node in pdf.walk() for name in node.observable_names()})
+    missing = set(needed) - set(centers)
+    if missing:
+        raise KeyError(f"binned dataset lacks observables {sorted(missing)}")
+    arrays = [centers[name] for name in needed]
+    plan = ctx.plan_for(pdf, tuple(needed))
+    st = ctx.store_for(arrays)
+    vals, nv = plan.pack(snap, norms)
+    contents = np.ascontiguousarray(ds.contents, dtype=np.float64)
+    out = ctypes.c_double()
+    err = L.PfbErr()
+    code = L.lib().pfb_binned_nll(ctx.handle, plan.handle, st, L.dptr(contents), contents.size, float(total),
+                                  float(ds.bin_volume()), L.dptr(vals), len(vals), L.dptr(nv), len(nv),
+                                  ctypes.byref(out), ctypes.byref(err))
+    raise_for(err, code, pdf, "pfb_binned_nll")
+    return out.value

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--cache", type=int, default=0, help="Dalitz lineshape cache mode")
     ap.add_argument("--pipeline", type=int, default=1, help="1: TMA pipeline, 0: SIMT streaming kernel")
+    ap.add_argument("--spin", default="native", choices=["native", "torch"],
+                    help="pre-launch flush + spin: pfb_ctx_spin (same carveout) or torch flush.sum + _sleep")
     args = ap.parse_args()
 
     import torch
@@ -46,6 +48,16 @@ def main():
     L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, args.pipeline), "pfb_ctx_set_pipeline")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     print(json.dumps({"fp64_peak_tflops": ctx.fp64_peak_tflops()}), flush=True)
+
+    def pre():
+        # L2 eviction + ~0.5 ms of GPU work: the host has enqueued the launch
+        # (and its ev0) before the GPU reaches them
+        if args.spin == "native":
+            ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * 4)
+        else:
+            flush.sum()
+            torch.cuda._sleep(1_000_000)
+
     n = args.n
     warps_list = [int(w) for w in args.warps.split(",")]
 
@@ -60,8 +72,7 @@ def main():
                 ctx.set_warps_per_block(w)
                 times = []
                 for r in range(3 + args.reps):
-                    flush.sum()
-                    torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work: the host has enqueued the launch before ev0 runs
+                    pre()
                     L.check(L.lib().pfb_terms_block_sums(ctx.handle, L.dptr(terms), n, L.dptr(out),
                                                          ctypes.byref(total)), "terms")
                     if r >= 3:
@@ -90,8 +101,7 @@ def main():
             times = []
             val = None
             for r in range(3 + args.reps):
-                flush.sum()
-                torch.cuda._sleep(2_000_000)  # ~1 ms of GPU work: the host has enqueued the launch before ev0 runs
+                pre()
                 val = pf.nll(pdf, ds, backend=backend)
                 if r >= 3:
                     times.append(ctx.last_kernel_ms())

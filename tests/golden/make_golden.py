@@ -294,13 +294,88 @@ def fits_fixture():
         json.dump(out, fh, indent=1)
 
 
+def binned_fixture():
+    """BinnedDataSet.fill bin contents and binned_nll values / errors / a fit
+    (reference core.py:312-379, engine.py:246-276, fitting.py:431-439)."""
+    from parafit.core import BinnedDataSet
+    from parafit.engine import binned_nll
+    from parafit.errors import NonPositiveExpectation
+    from parafit.fitting import FitManager
+
+    rng = np.random.default_rng(23)
+    out = {}
+    # 1-D: the C1 model over 100 bins; data include bin edges and both bounds
+    x, pdf, params = c1_model()
+    n = 20000
+    xs = np.concatenate([np.clip(rng.normal(5.0, 0.5, n // 3), 0, 10), rng.exponential(1 / 0.3, n - n // 3)])
+    xs = xs[(xs >= 0) & (xs <= 10)]
+    edges = np.array([0.0, 10.0, 0.1, 0.2, 0.3, 0.7, 1.0, 2.5, 9.9, 9.99999999, 5.0, 4.95, 0.30000000000000004])
+    xs = np.concatenate([xs, edges])
+    ds = UnbinnedDataSet([x])
+    ds.extend([xs])
+    b1 = BinnedDataSet([x], [100])
+    b1.fill(ds)
+    out["b1_x"] = xs
+    out["b1_contents"] = b1.contents.copy()
+    pts1 = [(5.0, 0.5, -0.3, 0.3), (4.8, 0.6, -0.25, 0.35), (5.2, 0.3, -0.5, 0.5)]
+    vals = []
+    for pt in pts1:
+        for v, value in zip(params, pt):
+            v.value = value
+        vals.append(binned_nll(pdf, b1, snapshot(pdf.param_closure())))
+    out["b1_points"] = np.array(pts1)
+    out["b1_nll"] = np.array(vals)
+    # 2-D: the C2 model over 40 x 25 bins (row-major, y fastest)
+    xv = Variable.observable("x", 0.0, 10.0)
+    yv = Variable.observable("y", 0.0, 10.0)
+    mu = Variable("mu", 5.0, 0.0, 10.0, step=0.01)
+    sigma = Variable("sigma", 1.0, 0.01, 5.0, step=1e-3)
+    alpha = Variable("alpha", -0.4, -5.0, 5.0, step=1e-3)
+    pdf2 = prod_pdf([gaussian(xv, mu, sigma), exponential(yv, alpha)])
+    m = 30000
+    x2 = np.clip(rng.normal(5.0, 1.0, m), 0, 10)
+    y2 = np.clip(rng.exponential(1 / 0.4, m), 0, 10)
+    ds2 = UnbinnedDataSet([xv, yv])
+    ds2.extend([x2, y2])
+    b2 = BinnedDataSet([xv, yv], [40, 25])
+    b2.fill(ds2)
+    out["b2_x"], out["b2_y"], out["b2_contents"] = x2, y2, b2.contents.copy()
+    pts2 = [(5.0, 1.0, -0.4), (4.9, 1.1, -0.35)]
+    vals = []
+    for pt in pts2:
+        mu.value, sigma.value, alpha.value = pt
+        vals.append(binned_nll(pdf2, b2, snapshot(pdf2.param_closure())))
+    out["b2_points"], out["b2_nll"] = np.array(pts2), np.array(vals)
+    mu.value, sigma.value, alpha.value = (4.9, 1.1, -0.35)
+    r = FitManager(pdf2, b2).fit()
+    out["b2_fit_values"] = np.array(r.values)
+    out["b2_fit_errors"] = np.array(r.errors)
+    out["b2_fit_nll"] = np.array([r.nll_min])
+    out["b2_fit_calls"] = np.array([r.n_calls])
+    # NonPositiveExpectation: a narrow gaussian underflows to 0 at far bin centres
+    xp = Variable.observable("x", 0.0, 1.0)
+    gm = Variable("gm", 0.5, 0.0, 1.0)
+    gs = Variable("gs", 0.01, 0.001, 1.0)
+    poly = gaussian(xp, gm, gs)
+    bp = BinnedDataSet([xp], [20])
+    for b in range(20):
+        bp.set_content(b, float(b % 3))
+    try:
+        binned_nll(poly, bp, snapshot(poly.param_closure()))
+        raise AssertionError("expected NonPositiveExpectation")
+    except NonPositiveExpectation as exc:
+        out["bp_contents"] = bp.contents.copy()
+        out["bp_bin"] = np.array([exc.bin_index])
+        out["bp_value"] = np.array([exc.value])
+    except ParafitError as exc:  # the density kernel raised first
+        out["bp_contents"] = bp.contents.copy()
+        out["bp_error"] = np.array([type(exc).__name__])
+    np.savez_compressed(os.path.join(OUT, "binned.npz"), **out)
+
+
 if __name__ == "__main__":
-    reduction_fixture()
-    c1_fixture()
-    c2_fixture()
-    c3_fixture()
-    shards_fixture()
-    errors_fixture()
-    fits_fixture()
+    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned"]
+    for name in which:
+        globals()[f"{name}_fixture"]()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -93,3 +93,30 @@ def test_error_cases_match_reference(golden_dir):
     got = O.nll(("gaussian", "z", 0.0, 1.0, -math.inf, math.inf), one)
     assert got == cases["single_event_gauss"]
     assert abs(got - 0.5 * math.log(2 * math.pi)) <= 1e-12
+
+
+# --- binned data -----------------------------------------------
+
+B1_AXES = [("x", 0.0, 10.0, 100)]
+B2_AXES = [("x", 0.0, 10.0, 40), ("y", 0.0, 10.0, 25)]
+
+
+def test_binned_fill_and_nll_pinned(golden_dir):
+    g = load(golden_dir, "binned.npz")
+    c1 = O.fill(B1_AXES, {"x": g["b1_x"]})
+    assert c1.tolist() == g["b1_contents"].tolist()
+    for pt, want in zip(g["b1_points"], g["b1_nll"]):
+        assert O.binned_nll(models.c1_spec(tuple(pt)), B1_AXES, c1) == want
+    c2 = O.fill(B2_AXES, {"x": g["b2_x"], "y": g["b2_y"]})
+    assert c2.tolist() == g["b2_contents"].tolist()
+    for pt, want in zip(g["b2_points"], g["b2_nll"]):
+        assert O.binned_nll(models.c2_spec(tuple(pt)), B2_AXES, c2) == want
+
+
+def test_binned_nonpositive_expectation_pinned(golden_dir):
+    g = load(golden_dir, "binned.npz")
+    spec = ("gaussian", "x", 0.5, 0.01, 0.0, 1.0)
+    with pytest.raises(O.OracleDensityError) as ei:
+        O.binned_nll(spec, [("x", 0.0, 1.0, 20)], g["bp_contents"].copy())
+    assert ei.value.kind == "NonPositiveExpectation"
+    assert ei.value.index == int(g["bp_bin"][0]) and ei.value.value == float(g["bp_value"][0])
