@@ -349,10 +349,15 @@ def main():
         peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     algo_bytes = 8 * len(arrays) * n_per
     achieved = algo_bytes / (ms_per_step * 1e-3) / 1e9
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture (profiles/traffic_<cfg>.json, 10M events), per launch of this
+    # run: measured bytes/event x events per launch.  C4 runs the C3 kernel.
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    tcfg = {"c4": "c3", "c5": "c1"}.get(cfg, cfg)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{tcfg}.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("bytes_per_launch")
+        tj = json.load(open(tpath))
+        traffic = tj["bytes_per_launch"] / tj["events"] * n_per
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_event": 8 * len(arrays)}
