@@ -63,6 +63,9 @@ enum pfb_status {
     PFB_E_DEGENERATE_GRID = 7,     /* DegenerateGrid                     errors.py:111 */
     PFB_E_INVALID_SUM = 8,         /* math.fsum ValueError (inf + -inf)  */
     PFB_E_NONPOSITIVE_EXPECTATION = 9, /* NonPositiveExpectation(bin, value) errors.py:102 */
+    PFB_E_ENVELOPE_HIT = 10,       /* toy generation: a density above the envelope
+                                      (mcgen.py _EnvelopeHit; caller rescans) */
+    PFB_E_ATTEMPTS_EXHAUSTED = 11, /* AttemptsExhausted                  errors.py */
     PFB_E_INVALID_ARGUMENT = 20,
     PFB_E_UNSUPPORTED_PLAN = 21,
     PFB_E_CUDA = 30,
@@ -241,6 +244,42 @@ int pfb_bin_fill(pfb_ctx* ctx, const pfb_store* store, int64_t begin, int64_t en
 int pfb_binned_nll(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* centers, const double* contents,
                    int64_t nbins, double total, double volume, const double* values, int32_t nvalues,
                    const double* norms, int32_t nnorms, double* out_nll, pfb_err* out_err);
+
+/* ---- toy generation, stream-exact ----------------------------- */
+/* One numpy PCG64 stream: the 128-bit state and increment of
+ * np.random.PCG64(SeedSequence(seed).spawn(streams)[i]).state. */
+typedef struct {
+    uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} pfb_pcg64;
+
+typedef struct {
+    int64_t attempts;     /* candidates drawn (stats["attempts"] / ["box_draws"]) */
+    int64_t accepted;     /* stats["accepted"] contribution of this stream */
+    int64_t in_boundary;  /* stats["in_boundary_draws"] (Dalitz) */
+    int64_t produced;     /* events written */
+    double observed;      /* PFB_E_ENVELOPE_HIT: the chunk's maximum density */
+} pfb_gen_stats;
+
+/* mcgen._scan_max (mcgen.py:52-54): max of the plan's unnormalised root
+ * density (norms[root] = 1, children's norms as the reference passes them)
+ * over points midpoints of [lo, hi]. */
+int pfb_pcg_scan_1d(pfb_ctx* ctx, const pfb_plan* plan, const double* values, int32_t nvalues,
+                    const double* norms, int32_t nnorms, double lo, double hi, int64_t points, double* out_max);
+/* _dalitz_scan_grid + _masked_intensity_max (mcgen.py:209-222) on an n x n grid. */
+int pfb_pcg_scan_dalitz(pfb_ctx* ctx, const pfb_dalitz_desc* channel, const double* term_values, int32_t n,
+                        double* out_max);
+/* _accept_reject_1d for one stream (mcgen.py:66-97): writes the accepted
+ * samples (in the reference's order, the first n_wanted) to out column 0 at
+ * out_offset.  PFB_E_ENVELOPE_HIT (stats->observed) asks the caller to rescan
+ * and restart, PFB_E_ATTEMPTS_EXHAUSTED when the budget runs out. */
+int pfb_pcg_generate_1d(pfb_ctx* ctx, const pfb_plan* plan, const double* values, int32_t nvalues,
+                        const double* norms, int32_t nnorms, double lo, double hi, double envelope,
+                        const pfb_pcg64* stream, int64_t n_wanted, int64_t budget, pfb_store* out,
+                        int64_t out_offset, pfb_gen_stats* stats);
+/* One stream of _dalitz_streams (mcgen.py:232-257): columns 0/1 = s12/s13. */
+int pfb_pcg_generate_dalitz(pfb_ctx* ctx, const pfb_dalitz_desc* channel, const double* term_values,
+                            double envelope, const pfb_pcg64* stream, int64_t n_wanted, int64_t budget,
+                            pfb_store* out, int64_t out_offset, pfb_gen_stats* stats);
 
 /* ---- sharding ------------------------------------------------------------------ */
 /* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */

@@ -31,6 +31,8 @@ E_NONPOSITIVE_NORM = 6
 E_DEGENERATE_GRID = 7
 E_INVALID_SUM = 8
 E_NONPOSITIVE_EXPECTATION = 9
+E_ENVELOPE_HIT = 10
+E_ATTEMPTS_EXHAUSTED = 11
 E_INVALID_ARGUMENT = 20
 E_UNSUPPORTED_PLAN = 21
 E_CUDA = 30
@@ -75,6 +77,16 @@ class PfbDalitzDesc(ctypes.Structure):
 
 class PfbErr(ctypes.Structure):
     _fields_ = [("code", c_int32), ("node", c_int32), ("index", c_int64), ("value", c_double)]
+
+
+class PfbPcg64(ctypes.Structure):
+    _fields_ = [("state_hi", ctypes.c_uint64), ("state_lo", ctypes.c_uint64), ("inc_hi", ctypes.c_uint64),
+                ("inc_lo", ctypes.c_uint64)]
+
+
+class PfbGenStats(ctypes.Structure):
+    _fields_ = [("attempts", c_int64), ("accepted", c_int64), ("in_boundary", c_int64), ("produced", c_int64),
+                ("observed", c_double)]
 
 
 _PTR = c_void_p
@@ -128,6 +140,12 @@ _SIGNATURES = [
     ("pfb_store_download", c_int, [_PTR, c_int32, _DBL_P, c_int64, c_int64]),
     ("pfb_fp64_peak", c_int, [_PTR, _DBL_P]),
     ("pfb_ctx_spin", c_int, [_PTR, c_int64, _PTR, c_int64]),
+    ("pfb_pcg_scan_1d", c_int, [_PTR, _PTR, _DBL_P, c_int32, _DBL_P, c_int32, c_double, c_double, c_int64, _DBL_P]),
+    ("pfb_pcg_scan_dalitz", c_int, [_PTR, POINTER(PfbDalitzDesc), _DBL_P, c_int32, _DBL_P]),
+    ("pfb_pcg_generate_1d", c_int, [_PTR, _PTR, _DBL_P, c_int32, _DBL_P, c_int32, c_double, c_double, c_double,
+                                    POINTER(PfbPcg64), c_int64, c_int64, _PTR, c_int64, POINTER(PfbGenStats)]),
+    ("pfb_pcg_generate_dalitz", c_int, [_PTR, POINTER(PfbDalitzDesc), _DBL_P, c_double, POINTER(PfbPcg64), c_int64,
+                                        c_int64, _PTR, c_int64, POINTER(PfbGenStats)]),
     ("pfb_bin_fill", c_int, [_PTR, _PTR, c_int64, c_int64, c_int32, _PTR, _PTR, _PTR, _PTR, _PTR]),
     ("pfb_binned_nll", c_int, [_PTR, _PTR, _PTR, _PTR, c_int64, c_double, c_double, _PTR, c_int32, _PTR, c_int32,
                                _DBL_P, _PTR]),

@@ -28,6 +28,20 @@ cudaError_t launch_binned_probe(const NllArgs& A, int64_t b, double total, doubl
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
 cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
                               cudaStream_t stream);
+struct PcgParams;
+struct PcgHostResult {
+    int status;
+    int64_t attempts, accepted, in_boundary, produced;
+    double observed;
+};
+cudaError_t pcg_generate_entry(const NllArgs& A, int dalitz, const double* box, double envelope,
+                               const GridConsts* g, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                               uint64_t inc_lo, int64_t n_wanted, int64_t budget, double* out0, double* out1,
+                               cudaStream_t stream, PcgHostResult* R);
+cudaError_t pcg_scan_1d(const NllArgs& A, double lo, double hi, int64_t points, double* out_max,
+                        unsigned long long* scratch, cudaStream_t stream, int sm_count);
+cudaError_t pcg_scan_dalitz(const NllArgs& A, const GridConsts& g, double* out_max, unsigned long long* scratch,
+                            cudaStream_t stream, int sm_count);
 cudaError_t launch_grid_mask(const GridConsts& g, uint8_t* mask, int* row_count, cudaStream_t st);
 cudaError_t launch_grid_compact(const GridConsts& g, const uint8_t* mask, const int* row_offset,
                                 double* p12, double* p13, cudaStream_t st);
@@ -1803,6 +1817,134 @@ int pfb_binned_nll(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, const do
     if (out_nll) *out_nll = r;
     if (out_err) *out_err = e;
     return code;
+}
+
+
+}  // extern "C"
+
+// ---- stream-exact toy generation ------------------------------
+
+static GridConsts grid_consts_of(const pfb_dalitz_desc& d, int nx, int ny) {
+    GridConsts k{};
+    k.nx = nx;
+    k.ny = ny;
+    const double M = d.mother_mass;
+    // DecayChannel.s12_range / s13_range (dalitz.py:68-74): Python (a)**2
+    const double a12 = d.m1 + d.m2, b12 = M - d.m3, a13 = d.m1 + d.m3, b13 = M - d.m2;
+    k.lo12 = a12 * a12;
+    k.hi12 = b12 * b12;
+    k.lo13 = a13 * a13;
+    const double hi13 = b13 * b13;
+    k.dx = (k.hi12 - k.lo12) / nx;
+    k.dy = (hi13 - k.lo13) / ny;
+    k.m1sq = d.m1 * d.m1;
+    k.m2sq = d.m2 * d.m2;
+    k.m3sq = d.m3 * d.m3;
+    k.M2 = M * M;
+    return k;
+}
+
+static int pack_density_args(pfb_ctx* c, const pfb_plan* p, const double* values, int32_t nvalues,
+                             const double* norms, int32_t nnorms, NllArgs* A) {
+    if (p->ctx != c || nvalues != p->nraw || nnorms != (int32_t)p->nodes.size() || p->nslots > 2)
+        return PFB_E_INVALID_ARGUMENT;
+    pfb_store dummy;
+    dummy.ctx = c;
+    dummy.ncols = kStoreMaxCols;
+    dummy.n = 0;
+    const int frac = pack_args(p, &dummy, 0, 0, values, norms, A);
+    return frac >= 0 ? PFB_E_FRACTION_OUT_OF_RANGE : PFB_OK;
+}
+
+static int gen_status(const PcgHostResult& R, pfb_gen_stats* stats) {
+    if (stats) {
+        stats->attempts = R.attempts;
+        stats->accepted = R.accepted;
+        stats->in_boundary = R.in_boundary;
+        stats->produced = R.produced;
+        stats->observed = R.observed;
+    }
+    switch (R.status) {
+        case 0: return PFB_OK;
+        case 2: return PFB_E_NONFINITE_DENSITY;
+        case 10: return PFB_E_ENVELOPE_HIT;
+        default: return PFB_E_ATTEMPTS_EXHAUSTED;
+    }
+}
+
+extern "C" {
+
+int pfb_pcg_scan_1d(pfb_ctx* c, const pfb_plan* p, const double* values, int32_t nvalues, const double* norms,
+                    int32_t nnorms, double lo, double hi, int64_t points, double* out_max) {
+    if (!c || !p || !values || !norms || !out_max || points < 1) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    int rc = pack_density_args(c, p, values, nvalues, norms, nnorms, A.get());
+    if (rc) return rc;
+    rc = ensure_bin(c, 0);
+    if (rc) return rc;
+    CK(pcg_scan_1d(*A, lo, hi, points, out_max, c->bin_key, c->stream, c->sm_count));
+    ++c->launches;
+    return PFB_OK;
+}
+
+int pfb_pcg_scan_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term_values, int32_t n,
+                        double* out_max) {
+    if (!c || !d || !term_values || !out_max || n < 1 || d->nterms < 1 || d->nterms > kMaxDal)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    memset(A.get(), 0, sizeof(NllArgs));
+    fill_daldesc(*d, term_values, &A->dal);
+    int rc = ensure_bin(c, 0);
+    if (rc) return rc;
+    CK(pcg_scan_dalitz(*A, grid_consts_of(*d, n, n), out_max, c->bin_key, c->stream, c->sm_count));
+    ++c->launches;
+    return PFB_OK;
+}
+
+int pfb_pcg_generate_1d(pfb_ctx* c, const pfb_plan* p, const double* values, int32_t nvalues,
+                        const double* norms, int32_t nnorms, double lo, double hi, double envelope,
+                        const pfb_pcg64* stream, int64_t n_wanted, int64_t budget, pfb_store* out,
+                        int64_t out_offset, pfb_gen_stats* stats) {
+    if (!c || !p || !values || !norms || !stream || !out || out->ctx != c || n_wanted < 0 || budget < 0 ||
+        out_offset < 0 || out_offset + n_wanted > out->n || out->ncols < 1)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    int rc = pack_density_args(c, p, values, nvalues, norms, nnorms, A.get());
+    if (rc) return rc;
+    const double box[4] = {lo, hi - lo, 0.0, 0.0};
+    PcgHostResult R;
+    CK(pcg_generate_entry(*A, 0, box, envelope, nullptr, stream->state_hi, stream->state_lo, stream->inc_hi,
+                          stream->inc_lo, n_wanted, budget, out->cols[0] + out_offset, nullptr, c->stream, &R));
+    c->launches += 2;
+    return gen_status(R, stats);
+}
+
+int pfb_pcg_generate_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term_values, double envelope,
+                            const pfb_pcg64* stream, int64_t n_wanted, int64_t budget, pfb_store* out,
+                            int64_t out_offset, pfb_gen_stats* stats) {
+    if (!c || !d || !term_values || !stream || !out || out->ctx != c || n_wanted < 0 || budget < 0 ||
+        out_offset < 0 || out_offset + n_wanted > out->n || out->ncols < 2 || d->nterms < 1 ||
+        d->nterms > kMaxDal)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    memset(A.get(), 0, sizeof(NllArgs));
+    fill_daldesc(*d, term_values, &A->dal);
+    const GridConsts g = grid_consts_of(*d, 1, 1);
+    const double M = d->mother_mass;
+    const double b13 = M - d->m2;
+    const double hi13 = b13 * b13;
+    // uniform(lo, hi): scale = hi - lo as numpy computes it
+    const double box[4] = {g.lo12, g.hi12 - g.lo12, g.lo13, hi13 - g.lo13};
+    PcgHostResult R;
+    CK(pcg_generate_entry(*A, 1, box, envelope, &g, stream->state_hi, stream->state_lo, stream->inc_hi,
+                          stream->inc_lo, n_wanted, budget, out->cols[0] + out_offset, out->cols[1] + out_offset,
+                          c->stream, &R));
+    c->launches += 2;
+    return gen_status(R, stats);
 }
 
 }  // extern "C"

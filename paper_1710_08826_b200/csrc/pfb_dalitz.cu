@@ -15,22 +15,6 @@
 
 namespace pfb {
 
-__device__ __forceinline__ bool in_boundary_exact(const GridConsts& g, double s12, double s13) {
-    const double rs = __dsqrt_rn(s12);
-    const double two_rs = Mul(2.0, rs);
-    const double e1 = Div(Sub(Add(s12, g.m1sq), g.m2sq), two_rs);
-    const double e3 = Div(Sub(Sub(g.M2, s12), g.m3sq), two_rs);
-    const double p1 = __dsqrt_rn(Sub(Mul(e1, e1), g.m1sq));
-    const double p3 = __dsqrt_rn(Sub(Mul(e3, e3), g.m3sq));
-    const double es = Add(e1, e3);
-    const double esum = Mul(es, es);
-    const double pp = Add(p1, p3), pm = Sub(p1, p3);
-    const double lo = Sub(esum, Mul(pp, pp));
-    const double hi = Sub(esum, Mul(pm, pm));
-    // NaN (outside the s12 band) compares false, as numpy does.
-    return (s12 >= g.lo12) && (s12 <= g.hi12) && (s13 >= lo) && (s13 <= hi);
-}
-
 __device__ __forceinline__ double centre(double lo, int i, double d) {
     return Add(lo, Mul((double)i + 0.5, d));
 }

@@ -17,6 +17,24 @@ __device__ __forceinline__ double Sub(double a, double b) { return __dsub_rn(a, 
 __device__ __forceinline__ double Mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double Div(double a, double b) { return __ddiv_rn(a, b); }
 
+// in_boundary_mask (dalitz.py:127-150) with the reference's exact IEEE
+// operation sequence (bit-exact): s13 limits from the s12 invariant mass.
+__device__ __forceinline__ bool in_boundary_exact(const GridConsts& g, double s12, double s13) {
+    const double rs = __dsqrt_rn(s12);
+    const double two_rs = Mul(2.0, rs);
+    const double e1 = Div(Sub(Add(s12, g.m1sq), g.m2sq), two_rs);
+    const double e3 = Div(Sub(Sub(g.M2, s12), g.m3sq), two_rs);
+    const double p1 = __dsqrt_rn(Sub(Mul(e1, e1), g.m1sq));
+    const double p3 = __dsqrt_rn(Sub(Mul(e3, e3), g.m3sq));
+    const double es = Add(e1, e3);
+    const double esum = Mul(es, es);
+    const double pp = Add(p1, p3), pm = Sub(p1, p3);
+    const double lo = Sub(esum, Mul(pp, pp));
+    const double hi = Sub(esum, Mul(pm, pm));
+    // NaN (outside the s12 band) compares false, as numpy does.
+    return (s12 >= g.lo12) && (s12 <= g.hi12) && (s13 >= lo) && (s13 <= hi);
+}
+
 // ---------------------------------------------------------------------------
 // Dalitz amplitude of one term with the reference's exact operation sequence
 // (dalitz.py:162-197): BW = 1/(m^2 - s - i m Gamma) by numpy's Smith division,

@@ -69,7 +69,19 @@ __device__ __forceinline__ double dalitz_intensity_literal(const DalDesc& D, dou
 // overflow and density errors.  literal_density returns p = root / norm_root
 // (eval_batch(...) / norms[pdf.id], engine.py:181, 265), or NaN with `rank`
 // set when a node kernel raises; literal_event adds the p > 0 check and -ln.
-static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t j, int* rank, double* val) {
+// Observable values of one event: from the store columns (event j) or from
+// registers (candidates of the toy generator, pfb_pcg.cu).
+struct ColLoader {
+    int64_t j;
+    __device__ __forceinline__ double operator()(const NllArgs& A, int c) const { return A.col[c][j]; }
+};
+struct ValLoader {
+    double v[kMaxCols];
+    __device__ __forceinline__ double operator()(const NllArgs&, int c) const { return v[c]; }
+};
+
+template <class Ld>
+static __device__ __noinline__ double literal_density_t(const NllArgs& A, const Ld ld, int* rank, double* val) {
     double st[kMaxNodes];
     int sid[kMaxNodes];
     int sp = 0;
@@ -78,7 +90,7 @@ static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t 
         double v = 0.0;
         switch (op.kind) {
             case PFB_GAUSSIAN: {
-                const double x = A.col[op.col0][j];
+                const double x = ld(A, op.col0);
                 const double z = Div(Sub(x, A.v[op.voff]), A.v[op.voff + 1]);
                 v = exp(Mul(Mul(-0.5, z), z));
                 if (!finite(v)) {
@@ -89,7 +101,7 @@ static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t 
                 break;
             }
             case PFB_EXPONENTIAL: {
-                const double x = A.col[op.col0][j];
+                const double x = ld(A, op.col0);
                 v = exp(Mul(A.v[op.voff], x));
                 if (!finite(v)) {
                     *rank = op.rank;
@@ -99,7 +111,7 @@ static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t 
                 break;
             }
             case PFB_POLYNOMIAL: {
-                const double x = A.col[op.col0][j];
+                const double x = ld(A, op.col0);
                 const double* c = A.v + op.voff;
                 const int n = op.nv;
                 v = Add(c[n - 1], Mul(x, 0.0));
@@ -133,7 +145,7 @@ static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t 
                 break;
             }
             case PFB_DALITZ: {
-                v = dalitz_intensity_literal(A.dal, A.col[op.col0][j], A.col[op.col1][j]);
+                v = dalitz_intensity_literal(A.dal, ld(A, op.col0), ld(A, op.col1));
                 break;
             }
             default:
@@ -144,6 +156,10 @@ static __device__ __noinline__ double literal_density(const NllArgs& A, int64_t 
         ++sp;
     }
     return Div(st[0], A.norm[A.nops - 1]);
+}
+
+static __device__ __forceinline__ double literal_density(const NllArgs& A, int64_t j, int* rank, double* val) {
+    return literal_density_t(A, ColLoader{j}, rank, val);
 }
 
 static __device__ __forceinline__ double literal_event(const NllArgs& A, int64_t j, int* rank, double* val) {

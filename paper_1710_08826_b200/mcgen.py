@@ -1,15 +1,16 @@
-"""Synthetic event generation for benchmarks and tests (host numpy).
+"""Toy event generation.
 
-Not on the NLL path: these samplers only produce the input columns.  The
-reference generates by PCG64 accept-reject (mcgen.py:68-257); parity never
-depends on the sampler because the device and the CPU reference always
-consume the same arrays.  Samplers here are exact inverse-CDF where a closed
-form exists (truncated exponential, truncated Gaussian via erf/erfinv-free
-accept on a wide proposal) and vectorised accept-reject for the Dalitz plot.
+* generate_1d / generate_dalitz (+ GenSpec): the reference's generators
+  (mcgen.py:35-257) on the GPU, stream for stream: the same numpy PCG64
+  streams (SeedSequence spawning), the same chunked accept-reject, the same
+  envelope / rescan / budget semantics -> the same events (pfb_pcg_*).
+* device_*: fast Philox-based samplers for benchmark inputs (pfb_gen_*).
+* sumpdf_1d / prod_2d / dalitz: host numpy samplers for small test inputs.
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -193,3 +194,191 @@ def device_dalitz(n, terms, channel, seed, ctx=None, envelope=None):
     L.check(L.lib().pfb_gen_dalitz(ctx.handle, ctypes.byref(d), L.dptr(vals), env, seed, n, st, ctypes.byref(cand)),
             "pfb_gen_dalitz")
     return tuple(_adopt(ctx, st, 2, n))
+
+
+# --- the reference generators, stream-exact on the GPU ------------
+
+SCAN_POINTS = 4096  # mcgen.py:29-31
+RESCAN_POINTS = 4 * SCAN_POINTS
+CHUNK = 8192
+
+
+from dataclasses import dataclass  # noqa: E402
+
+
+@dataclass(frozen=True)
+class GenSpec:
+    """How many events to draw, from which seed, under which safety margins
+    (reference mcgen.py:35-50)."""
+
+    n_events: int
+    seed: int = 0
+    envelope_safety: float = 1.1
+    max_attempts_factor: int = 1000
+    streams: int = 1
+
+    def __post_init__(self):
+        if self.n_events < 1:
+            raise ValueError("n_events must be >= 1")
+        if self.envelope_safety < 1.0:
+            raise ValueError("envelope_safety must be >= 1")
+        if self.streams < 1:
+            raise ValueError("streams must be >= 1")
+
+
+def _stream_states(spec: GenSpec):
+    """PCG64 states of SeedSequence(seed).spawn(streams) (mcgen.py:57-59)."""
+    from . import _lib as L
+
+    out = []
+    for child in np.random.SeedSequence(spec.seed).spawn(spec.streams):
+        st = np.random.PCG64(child).state["state"]
+        s, inc = int(st["state"]), int(st["inc"])
+        p = L.PfbPcg64()
+        p.state_hi, p.state_lo = s >> 64, s & ((1 << 64) - 1)
+        p.inc_hi, p.inc_lo = inc >> 64, inc & ((1 << 64) - 1)
+        out.append(p)
+    return out
+
+
+def _split_counts(total: int, parts: int) -> list[int]:
+    base, extra = divmod(total, parts)
+    return [base + (1 if k < extra else 0) for k in range(parts)]
+
+
+class _EnvelopeHit(Exception):
+    def __init__(self, observed: float):
+        self.observed = observed
+
+
+def _run_streams(spec, budget, gen_one, stats, dalitz: bool):
+    """The per-stream loop of _generate_streams / _dalitz_streams: events of
+    stream i follow those of stream i-1."""
+    from . import _lib as L
+    from .errors import AttemptsExhausted
+
+    states = _stream_states(spec)
+    counts = _split_counts(spec.n_events, spec.streams)
+    budgets = _split_counts(budget, spec.streams)
+    offset = 0
+    for state, cnt, bud in zip(states, counts, budgets):
+        if cnt <= 0:
+            continue
+        gs = L.PfbGenStats()
+        code = gen_one(state, cnt, bud, offset, gs)
+        if dalitz:
+            stats["box_draws"] = stats.get("box_draws", 0) + gs.attempts
+            stats["in_boundary_draws"] = stats.get("in_boundary_draws", 0) + gs.in_boundary
+        if code == L.E_ENVELOPE_HIT:
+            raise _EnvelopeHit(gs.observed)
+        if code == L.E_ATTEMPTS_EXHAUSTED:
+            if dalitz:
+                raise AttemptsExhausted(f"{gs.attempts} draws produced only {gs.produced}/{cnt} events in one stream")
+            raise AttemptsExhausted(f"{gs.attempts} draws produced only {gs.produced}/{cnt} events")
+        L.check(code, "pfb_pcg_generate")
+        if not dalitz:
+            stats["attempts"] = stats.get("attempts", 0) + gs.attempts
+        stats["accepted"] = stats.get("accepted", 0) + gs.accepted
+        offset += cnt
+
+
+def generate_1d(pdf, obs, spec: GenSpec, stats: dict | None = None, device: int = 0):
+    """Reference generate_1d (mcgen.py:108-153) on the GPU: the same events
+    for the same spec (see pfb_pcg.cu for the one caveat)."""
+    from . import _lib as L
+    from .core import UnbinnedDataSet
+    from .engine import device_context
+    from .errors import EnvelopeExceeded, UnboundedObservable
+    from .pdf import normalize
+
+    lo, hi = obs.lower, obs.upper
+    if not (math.isfinite(lo) and math.isfinite(hi)):
+        raise UnboundedObservable(f"{obs.name!r} needs finite bounds for generation")
+    norms = {n.id: normalize(n).value for n in pdf.walk() if n is not pdf} if pdf.children else {}
+    norms[pdf.id] = 1.0  # eval_batch returns the unnormalised root density
+    ctx = device_context(device)
+    plan = ctx.plan_for(pdf, (obs.name,))
+    vals, nv = plan.pack(None, norms)
+    vals, nv = vals.copy(), nv.copy()
+
+    def scan(points):
+        out = ctypes.c_double()
+        L.check(L.lib().pfb_pcg_scan_1d(ctx.handle, plan.handle, L.dptr(vals), len(vals), L.dptr(nv), len(nv),
+                                        lo, hi, points, ctypes.byref(out)), "pfb_pcg_scan_1d")
+        return out.value
+
+    envelope = spec.envelope_safety * scan(SCAN_POINTS)
+    budget = spec.max_attempts_factor * spec.n_events
+    stats = stats if stats is not None else {}
+    st = _device_store(ctx, 1, spec.n_events)
+    for attempt in range(2):
+        try:
+            stats.clear()
+            stats["envelope"] = envelope
+
+            def one(state, cnt, bud, offset, gs, env=envelope):
+                return L.lib().pfb_pcg_generate_1d(ctx.handle, plan.handle, L.dptr(vals), len(vals), L.dptr(nv),
+                                                   len(nv), lo, hi, env, ctypes.byref(state), cnt, bud, st, offset,
+                                                   ctypes.byref(gs))
+
+            _run_streams(spec, budget, one, stats, dalitz=False)
+            break
+        except _EnvelopeHit as hit:
+            if attempt == 1:
+                L.lib().pfb_store_destroy(st)
+                raise EnvelopeExceeded(f"density {hit.observed} exceeded envelope {envelope} after a rescan") from None
+            envelope = spec.envelope_safety * max(scan(RESCAN_POINTS), hit.observed)
+    col = _adopt(ctx, st, 1, spec.n_events)[0]
+    return UnbinnedDataSet.from_columns([obs], [col], copy=False)
+
+
+def generate_dalitz(terms, ch, spec: GenSpec, observables=None, stats: dict | None = None, device: int = 0):
+    """Reference generate_dalitz (mcgen.py:155-199) on the GPU: flat phase
+    space over the (s12, s13) box, boundary filter, intensity accept-reject."""
+    from . import _lib as L
+    from .core import UnbinnedDataSet, Variable
+    from .engine import device_context
+    from .errors import EnvelopeExceeded
+
+    if not terms:
+        raise ValueError("need at least one resonance term")
+    if observables is None:
+        observables = (Variable.observable("s12", *ch.s12_range), Variable.observable("s13", *ch.s13_range))
+    d = L.PfbDalitzDesc()
+    d.mother_mass, d.m1, d.m2, d.m3 = ch.mother_mass, ch.m1, ch.m2, ch.m3
+    d.nterms = len(terms)
+    vals = np.zeros(4 * len(terms))
+    for k, t in enumerate(terms):
+        d.pair[k], d.spin[k] = int(t.pair), int(t.spin)
+        vals[4 * k:4 * k + 4] = (t.mass.value, t.width.value, t.magnitude.value, t.phase.value)
+    ctx = device_context(device)
+
+    def scan(n):
+        out = ctypes.c_double()
+        L.check(L.lib().pfb_pcg_scan_dalitz(ctx.handle, ctypes.byref(d), L.dptr(vals), n, ctypes.byref(out)),
+                "pfb_pcg_scan_dalitz")
+        return out.value
+
+    envelope = spec.envelope_safety * scan(512)
+    budget = spec.max_attempts_factor * spec.n_events
+    stats = stats if stats is not None else {}
+    st = _device_store(ctx, 2, spec.n_events)
+    for attempt in range(2):
+        try:
+            stats.clear()
+            stats["envelope"] = envelope
+
+            def one(state, cnt, bud, offset, gs, env=envelope):
+                return L.lib().pfb_pcg_generate_dalitz(ctx.handle, ctypes.byref(d), L.dptr(vals), env,
+                                                       ctypes.byref(state), cnt, bud, st, offset, ctypes.byref(gs))
+
+            _run_streams(spec, budget, one, stats, dalitz=True)
+            break
+        except _EnvelopeHit as hit:
+            if attempt == 1:
+                L.lib().pfb_store_destroy(st)
+                raise EnvelopeExceeded(
+                    f"intensity {hit.observed} exceeded envelope {envelope} after a rescan") from None
+            envelope = spec.envelope_safety * max(scan(2048), hit.observed)
+    s12, s13 = _adopt(ctx, st, 2, spec.n_events)
+    return UnbinnedDataSet.from_columns(list(observables), [s12, s13], copy=False)

@@ -373,8 +373,57 @@ def binned_fixture():
     np.savez_compressed(os.path.join(OUT, "binned.npz"), **out)
 
 
+def toys_fixture():
+    """The reference's toy generators (mcgen.py): exact events and stats for a
+    few specs, incl. multiple streams and an envelope rescan."""
+    from parafit.mcgen import GenSpec as RSpec
+    from parafit.mcgen import generate_1d as rgen1d
+    from parafit.mcgen import generate_dalitz as rgendal
+
+    out = {}
+    x, pdf, params = c1_model()
+    for tag, spec in [("a", RSpec(20000, seed=5)), ("b", RSpec(10001, seed=9, streams=3))]:
+        stats = {}
+        ds = rgen1d(pdf, x, spec, stats)
+        out[f"c1{tag}_x"] = ds.column("x")
+        out[f"c1{tag}_stats"] = np.array([stats["envelope"], stats["attempts"], stats["accepted"]])
+    # a spike the 4096-point scan misses: envelope hit -> rescan -> restart
+    xs = Variable.observable("x", 0.0, 10.0)
+    spike = gaussian(xs, Variable("m", 5.00061, 0.0, 10.0), Variable("s", 0.001, 1e-5, 1.0))
+    stats = {}
+    ds = rgen1d(spike, xs, RSpec(300, seed=2, max_attempts_factor=100000), stats)
+    out["spike_x"] = ds.column("x")
+    out["spike_stats"] = np.array([stats["envelope"], stats["attempts"], stats["accepted"]])
+    # ... and one it still misses after the rescan: EnvelopeExceeded
+    from parafit.errors import EnvelopeExceeded as REnv
+
+    narrow = gaussian(xs, Variable("m2", 5.00061, 0.0, 10.0), Variable("s2", 0.0005, 1e-5, 1.0))
+    try:
+        rgen1d(narrow, xs, RSpec(300, seed=2, max_attempts_factor=100000))
+        out["narrow_exceeded"] = np.array([0])
+    except REnv:
+        out["narrow_exceeded"] = np.array([1])
+    # the default budget (1000 draws per event) runs out on the spike
+    from parafit.errors import AttemptsExhausted as RAtt
+
+    try:
+        rgen1d(spike, xs, RSpec(300, seed=2))
+        out["spike_exhausted"] = np.array([""])
+    except RAtt as exc:
+        out["spike_exhausted"] = np.array([str(exc)])
+    terms = c3_terms()
+    for tag, spec in [("a", RSpec(3000, seed=3)), ("b", RSpec(2001, seed=4, streams=2))]:
+        stats = {}
+        ds = rgendal(terms, D_CHANNEL, spec, stats=stats)
+        out[f"dal{tag}_s12"] = ds.column("s12")
+        out[f"dal{tag}_s13"] = ds.column("s13")
+        out[f"dal{tag}_stats"] = np.array([stats["envelope"], stats["box_draws"], stats["in_boundary_draws"],
+                                           stats["accepted"]])
+    np.savez_compressed(os.path.join(OUT, "toys.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned"]
+    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned", "toys"]
     for name in which:
         globals()[f"{name}_fixture"]()
     for f in sorted(os.listdir(OUT)):
