@@ -281,6 +281,20 @@ int pfb_pcg_generate_dalitz(pfb_ctx* ctx, const pfb_dalitz_desc* channel, const 
                             double envelope, const pfb_pcg64* stream, int64_t n_wanted, int64_t budget,
                             pfb_store* out, int64_t out_offset, pfb_gen_stats* stats);
 
+/* ---- binary SoA ingest ---------------------------------------- */
+/* Rows of a 1-D little-endian float64 .npy column file (replaces the CSV path
+ * dataio.py:20-83 for large runs). */
+int pfb_npy_length(const char* path, int64_t* n_out);
+/* Rows [src_offset, src_offset + count) of a .npy column straight into device
+ * column `col` at dst_offset (pinned double-buffered, overlapped reads and
+ * copies; no host copy of the column). */
+int pfb_store_load_npy(pfb_store* store, int32_t col, const char* path, int64_t src_offset, int64_t dst_offset,
+                       int64_t count);
+/* The dataset range check (core.py:262-272) on the device: first row of
+ * [begin, end) with x < lower, x > upper or non-finite (-1 if none). */
+int pfb_store_check_range(pfb_store* store, int32_t col, int64_t begin, int64_t end, double lower, double upper,
+                          int64_t* first_bad, double* bad_value);
+
 /* ---- sharding ------------------------------------------------------------------ */
 /* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */
 int pfb_shard_bounds(int64_t n, int32_t workers, int64_t block, int64_t* bounds);

@@ -9,6 +9,9 @@
 #include <memory>
 #include <vector>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include "pfb_internal.cuh"
 
 namespace pfb {
@@ -28,6 +31,9 @@ cudaError_t launch_binned_probe(const NllArgs& A, int64_t b, double total, doubl
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
 cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
                               cudaStream_t stream);
+int npy_parse(int fd, int64_t* n_out, int64_t* data_off);
+cudaError_t launch_range_check(const double* x, int64_t n, double lo, double hi, unsigned long long* first,
+                               cudaStream_t stream, int sm_count);
 struct PcgParams;
 struct PcgHostResult {
     int status;
@@ -113,6 +119,9 @@ struct pfb_ctx {
     double* e2e_dev[kMaxCols] = {nullptr, nullptr, nullptr, nullptr};
     int64_t e2e_cap = 0;
     std::vector<cudaEvent_t> chunk_events;
+    // file ingest staging (pfb_store_load_npy)
+    double* io_pinned[2] = {nullptr, nullptr};
+    cudaEvent_t io_event[2] = {nullptr, nullptr};
     // binned data scratch
     void* bin_dev = nullptr;  // bin counts / contents
     int64_t bin_cap = 0;      // bytes
@@ -271,6 +280,10 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaFree(c->bsums);
     cudaFree(c->bin_dev);
     cudaFree(c->bin_key);
+    for (int b = 0; b < 2; ++b) {
+        if (c->io_pinned[b]) cudaFreeHost(c->io_pinned[b]);
+        if (c->io_event[b]) cudaEventDestroy(c->io_event[b]);
+    }
     for (auto& p : c->e2e_dev) cudaFree(p);
     for (auto& e : c->chunk_events) cudaEventDestroy(e);
     cudaFreeHost(c->res_host);
@@ -1945,6 +1958,91 @@ int pfb_pcg_generate_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* 
                           c->stream, &R));
     c->launches += 2;
     return gen_status(R, stats);
+}
+
+
+// ---- binary SoA ingest ---------------------------------------
+
+static constexpr int64_t kIoChunk = 4 << 20;  // doubles per staging buffer (32 MB)
+
+int pfb_npy_length(const char* path, int64_t* n_out) {
+    if (!path || !n_out) return PFB_E_INVALID_ARGUMENT;
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return PFB_E_INVALID_ARGUMENT;
+    int64_t n = 0, off = 0;
+    const int bad = npy_parse(fd, &n, &off);
+    close(fd);
+    if (bad) return PFB_E_INVALID_ARGUMENT;
+    *n_out = n;
+    return PFB_OK;
+}
+
+int pfb_store_load_npy(pfb_store* st, int32_t col, const char* path, int64_t src_offset, int64_t dst_offset,
+                       int64_t count) {
+    if (!st || !path || col < 0 || col >= st->ncols || src_offset < 0 || dst_offset < 0 || count < 0 ||
+        dst_offset + count > st->n)
+        return PFB_E_INVALID_ARGUMENT;
+    pfb_ctx* c = st->ctx;
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return PFB_E_INVALID_ARGUMENT;
+    std::unique_ptr<int, void (*)(int*)> fd_guard(new int(fd), [](int* f) {
+        close(*f);
+        delete f;
+    });
+    int64_t n = 0, off = 0;
+    if (npy_parse(fd, &n, &off) || src_offset + count > n) return PFB_E_INVALID_ARGUMENT;
+    if (count == 0) return PFB_OK;
+    CK(cudaSetDevice(c->device));
+    for (int b = 0; b < 2; ++b) {
+        if (!c->io_pinned[b]) CK(cudaHostAlloc(&c->io_pinned[b], sizeof(double) * kIoChunk, cudaHostAllocDefault));
+        if (!c->io_event[b]) CK(cudaEventCreateWithFlags(&c->io_event[b], cudaEventDisableTiming));
+    }
+    CK(cudaStreamSynchronize(c->stream));  // the column is not in use by queued kernels
+    bool used[2] = {false, false};
+    for (int64_t done = 0, k = 0; done < count; done += kIoChunk, ++k) {
+        const int b = (int)(k & 1);
+        const int64_t m = count - done < kIoChunk ? count - done : kIoChunk;
+        if (used[b]) CK(cudaEventSynchronize(c->io_event[b]));  // its previous copy has landed
+        char* dst = reinterpret_cast<char*>(c->io_pinned[b]);
+        int64_t want = m * (int64_t)sizeof(double), got = 0;
+        const int64_t pos = off + (src_offset + done) * (int64_t)sizeof(double);
+        while (got < want) {
+            const ssize_t r = pread(fd, dst + got, (size_t)(want - got), pos + got);
+            if (r <= 0) return PFB_E_INVALID_ARGUMENT;
+            got += r;
+        }
+        CK(cudaMemcpyAsync(st->cols[col] + dst_offset + done, c->io_pinned[b], (size_t)want,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaEventRecord(c->io_event[b], c->copy_stream));
+        used[b] = true;
+    }
+    CK(cudaStreamSynchronize(c->copy_stream));
+    return PFB_OK;
+}
+
+int pfb_store_check_range(pfb_store* st, int32_t col, int64_t begin, int64_t end, double lower, double upper,
+                          int64_t* first_bad, double* bad_value) {
+    if (!st || !first_bad || col < 0 || col >= st->ncols || begin < 0 || end < begin || end > st->n)
+        return PFB_E_INVALID_ARGUMENT;
+    pfb_ctx* c = st->ctx;
+    *first_bad = -1;
+    if (end == begin) return PFB_OK;
+    CK(cudaSetDevice(c->device));
+    int rc = ensure_bin(c, 0);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->bin_key, 0xff, sizeof(unsigned long long), c->stream));
+    CK(launch_range_check(st->cols[col] + begin, end - begin, lower, upper, c->bin_key, c->stream, c->sm_count));
+    ++c->launches;
+    unsigned long long key = 0;
+    CK(cudaMemcpyAsync(&key, c->bin_key, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (key != ~0ull) {
+        *first_bad = (int64_t)key;
+        double v = 0.0;
+        CK(cudaMemcpy(&v, st->cols[col] + begin + key, sizeof(double), cudaMemcpyDeviceToHost));
+        if (bad_value) *bad_value = v;
+    }
+    return PFB_OK;
 }
 
 }  // extern "C"

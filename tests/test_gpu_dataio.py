@@ -1,0 +1,73 @@
+"""Binary SoA ingest straight to HBM: a dataset loaded from
+column files gives the in-memory dataset's NLL bit for bit, shards load only
+their rows, and the reference's range check raises the same OutOfRange."""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests import models
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import paper_1710_08826_b200 as pf
+    from paper_1710_08826_b200 import _lib as L
+
+    if L.device_count() < 1:
+        pytest.fail("GPU test run without a CUDA device")
+    return pf
+
+
+def test_load_equals_in_memory_and_shards(pf, golden_dir, tmp_path):
+    from paper_1710_08826_b200 import dataio
+    from paper_1710_08826_b200.sharding import shard_bounds
+
+    g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
+    (x, y), pdf, params = models.c2()
+    mem = models.dataset([x, y], [g["x"], g["y"]])
+    files = dataio.save_npy(mem, str(tmp_path))
+    ds = dataio.load_npy([x, y], str(tmp_path))
+    assert ds.n_events == mem.n_events
+    assert pf.nll(pdf, ds) == pf.nll(pdf, mem)
+    assert np.array_equal(np.asarray(ds.column("x")), g["x"])
+    # each rank's shard: its rows only, and the exact partials recombine
+    from paper_1710_08826_b200 import sharding
+
+    w = 3
+    b = shard_bounds(mem.n_events, w)
+    parts = []
+    for r in range(w):
+        sh = dataio.load_npy_shard([x, y], files, r, w)
+        assert sh.n_events == b[r + 1] - b[r]
+        assert np.array_equal(np.asarray(sh.column("y")), g["y"][b[r]:b[r + 1]])
+        snap = pf.snapshot(pdf.param_closure())
+        norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+        parts.append(pf.nll_block_sums(pdf, sh.columns(), snap, norms, 0, sh.n_events))
+    total = sharding.round_acc(sharding.acc_of_values(np.concatenate(parts)))
+    assert total == pf.nll(pdf, mem)
+
+
+def test_range_check_matches_reference_error(pf, tmp_path):
+    from paper_1710_08826_b200 import dataio
+    from paper_1710_08826_b200 import errors as E
+
+    x = pf.Variable.observable("x", 0.0, 10.0)
+    y = pf.Variable.observable("y", 0.0, 10.0)
+    xs = np.linspace(0.0, 10.0, 50001)
+    ys = np.full_like(xs, 5.0)
+    ys[31337] = 10.5
+    ys[40000] = np.nan
+    np.save(tmp_path / "x.npy", xs)
+    np.save(tmp_path / "y.npy", ys)
+    with pytest.raises(E.OutOfRange) as ei:
+        dataio.load_npy([x, y], str(tmp_path))
+    want = None
+    try:
+        models.dataset([x, y], [xs, ys])
+    except E.OutOfRange as exc:
+        want = exc
+    assert want is not None and (ei.value.index, ei.value.value, ei.value.name) == (want.index, want.value, want.name)
