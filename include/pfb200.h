@@ -338,6 +338,11 @@ int pfb_fp64_peak(pfb_ctx* ctx, double* out_tflops);
  * busy for `cycles` clocks, so that a launch queued behind it is timed
  * without host-launch latency.  Uses the NLL kernels' shared-memory carveout. */
 int pfb_ctx_spin(pfb_ctx* ctx, int64_t cycles, const double* flush_buf, int64_t flush_bytes);
+/* Read-bandwidth microbenchmark of `bytes` of a device buffer: mode 0 SIMT
+ * 16-byte loads, 1 bulk-copy ring (1 CTA/SM), 2 bulk-copy ring (2 CTAs/SM)
+ * with chunk_kb-KB stages; median GB/s over reps launches. */
+int pfb_read_bw(pfb_ctx* ctx, const double* buf, int64_t bytes, int32_t mode, int32_t chunk_kb, int32_t reps,
+                double* out_gbps);
 
 #ifdef __cplusplus
 }

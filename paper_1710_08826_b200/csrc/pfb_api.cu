@@ -32,6 +32,8 @@ cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cu
 cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
                               cudaStream_t stream);
 int npy_parse(int fd, int64_t* n_out, int64_t* data_off);
+cudaError_t launch_read_bw(int mode, const double* buf, int64_t bytes, int chunk_kb, double* sink,
+                           unsigned long long* counter, int sm_count, cudaStream_t stream);
 cudaError_t launch_range_check(const double* x, int64_t n, double lo, double hi, unsigned long long* first,
                                cudaStream_t stream, int sm_count);
 struct PcgParams;
@@ -2042,6 +2044,38 @@ int pfb_store_check_range(pfb_store* st, int32_t col, int64_t begin, int64_t end
         CK(cudaMemcpy(&v, st->cols[col] + begin + key, sizeof(double), cudaMemcpyDeviceToHost));
         if (bad_value) *bad_value = v;
     }
+    return PFB_OK;
+}
+
+
+// Read-bandwidth microbenchmark (roofline calibration): `bytes` of a device
+// buffer read once per launch; mode 0 SIMT loads, 1 bulk copies (1 CTA/SM),
+// 2 bulk copies (2 CTAs/SM) with chunk_kb-KB stages.  Median of `reps`.
+int pfb_read_bw(pfb_ctx* c, const double* buf, int64_t bytes, int32_t mode, int32_t chunk_kb, int32_t reps,
+                double* out_gbps) {
+    if (!c || !buf || bytes <= 0 || !out_gbps || mode < 0 || mode > 2 || reps < 1 || chunk_kb < 1)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    int rc = ensure_bin(c, 0);
+    if (rc) return rc;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    std::vector<float> ms;
+    for (int r = 0; r < reps + 1; ++r) {
+        CK(launch_spin_flush(200000, nullptr, 0, c->probe_dev, c->sm_count, c->stream));
+        CK(cudaEventRecord(a, c->stream));
+        CK(launch_read_bw(mode, buf, bytes, chunk_kb, c->probe_dev, c->bin_key, c->sm_count, c->stream));
+        CK(cudaEventRecord(b, c->stream));
+        CK(cudaEventSynchronize(b));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, a, b));
+        if (r) ms.push_back(t);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(ms.begin(), ms.end());
+    *out_gbps = (double)bytes / (ms[ms.size() / 2] * 1e-3) / 1e9;
     return PFB_OK;
 }
 

@@ -114,6 +114,107 @@ cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes
     return cudaGetLastError();
 }
 
+// ---- read-bandwidth microbenchmarks (roofline calibration, not on the NLL path)
+// mode 0: SIMT, 8 x 16-byte loads in flight per thread, grid-stride
+__global__ void __launch_bounds__(256) read_simt_kernel(const double2* __restrict__ p, int64_t n2, double* sink) {
+    double acc = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 7 * stride < n2; i += 8 * stride) {
+        double2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldcs(p + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += v[k].x + v[k].y;
+    }
+    for (; i < n2; i += stride) {
+        const double2 v = __ldcs(p + i);
+        acc += v.x + v.y;
+    }
+    if (acc == 12345.678) sink[0] = acc;
+}
+
+// mode 1/2: bulk copies into an S-stage ring, one producer thread, consumers
+// only wait and release (S x chunk bytes per CTA)
+template <int S>
+__global__ void __launch_bounds__(64) read_bulk_kernel(const char* p, int64_t nchunks, int chunk,
+                                                       unsigned long long* counter, double* sink) {
+    extern __shared__ __align__(128) char ring[];
+    __shared__ unsigned long long full[S], empty[S];
+    __shared__ long long item[S];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            long long nxt = (long long)atomicAdd(counter, 1ull);
+            for (int u = 0;; ++u) {
+                const int s = u % S;
+                mbar_wait(&empty[s], ((u / S) & 1) ^ 1);
+                const long long it = nxt;
+                if (it < nchunks) nxt = (long long)atomicAdd(counter, 1ull);
+                item[s] = it < nchunks ? it : -1;
+                if (it >= nchunks) {
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                mbar_arrive_expect_tx(&full[s], (unsigned)chunk);
+                bulk_g2s(ring + (int64_t)s * chunk, p + it * (int64_t)chunk, (unsigned)chunk, &full[s]);
+            }
+        }
+    } else {
+        double acc = 0.0;
+        for (int u = 0;; ++u) {
+            const int s = u % S;
+            mbar_wait(&full[s], (u / S) & 1);
+            if (item[s] < 0) break;
+            acc += reinterpret_cast<const double*>(ring + (int64_t)s * chunk)[lane];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (acc == 12345.678) sink[0] = acc;
+    }
+}
+
+cudaError_t launch_read_bw(int mode, const double* buf, int64_t bytes, int chunk_kb, double* sink,
+                           unsigned long long* counter, int sm_count, cudaStream_t stream) {
+    if (mode == 0) {
+        read_simt_kernel<<<sm_count * 8, 256, 0, stream>>>(reinterpret_cast<const double2*>(buf), bytes / 16, sink);
+        return cudaGetLastError();
+    }
+    const int chunk = chunk_kb * 1024;
+    const int64_t nchunks = bytes / chunk;
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    if (e) return e;
+    // mode 1: one CTA per SM, as many stages as fit; mode 2: two CTAs per SM
+    const int per_cta = mode == 1 ? 200 * 1024 : 100 * 1024;
+    int S = per_cta / chunk;
+    S = S >= 8 ? 8 : (S >= 6 ? 6 : (S >= 4 ? 4 : (S >= 3 ? 3 : 2)));
+    const size_t smem = (size_t)S * chunk;
+    const int grid = sm_count * (mode == 1 ? 1 : 2);
+#define PFB_RB(SS)                                                                                            \
+    case SS:                                                                                                  \
+        cudaFuncSetAttribute(read_bulk_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        read_bulk_kernel<SS><<<grid, 64, smem, stream>>>(reinterpret_cast<const char*>(buf), nchunks, chunk, \
+                                                         counter, sink);                                      \
+        break;
+    switch (S) {
+        PFB_RB(2)
+        PFB_RB(3)
+        PFB_RB(4)
+        PFB_RB(6)
+        PFB_RB(8)
+    }
+#undef PFB_RB
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream) {
     fp64_peak_kernel<<<blocks, threads, 0, stream>>>(out, iters);
     return cudaGetLastError();

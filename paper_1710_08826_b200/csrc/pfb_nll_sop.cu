@@ -35,8 +35,11 @@ static bool sum2ge_ok(const NllArgs& A) {
     return true;
 }
 
+// pipeline 1: the unit-sum TMA kernel; 2: the reference-tree TMA kernel;
+// 0: the SIMT streaming kernel
 template <class Ev>
 static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    if (A.tma == 1) return launch_tma_sum<Ev>(A, stream, sm_count);
     if (A.tma) return launch_tma<Ev>(A, stream, sm_count);
     return launch_p<Ev>(A, stream, sm_count);
 }
