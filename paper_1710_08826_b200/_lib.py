@@ -12,7 +12,9 @@ import os
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint8, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libpfb200.so")
+# PFB200_LIB selects an alternative build of the same library (A/B kernel
+# experiments in scripts/); the default is the in-tree build.
+LIB_PATH = os.environ.get("PFB200_LIB") or os.path.join(_HERE, "_native", "libpfb200.so")
 
 PFB_BLOCK = 4096
 PFB_NLIMBS = 68
