@@ -67,6 +67,8 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
             return launch_stream<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
         return launch_p<EvSop<2>>(A, stream, sm_count);
     }
+    // the kernels stream exactly the plan's columns (NC of them)
+    if (nc == 3) return launch_p<EvSop<3>>(A, stream, sm_count);
     return launch_p<EvSop<4>>(A, stream, sm_count);
 }
 

@@ -422,8 +422,32 @@ def toys_fixture():
     np.savez_compressed(os.path.join(OUT, "toys.npz"), **out)
 
 
+def trees_fixture():
+    """NLLs of generic trees (polynomial GL norms, nested add/prod, 3-term sums,
+    three observables) from the reference, built from tests/models.TREES."""
+    import parafit
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from tests import models
+
+    out = {}
+    for k, (name, spec) in enumerate(models.TREES):
+        cols = models.tree_data(name, 3 * 4096 + 321, 100 + k)
+        vals = []
+        for scale in (0.0, 0.01, -0.02):
+            root, obs, _ = models.build_tree(parafit, models.perturb(spec, scale))
+            names = sorted(obs)
+            ds = UnbinnedDataSet([obs[c] for c in names])
+            ds.extend([cols[c] for c in names])
+            vals.append(nll(root, ds, snapshot(root.param_closure()), Backend("serial")))
+        for c, v in cols.items():
+            out[f"{name}__{c}"] = v
+        out[f"{name}__nll"] = np.array(vals)
+    np.savez_compressed(os.path.join(OUT, "trees.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned", "toys"]
+    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned", "toys", "trees"]
     for name in which:
         globals()[f"{name}_fixture"]()
     for f in sorted(os.listdir(OUT)):

@@ -83,3 +83,103 @@ def dataset(observables, columns):
     ds = pf.UnbinnedDataSet(list(observables))
     ds.extend([np.asarray(c, dtype=np.float64) for c in columns])
     return ds
+
+
+# --- generic trees: one spec language for the reference, this package and the oracle ---
+
+TREE_OBS = {"x": (0.0, 10.0), "y": (-2.0, 3.0), "z": (0.0, 1.0), "w": (1.0, 4.0)}
+
+# (name, spec) -- leaf specs are the oracle's: ("gaussian", col, mu, sigma, lo, hi),
+# ("exponential", col, alpha, lo, hi), ("polynomial", col, coeffs, lo, hi);
+# ("add", [children], [fractions]), ("prod", [children])
+def _g(c, mu, s):
+    return ("gaussian", c, mu, s) + TREE_OBS[c]
+
+
+def _e(c, a):
+    return ("exponential", c, a) + TREE_OBS[c]
+
+
+def _p(c, coeffs):
+    return ("polynomial", c, list(coeffs)) + TREE_OBS[c]
+
+
+TREES = [
+    ("gauss_poly", ("add", [_g("x", 4.0, 1.2), _p("x", [1.0, 0.2, 0.03])], [0.4])),
+    ("sum_times_poly", ("prod", [("add", [_g("x", 5.0, 0.7), _e("x", -0.2)], [0.6]), _p("y", [2.0, 0.1])])),
+    ("sum_of_prods", ("add", [("prod", [_g("x", 6.0, 1.5), _g("y", 0.5, 0.8)]),
+                              ("prod", [_e("x", -0.3), _p("y", [1.0, 0.2])])], [0.35])),
+    ("three_terms", ("add", [_g("x", 3.0, 0.5), _e("x", -0.15), _p("x", [1.0, -0.05])], [0.3, 0.25])),
+    ("prod3", ("prod", [_g("x", 5.5, 2.0), _e("y", 0.3), _p("z", [0.5, 1.0, 0.2])])),
+    ("prod4", ("prod", [("add", [_g("x", 5.0, 1.0), _e("x", -0.1)], [0.5]), _e("y", 0.2), _p("z", [0.5, 1.0]),
+                        _g("w", 2.5, 0.6)])),
+    ("gauss", _g("x", 4.5, 1.1)),
+    ("expo", _e("x", -0.25)),
+    ("poly", _p("z", [0.3, 0.0, 2.0, 0.5])),
+]
+
+
+def tree_columns(spec, out=None):
+    out = set() if out is None else out
+    if spec[0] in ("add", "prod"):
+        for ch in spec[1]:
+            tree_columns(ch, out)
+    else:
+        out.add(spec[1])
+    return out
+
+
+def build_tree(mod, spec, obs=None, params=None):
+    """The spec as a PdfNode tree of `mod` (the reference package or this one:
+    the builders have the same names).  Returns (root, observables, params)."""
+    obs = {} if obs is None else obs
+    params = [] if params is None else params
+
+    def var_obs(c):
+        if c not in obs:
+            obs[c] = mod.Variable.observable(c, *TREE_OBS[c])
+        return obs[c]
+
+    def par(name, v, lo, hi):
+        p = mod.Variable(f"{name}{len(params)}", v, lo, hi)
+        params.append(p)
+        return p
+
+    k = spec[0]
+    if k == "gaussian":
+        node = mod.gaussian(var_obs(spec[1]), par("mu", spec[2], -20.0, 20.0), par("sg", spec[3], 1e-3, 50.0))
+    elif k == "exponential":
+        node = mod.exponential(var_obs(spec[1]), par("al", spec[2], -10.0, 10.0))
+    elif k == "polynomial":
+        node = mod.polynomial(var_obs(spec[1]), [par("c", c, -10.0, 10.0) for c in spec[2]])
+    elif k == "add":
+        kids = [build_tree(mod, ch, obs, params)[0] for ch in spec[1]]
+        node = mod.add_pdf(kids, [par("f", f, 0.0, 1.0) for f in spec[2]])
+    else:
+        node = mod.prod_pdf([build_tree(mod, ch, obs, params)[0] for ch in spec[1]])
+    return node, obs, params
+
+
+def perturb(spec, scale):
+    """The spec with every parameter multiplied by (1 + scale) (fractions too)."""
+    k = spec[0]
+    if k == "add":
+        return ("add", [perturb(ch, scale) for ch in spec[1]], [f * (1 + scale) for f in spec[2]])
+    if k == "prod":
+        return ("prod", [perturb(ch, scale) for ch in spec[1]])
+    if k == "polynomial":
+        return (k, spec[1], [c * (1 + scale) for c in spec[2]]) + tuple(spec[3:])
+    if k == "gaussian":
+        return (k, spec[1], spec[2] * (1 + scale), spec[3] * (1 + scale)) + tuple(spec[4:])
+    return (k, spec[1], spec[2] * (1 + scale)) + tuple(spec[3:])
+
+
+def tree_data(name, n, seed):
+    """Uniform events over the spec's observables (deterministic per tree)."""
+    rng = np.random.default_rng(seed)
+    spec = dict(TREES)[name]
+    cols = {}
+    for c in sorted(tree_columns(spec)):
+        lo, hi = TREE_OBS[c]
+        cols[c] = rng.uniform(lo, hi, n)
+    return cols

@@ -120,3 +120,12 @@ def test_binned_nonpositive_expectation_pinned(golden_dir):
         O.binned_nll(spec, [("x", 0.0, 1.0, 20)], g["bp_contents"].copy())
     assert ei.value.kind == "NonPositiveExpectation"
     assert ei.value.index == int(g["bp_bin"][0]) and ei.value.value == float(g["bp_value"][0])
+
+
+@pytest.mark.parametrize("name", [t[0] for t in models.TREES])
+def test_generic_trees_pinned(golden_dir, name):
+    g = load(golden_dir, "trees.npz")
+    spec = dict(models.TREES)[name]
+    cols = {c: g[f"{name}__{c}"] for c in models.tree_columns(spec)}
+    got = [O.nll(models.perturb(spec, s), cols) for s in (0.0, 0.01, -0.02)]
+    assert got == g[f"{name}__nll"].tolist()
