@@ -1,7 +1,7 @@
 # Builds the B200 engine (libpfb200.so) and the C oracle.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(EXTRA)
 SRC := paper_1710_08826_b200/csrc
 OUT := paper_1710_08826_b200/_native
 LIB := $(OUT)/libpfb200.so

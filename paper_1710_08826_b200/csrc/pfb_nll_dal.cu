@@ -35,7 +35,11 @@ cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
         case 3:
             return launch_dal<EvDalitz<3>>(A, stream, sm_count);
         case 4:
-            if (signature_of(A.dal) == kSigD0) return launch_dal<EvDalitz<4, kSigD0>>(A, stream, sm_count);
+            if (signature_of(A.dal) == kSigD0) {
+                // product kernels: the reciprocal-free ratio form
+                if (A.tma) return launch_prod<EvDalitzR<kSigD0>>(A, stream, sm_count);
+                return launch_p<EvDalitz<4, kSigD0>>(A, stream, sm_count);
+            }
             return launch_dal<EvDalitz<4>>(A, stream, sm_count);
         default:  // any K: per-term reciprocals, no cache rows
             return launch_p<EvDalitzCached>(A, stream, sm_count);

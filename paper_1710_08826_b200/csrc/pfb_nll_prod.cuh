@@ -124,35 +124,73 @@ struct EvSum2GE {
     }
 };
 
+// Running state of one 16-event unit: the product m * 2^ex of the q factors,
+// for ratio evaluators (Ev::RATIO, p = q / r) the product md * 2^exd of the
+// r factors, and the sum ls of the log factors l.
+struct Unit {
+    double m = 1.0, md = 1.0, ls = 0.0;
+    int ex = 0, exd = 0;
+};
+
+template <class Ev, class = void>
+struct IsRatio {
+    static constexpr bool value = false;
+};
+template <class Ev>
+struct IsRatio<Ev, decltype((void)Ev::RATIO)> {
+    static constexpr bool value = Ev::RATIO;
+};
+
 // One row of a unit: evaluate two events (local block indices e, e+1),
-// mask absent tail events (TAIL), certify, multiply q into m * 2^ex, add l.
+// mask absent tail events (TAIL), certify, multiply into the unit.
 template <class Ev, bool TAIL>
-__device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev::NC], int e, int n, double& m,
-                                         int& ex, double& ls, bool& bad, const double* tab) {
+__device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev::NC], int e, int n, Unit& u,
+                                         bool& bad, const double* tab) {
+    constexpr bool RATIO = IsRatio<Ev>::value;
     bool okx, oky;
     double2 l = make_double2(0.0, 0.0);
-    double2 q = Ev::prob2(A, x, okx, oky, tab, l);
+    double2 r = make_double2(1.0, 1.0);
+    double2 q;
+    if constexpr (RATIO)
+        q = Ev::prob2r(A, x, okx, oky, r);
+    else
+        q = Ev::prob2(A, x, okx, oky, tab, l);
     if (TAIL) {
         if (e >= n) {
             q.x = 1.0;
+            r.x = 1.0;
             l.x = 0.0;
             okx = true;
         }
         if (e + 1 >= n) {
             q.y = 1.0;
+            r.y = 1.0;
             l.y = 0.0;
             oky = true;
         }
     }
-    bad |= !(okx && oky && p_in_range(q.x) && p_in_range(q.y));
-    ls = (ls + l.x) + l.y;
-    m = (m * q.x) * q.y;
-    renorm(m, ex);
+    bool ok = okx && oky && p_in_range(q.x) && p_in_range(q.y);
+    if constexpr (RATIO) {
+        ok = ok && p_in_range(r.x) && p_in_range(r.y);
+        u.md = (u.md * r.x) * r.y;
+        renorm(u.md, u.exd);
+    } else {
+        u.ls = (u.ls + l.x) + l.y;
+    }
+    bad |= !ok;
+    u.m = (u.m * q.x) * q.y;
+    renorm(u.m, u.ex);
 }
 
-__device__ __forceinline__ double unit_value(double m, int ex, double ls) {
-    const double fe = (double)ex;
-    return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(m) + ls));
+template <class Ev>
+__device__ __forceinline__ double unit_value(const Unit& u) {
+    if constexpr (IsRatio<Ev>::value) {
+        const double fe = (double)(u.ex - u.exd);
+        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) - log(u.md)));
+    } else {
+        const double fe = (double)u.ex;
+        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) + u.ls));
+    }
 }
 
 template <int P, class Ev>
@@ -235,8 +273,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
             // register naming (slot r % W holds row r until consumed/refilled)
 #pragma unroll 1
             for (int ju = 0; ju < ROWS / 8; ++ju) {
-                double m = 1.0, ls = 0.0;
-                int ex = 0;
+                Unit un;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int i = 8 * ju + r;
@@ -247,14 +284,13 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                         load_full(cur_item, r0 + i + W, win[r % W]);
                     else if (has_next)
                         load_full(next_item, r0 + i + W - ROWS, win[r % W]);
-                    prod_row<Ev, false>(A, cur, 0, kBlock, m, ex, ls, bad, s_tab);
+                    prod_row<Ev, false>(A, cur, 0, kBlock, un, bad, s_tab);
                 }
-                xch[par][grp][(r0 >> 3) + ju][lane] = unit_value(m, ex, ls);
+                xch[par][grp][(r0 >> 3) + ju][lane] = unit_value<Ev>(un);
             }
         } else {
             // the ragged tail block (once per launch): same structure, rolled
-            double m = 1.0, ls = 0.0;
-            int ex = 0;
+            Unit un;
 #pragma unroll 1
             for (int i = 0; i < ROWS; ++i) {
                 double2 cur[NC];
@@ -268,12 +304,10 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                     load(cur_item, r0 + i + W, win[W - 1]);
                 else if (has_next)
                     load_full(next_item, r0 + i + W - ROWS, win[W - 1]);
-                prod_row<Ev, true>(A, cur, (r0 + i) * 64 + 2 * lane, cur_item.n, m, ex, ls, bad, s_tab);
+                prod_row<Ev, true>(A, cur, (r0 + i) * 64 + 2 * lane, cur_item.n, un, bad, s_tab);
                 if ((i & 7) == 7) {
-                    xch[par][grp][(r0 + i) >> 3][lane] = unit_value(m, ex, ls);
-                    m = 1.0;
-                    ls = 0.0;
-                    ex = 0;
+                    xch[par][grp][(r0 + i) >> 3][lane] = unit_value<Ev>(un);
+                    un = Unit();
                 }
             }
         }
@@ -402,8 +436,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
         const double* xb = mybuf + b * NC * kUnitEvents;
         const bool tail = A.tail && it == 0;
         const int64_t bidx = tail ? A.nfull : it - (A.tail ? 1 : 0);
-        double m = 1.0, ls = 0.0;
-        int ex = 0;
+        Unit un;
         bool bad = false;
         if (!tail) {
 #pragma unroll
@@ -412,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
                     x[c] = *reinterpret_cast<const double2*>(xb + c * kUnitEvents + r * 64 + 2 * lane);
-                prod_row<Ev, false>(A, x, 0, kBlock, m, ex, ls, bad, s_tab);
+                prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab);
             }
         } else {
             const int n = A.tail;
@@ -431,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
                         x[c] = make_double2(v, v);
                     }
                 }
-                prod_row<Ev, true>(A, x, e, n, m, ex, ls, bad, s_tab);
+                prod_row<Ev, true>(A, x, e, n, un, bad, s_tab);
             }
         }
         // No barrier: every warp posts its unit value into ring slot j % R and
@@ -441,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
         if (lane == 0)
             while (ld_volatile(&s_done[slot]) < j / kRing) __nanosleep(32);
         __syncwarp();
-        xch[slot][w][lane] = unit_value(m, ex, ls);
+        xch[slot][w][lane] = unit_value<Ev>(un);
         const unsigned anybad = __any_sync(0xffffffffu, bad);
         unsigned arrived = 0;
         if (lane == 0) {
