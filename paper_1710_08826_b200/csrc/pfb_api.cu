@@ -319,7 +319,7 @@ int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
 }
 
 int pfb_ctx_set_pipeline(pfb_ctx* c, int mode) {
-    if (!c || mode < 0 || mode > 2) return PFB_E_INVALID_ARGUMENT;
+    if (!c || mode < 0 || mode > 3) return PFB_E_INVALID_ARGUMENT;
     c->pipeline = mode;
     return PFB_OK;
 }

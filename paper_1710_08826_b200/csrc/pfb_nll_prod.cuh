@@ -193,6 +193,225 @@ __device__ __forceinline__ double unit_value(const Unit& u) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed unit kernel.  PROD = false: unit sums of log-domain terms (C2 --
+// cheap per-event terms, HBM-bound); PROD = true: the product-mode units
+// above (C1 / Dalitz -- FP64-bound; the consumers read their rows from shared
+// memory instead of waiting on global loads).  Block structure: unit = 8 rows
+// x one lane's 2 columns (row order, x then y), block = lane tree of the unit
+// tree.  Consumers work in
+// teams of eight warps; warp w of a team owns unit-row w (the contiguous 4 KB
+// [512w, 512w+512) of every column block) and teams take alternate stages, so
+// a block costs ~16 evaluations per lane and one barrier-free fold (last of
+// the eight to post).  Blocks are not the reference tree's -- the NLL is
+// within rounding of it, not bitwise -- which is why the known-answer
+// reduction keeps nll_tma_kernel.
+constexpr int kSumWarps = 8;  // warps per team (one unit-row each)
+constexpr int kSumTeams = 2;
+constexpr int kSumThreads = 32 * (kSumWarps * kSumTeams + 1);
+constexpr int kSumRing = 4;
+
+template <class Ev, int S, bool PROD>
+__global__ void __launch_bounds__(kSumThreads, 1) nll_tma_unit_kernel(const __grid_constant__ NllArgs A) {
+    constexpr int NC = Ev::NC;
+    extern __shared__ __align__(128) double stage[];  // S x NC x 4096 doubles
+
+    __shared__ unsigned long long full_bar[S], empty_bar[S];
+    __shared__ long long s_blk[S];
+    __shared__ double xch[kSumTeams][kSumRing][kSumWarps][32];
+    __shared__ int xbad[kSumTeams][kSumRing][kSumWarps];
+    __shared__ unsigned int s_cnt[kSumTeams][kSumRing];
+    __shared__ int s_done[kSumTeams][kSumRing];
+    __shared__ long long sacc[kMaxPts][PFB_ACC_WORDS];
+    __shared__ double s_tab[16];
+    __shared__ unsigned int s_last;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    if (tid < 16) s_tab[tid] = kExp2Tab[tid];
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kSumWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < kMaxPts * PFB_ACC_WORDS; i += blockDim.x) (&sacc[0][0])[i] = 0;
+    if (tid < kSumTeams * kSumRing) {
+        (&s_cnt[0][0])[tid] = 0u;
+        (&s_done[0][0])[tid] = 0;
+    }
+    __syncthreads();
+
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    if (warp == kSumWarps * kSumTeams) {
+        if (lane == 0) {  // producer: as nll_tma_kernel's
+            int64_t it_next = (int64_t)atomicAdd(A.work_counter, 1ull);
+            for (int u = 0;; ++u) {
+                const int s = u % S;
+                mbar_wait(&empty_bar[s], ((u / S) & 1) ^ 1);
+                const int64_t it = it_next;
+                if (it < nitems) it_next = (int64_t)atomicAdd(A.work_counter, 1ull);
+                if (it >= nitems) {
+                    // one end marker per team
+                    s_blk[s] = -1;
+                    mbar_arrive(&full_bar[s]);
+                    for (int extra = 1; extra < kSumTeams; ++extra) {
+                        const int v = u + extra, s2 = v % S;
+                        mbar_wait(&empty_bar[s2], ((v / S) & 1) ^ 1);
+                        s_blk[s2] = -1;
+                        mbar_arrive(&full_bar[s2]);
+                    }
+                    break;
+                }
+                const bool is_tail = A.tail && it == 0;
+                const int64_t bidx = is_tail ? A.nfull : it - (A.tail ? 1 : 0);
+                s_blk[s] = bidx;
+                const unsigned bytes = is_tail ? (unsigned)(8 * (A.tail & ~1)) : (unsigned)(8 * kBlock);
+                mbar_arrive_expect_tx(&full_bar[s], bytes * NC);
+                if (bytes) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        bulk_g2s(stage + ((int64_t)s * NC + c) * kBlock,
+                                 A.col[c] + A.begin + bidx * (int64_t)kBlock, bytes, &full_bar[s]);
+                }
+            }
+        }
+    } else {
+        const int team = warp / kSumWarps;
+        const int w = warp % kSumWarps;
+        int f = 0;
+        for (int u = team;; u += kSumTeams) {
+            const int s = u % S;
+            mbar_wait(&full_bar[s], (u / S) & 1);
+            const int64_t bidx = s_blk[s];
+            if (bidx < 0) break;
+            const double* sx = stage + (int64_t)s * NC * kBlock;
+            const bool tail = A.tail && bidx == A.nfull;
+            const int n = tail ? A.tail : kBlock;
+            for (int m = 0; m < A.npts; ++m) {
+                bool bad = false;
+                double acc = 0.0;
+                Unit un;
+                if (!tail) {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const int e = (8 * w + r) * 64 + 2 * lane;
+                        double2 x[NC];
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
+                        if constexpr (PROD) {
+                            prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab);
+                        } else {
+                            const double2 t = Ev::eval2(A, x, 0, sacc[0], 2, bad, m);
+                            acc = (acc + t.x) + t.y;
+                        }
+                    }
+                } else {
+                    const int64_t gbase = A.begin + A.nfull * (int64_t)kBlock;
+#pragma unroll 1
+                    for (int r = 0; r < 8; ++r) {
+                        const int e = (8 * w + r) * 64 + 2 * lane;
+                        if (e >= n) break;  // rows ascend: nothing further in this lane
+                        const int nv = e + 1 < n ? 2 : 1;
+                        double2 x[NC];
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) {
+                            if (nv == 2) {
+                                x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
+                            } else {  // odd last event: not bulk-copied
+                                const double v = __ldg(A.col[c] + gbase + e);
+                                x[c] = make_double2(v, v);
+                            }
+                        }
+                        if constexpr (PROD) {
+                            prod_row<Ev, true>(A, x, e, n, un, bad, s_tab);
+                        } else {
+                            const double2 t = Ev::eval2(A, x, 0, sacc[0], nv, bad, m);
+                            acc = acc + t.x;
+                            if (nv == 2) acc = acc + t.y;
+                        }
+                    }
+                }
+                if constexpr (PROD) acc = unit_value<Ev>(un);
+                if (m == A.npts - 1) {  // the stage is no longer read by this warp
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty_bar[s]);
+                }
+                const unsigned anybad = __any_sync(0xffffffffu, bad);
+                const int slot = f % kSumRing;
+                if (lane == 0)
+                    while (*reinterpret_cast<volatile int*>(&s_done[team][slot]) < f / kSumRing) __nanosleep(20);
+                __syncwarp();
+                xch[team][slot][w][lane] = acc;
+                unsigned arrived = 0;
+                if (lane == 0) {
+                    xbad[team][slot][w] = anybad ? 1 : 0;
+                    __threadfence_block();
+                    arrived = atomicAdd(&s_cnt[team][slot], 1u);
+                }
+                arrived = __shfl_sync(0xffffffffu, arrived, 0);
+                if (arrived == kSumWarps - 1) {
+                    __threadfence_block();
+                    bool fbad = false;
+#pragma unroll
+                    for (int q = 0; q < kSumWarps; ++q) fbad |= xbad[team][slot][q] != 0;
+                    double bsum = 0.0;
+                    if (!fbad) {
+                        double v[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) v[q] = xch[team][slot][q][lane];
+                        double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+#pragma unroll
+                        for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
+                        bsum = T;
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (fbad) {
+                            const unsigned long long fs = atomicAdd(A.fix_counter, 1ull);
+                            A.fix_list[fs] = (A.block_base + bidx) * kMaxPts + m;
+                        } else {
+                            if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
+                            acc_add_shared(sacc[m], bsum);
+                        }
+                        s_cnt[team][slot] = 0u;
+                        __threadfence_block();
+                        *reinterpret_cast<volatile int*>(&s_done[team][slot]) = f / kSumRing + 1;
+                    }
+                }
+                ++f;
+            }
+        }
+    }
+    finish_launch_pts(A, &sacc[0][0], A.npts * PFB_ACC_WORDS, &s_last);
+}
+
+template <class Ev, bool PROD>
+static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    constexpr int NC = Ev::NC;
+    constexpr int S = NC == 1 ? 6 : (NC == 2 ? 3 : 1);
+    const size_t smem = (size_t)S * NC * kBlock * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(nll_tma_unit_kernel<Ev, S, PROD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    int64_t grid = sm_count;
+    if (grid > nitems) grid = nitems > 0 ? nitems : 1;
+    nll_tma_unit_kernel<Ev, S, PROD><<<(unsigned)grid, kSumThreads, smem, stream>>>(A);
+    return cudaGetLastError();
+}
+
+template <class Ev>
+static cudaError_t launch_tma_sum(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    return launch_tma_unit<Ev, false>(A, stream, sm_count);
+}
+
 template <int P, class Ev>
 __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __grid_constant__ NllArgs A) {
     static_assert(P == 1 || P == 2 || P == 4 || P == 8, "P");
@@ -556,7 +775,12 @@ static cudaError_t launch_prod_one(const NllArgs& A, cudaStream_t stream, int sm
 // tuning knob here too.
 template <class Ev>
 static cudaError_t launch_prod(const NllArgs& A, cudaStream_t stream, int sm_count) {
-    // pipeline 1: bulk-copy variant for single-column evaluators; 2: for all
+    // pipeline 1: per-warp bulk prefetch for single-column evaluators, the
+    // TMA-fed unit kernel (producer warp + two consumer teams) for two-column
+    // ones (Dalitz: 3% faster than the register window, measured);
+    // 2: bulk prefetch for all; 3: the TMA unit kernel for all
+    if (A.warps == 0 && (A.tma == 3 || (Ev::NC == 2 && A.tma == 1)))
+        return launch_tma_unit<Ev, true>(A, stream, sm_count);
     if (A.warps == 0 && (A.tma == 2 || (Ev::NC == 1 && A.tma == 1))) return launch_prod_bulk<Ev>(A, stream, sm_count);
     switch (A.warps) {
         case 1:

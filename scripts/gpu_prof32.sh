@@ -1,0 +1,2 @@
+timeout 600 python -m pytest tests/test_gpu_trees.py -q -x 2>&1 | tail -2
+for i in 1 2; do for p in 1 3; do timeout 300 python scripts/kernel_sweep.py --configs c3,c1 --warps 0 --pipeline $p 2>&1 | grep '"c[13]"' | cut -c1-110; done; done

@@ -25,7 +25,7 @@ def pf():
     return pf
 
 
-@pytest.mark.parametrize("pipeline", [1, 2, 0])
+@pytest.mark.parametrize("pipeline", [1, 2, 0, 3])
 @pytest.mark.parametrize("name", [t[0] for t in models.TREES])
 def test_tree_nll_matches_reference(pf, golden_dir, name, pipeline):
     from paper_1710_08826_b200 import _lib as L
