@@ -93,10 +93,10 @@ __device__ __forceinline__ double exp_tab(double x, const double* tab) {
 // Leaf/term layout fixed by the dispatcher: leaf 0 gaussian (ptv[0][0..1] =
 // mu, 1/sigma), leaf 1 exponential (ptv[0][2] = alpha), term t = leaf t, and
 // |ln c_t| < 200.
-// Certification: |u1| <= 250 and q in [2^-500, 2^500] (kernel check) put p
-// in [2^-861, 2^861] and keep the reference's exp(u1) finite and normal; a
-// subnormal exp(u0) in the reference is then below 2^-84 p (negligible).
-// d = u0 - u1 <= -u1 <= 250 for a certified event (u0 <= 0) and is clamped
+// Certification: |u1| < 256 and q in [2^-500, 2^500] (kernel check) put p
+// in [2^-870, 2^870] and keep the reference's exp(u1) finite and normal; a
+// subnormal exp(u0) in the reference is then below 2^-75 p (negligible).
+// d = u0 - u1 <= -u1 < 256 for a certified event (u0 <= 0) and is clamped
 // below at -707 (then c0 e^d < 2^-700 c1, negligible); whatever exp_tab
 // returns for an uncertified event (NaN d, d > 707) is discarded.
 struct EvSum2GE {
@@ -104,13 +104,17 @@ struct EvSum2GE {
     static constexpr int U = 4;
     static constexpr int MINB = 3;
 
+    // d = -(x - mu)^2 / (2 sigma^2) - alpha x as one FMA: c2 = -1/(2 sigma^2)
+    // is loop-invariant.  |u1| < 256 is read off the exponent bits (no FP64 op).
     __device__ static __forceinline__ double one(const NllArgs& A, double x, const double* tab, bool& ok,
                                                  double& l) {
-        const double z = (x - A.ptv[0][0]) * A.ptv[0][1];
+        const double is = A.ptv[0][1];
+        const double c2 = (-0.5 * is) * is;
+        const double w = x - A.ptv[0][0];
         const double u1 = A.ptv[0][2] * x;
-        double d = (-0.5 * z) * z - u1;
+        double d = fma(c2 * w, w, -u1);
         d = d < -707.0 ? -707.0 : d;
-        ok = fabs(u1) <= 250.0;  // certified => d <= 250: no upper clamp
+        ok = (__double2hiint(u1) & 0x7fffffff) < 0x40700000;  // |u1| < 256 => d <= 256: no upper clamp
         l = u1;
         return fma(A.term[0].coef, exp_tab(d, tab), A.term[1].coef);
     }
@@ -207,12 +211,20 @@ __device__ __forceinline__ double unit_value(const Unit& u) {
 // within rounding of it, not bitwise -- which is why the known-answer
 // reduction keeps nll_tma_kernel.
 constexpr int kSumWarps = 8;  // warps per team (one unit-row each)
-constexpr int kSumTeams = 2;
-constexpr int kSumThreads = 32 * (kSumWarps * kSumTeams + 1);
+#ifndef PFB_UNIT_TEAMS1
+#define PFB_UNIT_TEAMS1 3
+#endif
+// consumer teams: 2 for two-column stages (3 x 64 KB), 3 for one-column
+// stages (6 x 32 KB) when the evaluator fits 80 registers
+template <class Ev>
+struct UnitTeams {
+    static constexpr int value = Ev::NC == 1 ? PFB_UNIT_TEAMS1 : 2;
+};
 constexpr int kSumRing = 4;
 
-template <class Ev, int S, bool PROD>
-__global__ void __launch_bounds__(kSumThreads, 1) nll_tma_unit_kernel(const __grid_constant__ NllArgs A) {
+template <class Ev, int S, bool PROD, int TEAMS = UnitTeams<Ev>::value>
+__global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_kernel(const __grid_constant__ NllArgs A) {
+    constexpr int kSumTeams = TEAMS;
     constexpr int NC = Ev::NC;
     extern __shared__ __align__(128) double stage[];  // S x NC x 4096 doubles
 
@@ -403,7 +415,7 @@ static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
     int64_t grid = sm_count;
     if (grid > nitems) grid = nitems > 0 ? nitems : 1;
-    nll_tma_unit_kernel<Ev, S, PROD><<<(unsigned)grid, kSumThreads, smem, stream>>>(A);
+    nll_tma_unit_kernel<Ev, S, PROD><<<(unsigned)grid, 32 * (kSumWarps * UnitTeams<Ev>::value + 1), smem, stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -572,7 +584,10 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
 // with conflict-free 16-byte shared loads.
 constexpr int kBulkWarps = 8;
 constexpr int kUnitEvents = 512;  // events per warp per item
-constexpr int kRing = 4;          // block-fold slots (warps may drift this many items)
+#ifndef PFB_BULK_RING
+#define PFB_BULK_RING 4
+#endif
+constexpr int kRing = PFB_BULK_RING;  // block-fold slots (warps may drift this many items)
 
 template <class T>
 __device__ __forceinline__ T ld_volatile(const T* p) {
