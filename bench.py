@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override events per GPU")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: accumulator all-reduce through NCCL or the peer-memory kernel (pfb_peer_*)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -262,6 +264,11 @@ def main():
     out = ctypes.c_double()
     err = L.PfbErr()
 
+    peers = None
+    if world > 1 and args.collective == "peer":
+        from paper_1710_08826_b200.sharding import PeerGroup
+
+        peers = PeerGroup(ctx, rank, world)
     ev_a = torch.cuda.Event(enable_timing=True)
     ev_b = torch.cuda.Event(enable_timing=True)
 
@@ -277,7 +284,10 @@ def main():
         ev_a.record()
         L.check(L.lib().pfb_nll_partial_async(ctx.handle, plan.handle, store, 0, n_per, 0, L.dptr(vals), len(vals),
                                               L.dptr(nv), len(nv), ctypes.c_void_p(acc.data_ptr())), "partial")
-        torch.distributed.all_reduce(acc)
+        if peers is not None:
+            peers.allreduce(acc)
+        else:
+            torch.distributed.all_reduce(acc)
         ev_b.record()
         fails = ctypes.c_int64()
         L.check(L.lib().pfb_finalize(ctx.handle, ctypes.c_void_p(acc.data_ptr()), ctypes.byref(out),
@@ -392,7 +402,8 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[cfg]["workload"], "n_events_per_gpu": n_per,
                    "evaluator": plan.evaluator, "l2": "flushed (256 MB read) before every step",
-                   "parallelism": f"events sharded over {world} GPU(s), 1 all-reduce of 72 int64 per call"},
+                   "parallelism": f"events sharded over {world} GPU(s), 1 all-reduce of 72 int64 per call"
+                                  + (f" ({args.collective})" if world > 1 else "")},
         "nll_evals_per_s": args.steps / dev_s,
         "nll": nll_value,
         "wall_s": wall,

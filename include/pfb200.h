@@ -66,6 +66,7 @@ enum pfb_status {
     PFB_E_ENVELOPE_HIT = 10,       /* toy generation: a density above the envelope
                                       (mcgen.py _EnvelopeHit; caller rescans) */
     PFB_E_ATTEMPTS_EXHAUSTED = 11, /* AttemptsExhausted                  errors.py */
+    PFB_E_PEER_TIMEOUT = 12,       /* a peer rank never posted its accumulator */
     PFB_E_INVALID_ARGUMENT = 20,
     PFB_E_UNSUPPORTED_PLAN = 21,
     PFB_E_CUDA = 30,
@@ -294,6 +295,22 @@ int pfb_store_load_npy(pfb_store* store, int32_t col, const char* path, int64_t 
  * [begin, end) with x < lower, x > upper or non-finite (-1 if none). */
 int pfb_store_check_range(pfb_store* store, int32_t col, int64_t begin, int64_t end, double lower, double upper,
                           int64_t* first_bad, double* bad_value);
+
+/* ---- cross-GPU accumulator exchange over peer memory ------------------ */
+/* Replaces the NCCL all-reduce of the 72-limb accumulator between the
+ * one-process-per-GPU ranks with one single-CTA kernel over NVLink peer
+ * memory.  Setup: pfb_peer_create (mailbox in this GPU's HBM; out_handle
+ * receives its 64-byte cudaIpcMemHandle), exchange the handles between ranks
+ * (e.g. torch.distributed.all_gather_object), pfb_peer_open.  Each call:
+ * pfb_peer_allreduce sums dev_acc[0..72) over the ranks in place (rank order,
+ * integer limbs: bitwise the single-GPU accumulator); PFB_E_PEER_TIMEOUT if a
+ * peer does not post within timeout_s.  pfb_peer_attach / pfb_peer_mailbox
+ * wire peers living in the same process (raw device pointers). */
+int pfb_peer_create(pfb_ctx* ctx, int32_t rank, int32_t world, uint8_t* out_handle);
+int pfb_peer_open(pfb_ctx* ctx, const uint8_t* handles);
+int pfb_peer_attach(pfb_ctx* ctx, const void* const* mailboxes);
+int pfb_peer_mailbox(pfb_ctx* ctx, void** out);
+int pfb_peer_allreduce(pfb_ctx* ctx, int64_t* dev_acc, double timeout_s);
 
 /* ---- sharding ------------------------------------------------------------------ */
 /* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */

@@ -35,6 +35,7 @@ E_INVALID_SUM = 8
 E_NONPOSITIVE_EXPECTATION = 9
 E_ENVELOPE_HIT = 10
 E_ATTEMPTS_EXHAUSTED = 11
+E_PEER_TIMEOUT = 12
 E_INVALID_ARGUMENT = 20
 E_UNSUPPORTED_PLAN = 21
 E_CUDA = 30
@@ -142,6 +143,11 @@ _SIGNATURES = [
     ("pfb_store_download", c_int, [_PTR, c_int32, _DBL_P, c_int64, c_int64]),
     ("pfb_fp64_peak", c_int, [_PTR, _DBL_P]),
     ("pfb_ctx_spin", c_int, [_PTR, c_int64, _PTR, c_int64]),
+    ("pfb_peer_create", c_int, [_PTR, c_int32, c_int32, _PTR]),
+    ("pfb_peer_open", c_int, [_PTR, _PTR]),
+    ("pfb_peer_attach", c_int, [_PTR, _PTR]),
+    ("pfb_peer_mailbox", c_int, [_PTR, POINTER(_PTR)]),
+    ("pfb_peer_allreduce", c_int, [_PTR, _PTR, c_double]),
     ("pfb_read_bw", c_int, [_PTR, _PTR, c_int64, c_int32, c_int32, c_int32, _DBL_P]),
     ("pfb_npy_length", c_int, [ctypes.c_char_p, _I64_P]),
     ("pfb_store_load_npy", c_int, [_PTR, c_int32, ctypes.c_char_p, c_int64, c_int64, c_int64]),

@@ -36,6 +36,11 @@ cudaError_t launch_read_bw(int mode, const double* buf, int64_t bytes, int chunk
                            unsigned long long* counter, int sm_count, cudaStream_t stream);
 cudaError_t launch_range_check(const double* x, int64_t n, double lo, double hi, unsigned long long* first,
                                cudaStream_t stream, int sm_count);
+cudaError_t launch_peer_allreduce(long long* const* mbox, int world, int rank, unsigned long long seq,
+                                  long long timeout_cycles, long long* acc, unsigned long long* status,
+                                  cudaStream_t stream);
+size_t peer_mailbox_bytes();
+int peer_max();
 struct PcgParams;
 struct PcgHostResult {
     int status;
@@ -121,6 +126,12 @@ struct pfb_ctx {
     double* e2e_dev[kMaxCols] = {nullptr, nullptr, nullptr, nullptr};
     int64_t e2e_cap = 0;
     std::vector<cudaEvent_t> chunk_events;
+    // cross-GPU accumulator exchange over peer memory (pfb_peer_*)
+    int peer_world = 0, peer_rank = 0;
+    long long* peer_ptr[16] = {};
+    bool peer_ipc[16] = {};
+    unsigned long long peer_seq = 0;
+    unsigned long long* peer_status = nullptr;
     // file ingest staging (pfb_store_load_npy)
     double* io_pinned[2] = {nullptr, nullptr};
     cudaEvent_t io_event[2] = {nullptr, nullptr};
@@ -207,6 +218,10 @@ const char* pfb_strerror(int code) {
         case PFB_E_NONPOSITIVE_NORM: return "non-positive normalisation";
         case PFB_E_DEGENERATE_GRID: return "degenerate grid";
         case PFB_E_INVALID_SUM: return "-inf + inf in exact sum";
+        case PFB_E_NONPOSITIVE_EXPECTATION: return "non-positive binned expectation";
+        case PFB_E_ENVELOPE_HIT: return "density above the generation envelope";
+        case PFB_E_ATTEMPTS_EXHAUSTED: return "generation attempts exhausted";
+        case PFB_E_PEER_TIMEOUT: return "peer rank did not post its accumulator";
         case PFB_E_INVALID_ARGUMENT: return "invalid argument";
         case PFB_E_UNSUPPORTED_PLAN: return "unsupported plan";
         case PFB_E_CUDA: return "CUDA error";
@@ -282,6 +297,11 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaFree(c->bsums);
     cudaFree(c->bin_dev);
     cudaFree(c->bin_key);
+    for (int q = 0; q < 16; ++q) {
+        if (c->peer_ipc[q] && c->peer_ptr[q]) cudaIpcCloseMemHandle(c->peer_ptr[q]);
+    }
+    if (c->peer_world) cudaFree(c->peer_ptr[c->peer_rank]);
+    cudaFree(c->peer_status);
     for (int b = 0; b < 2; ++b) {
         if (c->io_pinned[b]) cudaFreeHost(c->io_pinned[b]);
         if (c->io_event[b]) cudaEventDestroy(c->io_event[b]);
@@ -2077,6 +2097,76 @@ int pfb_read_bw(pfb_ctx* c, const double* buf, int64_t bytes, int32_t mode, int3
     std::sort(ms.begin(), ms.end());
     *out_gbps = (double)bytes / (ms[ms.size() / 2] * 1e-3) / 1e9;
     return PFB_OK;
+}
+
+
+// ---- cross-GPU accumulator exchange over peer memory ---------------
+
+int pfb_peer_create(pfb_ctx* c, int32_t rank, int32_t world, uint8_t* out_handle) {
+    if (!c || world < 1 || world > peer_max() || rank < 0 || rank >= world || c->peer_world)
+        return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    long long* m = nullptr;
+    CK(cudaMalloc(&m, peer_mailbox_bytes()));
+    CK(cudaMemset(m, 0, peer_mailbox_bytes()));
+    if (!c->peer_status) CK(cudaMalloc(&c->peer_status, sizeof(unsigned long long)));
+    c->peer_world = world;
+    c->peer_rank = rank;
+    c->peer_ptr[rank] = m;
+    c->peer_seq = 0;
+    if (out_handle) {
+        cudaIpcMemHandle_t h;
+        memset(&h, 0, sizeof(h));
+        if (world > 1) CK(cudaIpcGetMemHandle(&h, m));
+        memcpy(out_handle, &h, sizeof(h));
+    }
+    return PFB_OK;
+}
+
+int pfb_peer_open(pfb_ctx* c, const uint8_t* handles) {
+    if (!c || !handles || !c->peer_world) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    for (int q = 0; q < c->peer_world; ++q) {
+        if (q == c->peer_rank || c->peer_ptr[q]) continue;
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + (size_t)q * sizeof(cudaIpcMemHandle_t), sizeof(h));
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->peer_ptr[q] = static_cast<long long*>(p);
+        c->peer_ipc[q] = true;
+    }
+    return PFB_OK;
+}
+
+int pfb_peer_attach(pfb_ctx* c, const void* const* mailboxes) {
+    if (!c || !mailboxes || !c->peer_world) return PFB_E_INVALID_ARGUMENT;
+    for (int q = 0; q < c->peer_world; ++q)
+        if (q != c->peer_rank) c->peer_ptr[q] = static_cast<long long*>(const_cast<void*>(mailboxes[q]));
+    return PFB_OK;
+}
+
+int pfb_peer_mailbox(pfb_ctx* c, void** out) {
+    if (!c || !out || !c->peer_world) return PFB_E_INVALID_ARGUMENT;
+    *out = c->peer_ptr[c->peer_rank];
+    return PFB_OK;
+}
+
+int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {
+    if (!c || !dev_acc || !c->peer_world || !(timeout_s > 0.0)) return PFB_E_INVALID_ARGUMENT;
+    for (int q = 0; q < c->peer_world; ++q)
+        if (!c->peer_ptr[q]) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    int khz = 0;
+    CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device));
+    const long long cycles = (long long)(timeout_s * (double)khz * 1e3);
+    const unsigned long long seq = ++c->peer_seq;
+    CK(launch_peer_allreduce(c->peer_ptr, c->peer_world, c->peer_rank, seq, cycles,
+                             reinterpret_cast<long long*>(dev_acc), c->peer_status, c->stream));
+    ++c->launches;
+    unsigned long long st = 0;
+    CK(cudaMemcpyAsync(&st, c->peer_status, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return st ? PFB_E_PEER_TIMEOUT : PFB_OK;
 }
 
 }  // extern "C"

@@ -159,6 +159,32 @@ def allreduce_accumulator(acc, group=None):
     return acc
 
 
+class PeerGroup:
+    """The ranks' accumulator exchange over NVLink peer memory (pfb_peer_*):
+    one single-CTA kernel per call instead of an NCCL all-reduce.  Handles are
+    exchanged once with torch.distributed; `allreduce(acc)` sums an int64[72]
+    CUDA tensor in place, bitwise the NCCL result."""
+
+    def __init__(self, ctx, rank: int, world: int, group=None, timeout_s: float = 10.0):
+        self.ctx, self.rank, self.world, self.timeout_s = ctx, int(rank), int(world), float(timeout_s)
+        handle = (ctypes.c_uint8 * 64)()
+        L.check(L.lib().pfb_peer_create(ctx.handle, self.rank, self.world, handle), "pfb_peer_create")
+        handles = [bytes(handle)]
+        if self.world > 1:
+            import torch.distributed as dist
+
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        buf = (ctypes.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        L.check(L.lib().pfb_peer_open(ctx.handle, buf), "pfb_peer_open")
+
+    def allreduce(self, acc) -> None:
+        code = L.lib().pfb_peer_allreduce(self.ctx.handle, ctypes.c_void_p(acc.data_ptr()), self.timeout_s)
+        if code == L.E_PEER_TIMEOUT:
+            raise TimeoutError(f"rank {self.rank}: a peer did not post its accumulator within {self.timeout_s} s")
+        L.check(code, "pfb_peer_allreduce")
+
+
 class ShardedNll:
     """Rank-local shard of a dataset resident in this rank's HBM.
 
@@ -167,10 +193,13 @@ class ShardedNll:
     Every rank returns the same bits, equal to the single-GPU NLL.
     """
 
-    def __init__(self, pdf, ds, rank: int, world: int, device: int, group=None):
+    def __init__(self, pdf, ds, rank: int, world: int, device: int, group=None, collective: str = "nccl"):
         import torch
 
         from . import engine
+
+        if collective not in ("nccl", "peer"):
+            raise ValueError("collective must be 'nccl' or 'peer'")
 
         self.pdf = pdf
         self.rank, self.world, self.group = int(rank), int(world), group
@@ -186,6 +215,7 @@ class ShardedNll:
         self.store = self.ctx.store_for(self.arrays)
         self.acc = torch.zeros(L.PFB_ACC_WORDS, dtype=torch.int64, device=f"cuda:{device}")
         self.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        self.peers = PeerGroup(self.ctx, rank, world, group) if collective == "peer" else None
 
     def launch(self, snap, norms):
         """Enqueue the local partial (no host sync)."""
@@ -198,7 +228,10 @@ class ShardedNll:
     def finish(self) -> float:
         from . import engine
 
-        allreduce_accumulator(self.acc, self.group)
+        if self.peers is not None:
+            self.peers.allreduce(self.acc)
+        else:
+            allreduce_accumulator(self.acc, self.group)
         out = ctypes.c_double()
         fails = ctypes.c_int64()
         code = L.lib().pfb_finalize(self.ctx.handle, ctypes.c_void_p(self.acc.data_ptr()), ctypes.byref(out),
