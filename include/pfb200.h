@@ -360,6 +360,9 @@ int pfb_ctx_spin(pfb_ctx* ctx, int64_t cycles, const double* flush_buf, int64_t 
  * with chunk_kb-KB stages; median GB/s over reps launches. */
 int pfb_read_bw(pfb_ctx* ctx, const double* buf, int64_t bytes, int32_t mode, int32_t chunk_kb, int32_t reps,
                 double* out_gbps);
+/* Launch fixed-cost microbenchmark: mode 0 empty kernel, 1 + NllArgs
+ * parameter block, 2 + constant-bank reads, 3 + accumulator epilogue. */
+int pfb_overhead_probe(pfb_ctx* ctx, int32_t mode, int32_t reps, double* out_us);
 
 #ifdef __cplusplus
 }

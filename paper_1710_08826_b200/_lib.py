@@ -149,6 +149,7 @@ _SIGNATURES = [
     ("pfb_peer_mailbox", c_int, [_PTR, POINTER(_PTR)]),
     ("pfb_peer_allreduce", c_int, [_PTR, _PTR, c_double]),
     ("pfb_read_bw", c_int, [_PTR, _PTR, c_int64, c_int32, c_int32, c_int32, _DBL_P]),
+    ("pfb_overhead_probe", c_int, [_PTR, c_int32, c_int32, _DBL_P]),
     ("pfb_npy_length", c_int, [ctypes.c_char_p, _I64_P]),
     ("pfb_store_load_npy", c_int, [_PTR, c_int32, ctypes.c_char_p, c_int64, c_int64, c_int64]),
     ("pfb_store_check_range", c_int, [_PTR, c_int32, c_int64, c_int64, c_double, c_double, _I64_P, _DBL_P]),

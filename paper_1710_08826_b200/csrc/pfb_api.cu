@@ -32,6 +32,7 @@ cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cu
 cudaError_t launch_spin_flush(long long cycles, const double* buf, int64_t bytes, double* sink, int sm_count,
                               cudaStream_t stream);
 int npy_parse(int fd, int64_t* n_out, int64_t* data_off);
+cudaError_t launch_overhead_probe(int mode, const NllArgs& A, double* sink, cudaStream_t stream);
 cudaError_t launch_read_bw(int mode, const double* buf, int64_t bytes, int chunk_kb, double* sink,
                            unsigned long long* counter, int sm_count, cudaStream_t stream);
 cudaError_t launch_range_check(const double* x, int64_t n, double lo, double hi, unsigned long long* first,
@@ -2167,6 +2168,45 @@ int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {
     CK(cudaMemcpyAsync(&st, c->peer_status, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return st ? PFB_E_PEER_TIMEOUT : PFB_OK;
+}
+
+
+// Fixed-cost microbenchmark of one launch (event-timed, median of reps):
+// mode 0 empty kernel, 1 + the 6.4 KB NllArgs parameter block, 2 + 64
+// constant-bank reads, 3 + the accumulator epilogue (finish_launch).
+int pfb_overhead_probe(pfb_ctx* c, int32_t mode, int32_t reps, double* out_us) {
+    if (!c || !out_us || reps < 1 || mode < 0 || mode > 3) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    memset(A.get(), 0, sizeof(NllArgs));
+    A->acc = c->acc;
+    A->ticket = c->ticket;
+    A->work_counter = c->work_counter;
+    A->errkey = c->errkey;
+    A->acc_out = c->res_dev + kResHead;
+    A->result_i = c->res_dev;
+    A->fix_counter = c->fix_counter;
+    A->mode = MODE_EXPORT;
+    A->npts = 1;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    std::vector<float> ms;
+    for (int r = 0; r < reps + 1; ++r) {
+        CK(launch_spin_flush(400000, nullptr, 0, c->probe_dev, c->sm_count, c->stream));
+        CK(cudaEventRecord(a, c->stream));
+        CK(launch_overhead_probe(mode, *A, c->probe_dev, c->stream));
+        CK(cudaEventRecord(b, c->stream));
+        CK(cudaEventSynchronize(b));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, a, b));
+        if (r) ms.push_back(t);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(ms.begin(), ms.end());
+    *out_us = 1e3 * ms[ms.size() / 2];
+    return PFB_OK;
 }
 
 }  // extern "C"

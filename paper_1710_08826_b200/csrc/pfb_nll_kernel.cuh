@@ -773,6 +773,17 @@ enum KernelMode : int32_t {
     MODE_ACCUM = 2        // chained launches: keep accumulating
 };
 
+// Last-CTA election: one acq_rel atomic on the ticket replaces two
+// device-wide SC fences (__threadfence = MEMBAR.SC.GPU, microseconds on the
+// two-die B200): the release is cumulative over this CTA's accumulator
+// atomics (ordered before it by the CTA barrier), and the last CTA's acquire
+// makes every CTA's atomics visible to it.
+__device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* t) {
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    return old;
+}
+
 // Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and
 // resets the launch-scoped counters.  Shared by every fast kernel.
 template <bool LIST>
@@ -780,30 +791,27 @@ __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc,
     __syncthreads();
     for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x)
         if (sacc[i]) atomicAdd(A.acc + i, (unsigned long long)sacc[i]);
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (threadIdx.x == 0) *s_last = (ticket_acq_rel(A.ticket) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!*s_last) return;
-    if (threadIdx.x == 0) *A.work_counter = 0ull;
-    if (A.mode == MODE_ACCUM) {
-        if (threadIdx.x == 0) *A.ticket = 0u;
-        return;
+    // the last CTA: independent global round trips issued by different
+    // threads, so the export costs one atomic latency, not four in a row
+    const int t = threadIdx.x, nt = blockDim.x;
+    if (t == nt - 1) {
+        *A.work_counter = 0ull;
+        *A.ticket = 0u;
     }
-    __threadfence();
-    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) {
+    if (A.mode == MODE_ACCUM) return;
+    if (t == nt - 2 && !LIST)  // hand the deferred-block count to the fix-up launch
+        A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
+    if (t == nt - 3) A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
+    for (int i = t; i < PFB_ACC_WORDS; i += nt) {
         const long long v = (long long)atomicExch(A.acc + i, 0ull);
         if (A.mode == MODE_EXPORT)
             A.acc_out[i] = v;
         else
             A.acc_out[i] += v;
-    }
-    if (threadIdx.x == 0) {
-        *A.ticket = 0u;
-        if (!LIST) {  // hand the deferred-block count to the fix-up launch
-            A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
-        }
-        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
     }
 }
 

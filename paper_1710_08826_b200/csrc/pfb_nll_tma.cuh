@@ -77,28 +77,24 @@ __device__ __forceinline__ void finish_launch_pts(const NllArgs& A, long long* s
     __syncthreads();
     for (int i = tid; i < nwords; i += blockDim.x)
         if (sflat[i]) atomicAdd(A.acc + i, (unsigned long long)sflat[i]);
-    __threadfence();
     __syncthreads();
-    if (tid == 0) *s_last = (atomicAdd(A.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (tid == 0) *s_last = (ticket_acq_rel(A.ticket) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!*s_last) return;
-    if (tid == 0) *A.work_counter = 0ull;
-    if (A.mode == MODE_ACCUM) {
-        if (tid == 0) *A.ticket = 0u;
-        return;
+    const int nt = blockDim.x;  // independent round trips on different threads
+    if (tid == nt - 1) {
+        *A.work_counter = 0ull;
+        *A.ticket = 0u;
     }
-    __threadfence();
-    for (int i = tid; i < nwords; i += blockDim.x) {
+    if (A.mode == MODE_ACCUM) return;
+    if (tid == nt - 2) A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
+    if (tid == nt - 3) A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
+    for (int i = tid; i < nwords; i += nt) {
         const long long v = (long long)atomicExch(A.acc + i, 0ull);
         if (A.mode == MODE_EXPORT)
             A.acc_out[i] = v;
         else
             A.acc_out[i] += v;
-    }
-    if (tid == 0) {
-        *A.ticket = 0u;
-        A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
-        A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
     }
 }
 

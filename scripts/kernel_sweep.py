@@ -90,7 +90,7 @@ def main():
             obs, pdf, _ = models.c2()
         else:
             terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
-            cols = list(mcgen.dalitz(n, terms, models.D_CHANNEL_T, 3))
+            cols = list(mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 3))  # Philox on the GPU
             obs, pdf, _ = models.c3()
         gen_s = time.perf_counter() - t0
         ds = pf.UnbinnedDataSet(list(obs))
