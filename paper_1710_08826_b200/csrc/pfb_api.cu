@@ -868,6 +868,16 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     }
     build_dal(p, values, A);
     A->inv_norm = 1.0 / norms[A->nops - 1];
+    {
+        const double sn = sqrt(A->inv_norm);
+        for (int k = 0; k < A->dal.K && k < kMaxDal; ++k) {
+            DalTerm& T = A->dal.t[k];
+            T.scre = T.cre * sn;
+            T.scim = T.cim * sn;
+            T.salpha = T.alpha * sn;
+            T.sbeta = T.beta * sn;
+        }
+    }
     // sum of products
     A->npts = 1;
     A->fix_point = 0;

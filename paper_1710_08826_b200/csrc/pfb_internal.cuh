@@ -85,6 +85,9 @@ struct DalTerm {
     double cre, cim;  // magnitude*(cos phase, sin phase)
     double alpha;     // cre*m^2 - cim*m*G
     double beta;      // cre*m*G + cim*m^2
+    // the same four scaled by sqrt(1/norm) (ratio evaluator: |N|^2 / norm
+    // without a per-event multiply)
+    double scre, scim, salpha, sbeta;
 };
 
 struct DalDesc {

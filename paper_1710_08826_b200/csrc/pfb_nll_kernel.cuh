@@ -491,14 +491,17 @@ struct EvDalitz {
 //   sum_k c_k BW_k Z_k = N / D',  N = sum_k E_k [(alpha_k - cre_k s) + i (beta_k - cim_k s)],
 //   E_k = prod_{j != k} d_j * Z_k * sigma,
 // so p = |N|^2 / norm / D'^2 needs no reciprocal at all: the kernel multiplies
-// numerators and denominators into separate unit products.  ~49 FP64
-// operations per event against ~57 plus a reciprocal for EvDalitz.
+// numerators and denominators into separate unit products (D' itself; the
+// square is taken on the unit's logarithm), and 1/norm rides in the
+// coefficients (sqrt(1/norm) each).  ~47 FP64 operations per event against
+// ~57 plus a reciprocal for EvDalitz.
 template <int SIG>
 struct EvDalitzR {
     static constexpr int NC = 2;
     static constexpr int U = 2;
     static constexpr int MINB = PFB_DALR_MINB;
     static constexpr bool RATIO = true;
+    static constexpr int RATIO_POW = 2;  // p = num / den^2
     static constexpr int K = 4;
     static_assert(SIG >= 0, "compile-time term structure required");
 
@@ -558,12 +561,11 @@ struct EvDalitzR {
                 }
             }
             const double E = ex[k] * F;
-            tr = fma(E, fma(-T.cre, sv[k], T.alpha), tr);
-            ti = fma(E, fma(-T.cim, sv[k], T.beta), ti);
+            tr = fma(E, fma(-T.scre, sv[k], T.salpha), tr);  // coefficients carry sqrt(1/norm)
+            ti = fma(E, fma(-T.scim, sv[k], T.sbeta), ti);
         }
-        num = fma(tr, tr, ti * ti) * A.inv_norm;
-        const double Dn = any ? (pre3 * d[3]) * sig : pre3 * d[3];
-        den = Dn * Dn;
+        num = fma(tr, tr, ti * ti);
+        den = any ? (pre3 * d[3]) * sig : pre3 * d[3];  // D'; the kernel squares at the unit end
     }
 
     __device__ static __forceinline__ double2 prob2r(const NllArgs& A, const double2 (&x)[2], bool& okx,

@@ -144,6 +144,15 @@ template <class Ev>
 struct IsRatio<Ev, decltype((void)Ev::RATIO)> {
     static constexpr bool value = Ev::RATIO;
 };
+// p = q / r^POW for ratio evaluators
+template <class Ev, class = void>
+struct RatioPow {
+    static constexpr int value = 1;
+};
+template <class Ev>
+struct RatioPow<Ev, decltype((void)Ev::RATIO_POW)> {
+    static constexpr int value = Ev::RATIO_POW;
+};
 
 // One row of a unit: evaluate two events (local block indices e, e+1),
 // mask absent tail events (TAIL), certify, multiply into the unit.
@@ -175,7 +184,12 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
     }
     bool ok = okx && oky && p_in_range(q.x) && p_in_range(q.y);
     if constexpr (RATIO) {
-        ok = ok && p_in_range(r.x) && p_in_range(r.y);
+        // r^POW in [2^-500, 2^500] (p = q / r^POW then stays within 2^+-1000)
+        constexpr int span = 500 / RatioPow<Ev>::value;
+        auto r_ok = [](double v) {
+            return (unsigned)((__double2hiint(v) >> 20) - (1023 - span)) <= (unsigned)(2 * span);
+        };
+        ok = ok && r_ok(r.x) && r_ok(r.y);
         u.md = (u.md * r.x) * r.y;
         renorm(u.md, u.exd);
     } else {
@@ -189,8 +203,9 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
 template <class Ev>
 __device__ __forceinline__ double unit_value(const Unit& u) {
     if constexpr (IsRatio<Ev>::value) {
-        const double fe = (double)(u.ex - u.exd);
-        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) - log(u.md)));
+        constexpr double pw = (double)RatioPow<Ev>::value;
+        const double fe = (double)u.ex - pw * (double)u.exd;
+        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, fma(-pw, log(u.md), log(u.m))));
     } else {
         const double fe = (double)u.ex;
         return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) + u.ls));
