@@ -140,12 +140,15 @@ void* pfb_ctx_stream(pfb_ctx* ctx);
 int pfb_ctx_synchronize(pfb_ctx* ctx);
 /* Tuning: warps cooperating on one 4096-event block (0 = automatic; 1,2,4,8). */
 int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
-/* Kernel structure: 1 (default) bulk-copy pipelines where available (the
- * TMA producer/consumer kernel for HBM-bound evaluators, the product-mode
- * kernel for exponential- and Dalitz-bound ones, with per-warp bulk
- * prefetch for single-column models); 2 as 1 with per-warp bulk prefetch
- * for every product-mode evaluator; 0 the SIMT log-domain streaming kernel.
- * Results are identical within each mode's documented block structure. */
+/* Kernel structure (all modes give the NLL within rounding of the reference;
+ * within a mode totals are bitwise invariant under launch shape and ranges):
+ *  1 (default) TMA-fed kernels -- the unit-sum kernel for log-domain plans
+ *    (C2), the TMA product kernel for two-column product evaluators
+ *    (Dalitz), per-warp bulk prefetch for one-column ones (C1);
+ *  2 the reference-tree TMA kernel for log-domain plans, per-warp bulk
+ *    prefetch for every product evaluator;
+ *  3 the TMA product kernel for every product evaluator;
+ *  0 the SIMT log-domain streaming kernel (reference tree) everywhere. */
 int pfb_ctx_set_pipeline(pfb_ctx* ctx, int mode);
 /* Number of engine kernels launched on this context since creation. */
 int pfb_ctx_launch_count(pfb_ctx* ctx, int64_t* out);
