@@ -276,3 +276,40 @@ def test_backend_protocol_drop_in(pf, golden_dir):
         sums.extend(c.tolist())
     assert math.fsum(sums) == pf.nll(pdf, ds)
     assert rel(math.fsum(sums), g["nll"][0]) <= RTOL
+
+
+# --- certification failures: the exact fix-up path behind every fast kernel -------
+
+
+@pytest.mark.parametrize("alpha", [-40.0, 35.0])
+def test_c1_uncertified_blocks_take_the_exact_fixup(pf, alpha):
+    """|alpha x| >= 256 cannot be certified by the product-mode C1 evaluator:
+    those blocks go to the literal fix-up launch, and the NLL still matches."""
+    rng = np.random.default_rng(12)
+    n = 9 * 4096 + 99
+    xs = np.clip(np.concatenate([rng.normal(5.0, 0.5, n // 2), rng.uniform(0.0, 10.0, n - n // 2)]), 0, 10)
+    x = pf.Variable.observable("x", 0.0, 10.0)
+    pdf = pf.add_pdf([pf.gaussian(x, pf.Variable("mu", 5.0, 0.0, 10.0), pf.Variable("sigma", 0.5, 0.01, 5.0)),
+                      pf.exponential(x, pf.Variable("alpha", alpha, -50.0, 50.0))], [pf.Variable("f", 0.3, 0.0, 1.0)])
+    ds = models.dataset([x], [xs])
+    ctx = pf.device_context(0)
+    before = ctx.launch_count()
+    got = pf.nll(pdf, ds)
+    assert ctx.launch_count() - before == 2  # fast kernel + exact fix-up
+    want = O.nll(models.c1_spec((5.0, 0.5, alpha, 0.3)), {"x": xs})
+    assert rel(got, want) <= RTOL
+
+
+def test_c2_uncertified_blocks_take_the_exact_fixup(pf):
+    rng = np.random.default_rng(13)
+    n = 7 * 4096 + 5
+    xs = np.clip(rng.normal(5.0, 1.0, n), 0, 10)
+    xs[::3000] = 0.05  # u ~ -725 at sigma = 0.13: beyond the log-domain guard (subnormal in the reference)
+    ys = np.clip(rng.exponential(2.5, n), 0, 10)
+    (x, y), pdf, _ = models.c2((5.0, 0.13, -0.4))
+    ds = models.dataset([x, y], [xs, ys])
+    ctx = pf.device_context(0)
+    before = ctx.launch_count()
+    got = pf.nll(pdf, ds)
+    assert ctx.launch_count() - before == 2
+    assert rel(got, O.nll(models.c2_spec((5.0, 0.13, -0.4)), {"x": xs, "y": ys})) <= RTOL
