@@ -229,11 +229,14 @@ constexpr int kSumWarps = 8;  // warps per team (one unit-row each)
 #ifndef PFB_UNIT_TEAMS1
 #define PFB_UNIT_TEAMS1 3
 #endif
+#ifndef PFB_UNIT_TEAMS2
+#define PFB_UNIT_TEAMS2 2
+#endif
 // consumer teams: 2 for two-column stages (3 x 64 KB), 3 for one-column
 // stages (6 x 32 KB) when the evaluator fits 80 registers
 template <class Ev>
 struct UnitTeams {
-    static constexpr int value = Ev::NC == 1 ? PFB_UNIT_TEAMS1 : 2;
+    static constexpr int value = Ev::NC == 1 ? PFB_UNIT_TEAMS1 : PFB_UNIT_TEAMS2;
 };
 constexpr int kSumRing = 4;
 
