@@ -31,6 +31,8 @@
 #pragma once
 #include "pfb_nll_tma.cuh"
 
+
+
 namespace pfb {
 
 // ln 2 split so that ex * kLn2Hi is exact for |ex| < 2^21 (fdlibm split).
@@ -74,7 +76,7 @@ __device__ __forceinline__ double exp_tab(double x, const double* tab) {
     const double kd = t - 0x1.8p52;
     double r = fma(kd, -kExpK[1], x);
     r = fma(kd, -kExpK[2], r);
-    double q = fma(r, kExpK[3], kExpK[4]);
+    double q = fma(r, kExpK[3], kExpK[4]);  // Horner (Estrin measured slower: throughput-bound)
     q = fma(q, r, kExpK[5]);
     q = fma(q, r, kExpK[6]);
     q = fma(q, r, kExpK[7]);
