@@ -248,7 +248,13 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     constexpr int NC = Ev::NC;
     extern __shared__ __align__(128) double stage[];  // S x NC x 4096 doubles
 
-    __shared__ unsigned long long full_bar[S], empty_bar[S];
+    // full barriers per (team, stage): a team waits only on the phases of
+    // its own uses of a stage, one phase at a time.  (A single full barrier
+    // per stage would let a team waiting for its next use of the stage match
+    // the parity of the previous team's still-pending phase -- the mbarrier
+    // parity wait cannot tell phases two apart.)
+    constexpr int L = S % kSumTeams == 0 ? S : S * kSumTeams;  // lcm(S, teams) for S in {3, 6}
+    __shared__ unsigned long long full_bar[kSumTeams][S], empty_bar[S];
     __shared__ long long s_blk[S];
     __shared__ double xch[kSumTeams][kSumRing][kSumWarps][32];
     __shared__ int xbad[kSumTeams][kSumRing][kSumWarps];
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     if (tid < 16) s_tab[tid] = kExp2Tab[tid];
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full_bar[s], 1);
+            for (int t = 0; t < kSumTeams; ++t) mbar_init(&full_bar[t][s], 1);
             mbar_init(&empty_bar[s], kSumWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -288,12 +294,12 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                 if (it >= nitems) {
                     // one end marker per team
                     s_blk[s] = -1;
-                    mbar_arrive(&full_bar[s]);
+                    mbar_arrive(&full_bar[u % kSumTeams][s]);
                     for (int extra = 1; extra < kSumTeams; ++extra) {
                         const int v = u + extra, s2 = v % S;
                         mbar_wait(&empty_bar[s2], ((v / S) & 1) ^ 1);
                         s_blk[s2] = -1;
-                        mbar_arrive(&full_bar[s2]);
+                        mbar_arrive(&full_bar[v % kSumTeams][s2]);
                     }
                     break;
                 }
@@ -301,12 +307,13 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                 const int64_t bidx = is_tail ? A.nfull : it - (A.tail ? 1 : 0);
                 s_blk[s] = bidx;
                 const unsigned bytes = is_tail ? (unsigned)(8 * (A.tail & ~1)) : (unsigned)(8 * kBlock);
-                mbar_arrive_expect_tx(&full_bar[s], bytes * NC);
+                unsigned long long* fb = &full_bar[u % kSumTeams][s];
+                mbar_arrive_expect_tx(fb, bytes * NC);
                 if (bytes) {
 #pragma unroll
                     for (int c = 0; c < NC; ++c)
                         bulk_g2s(stage + ((int64_t)s * NC + c) * kBlock,
-                                 A.col[c] + A.begin + bidx * (int64_t)kBlock, bytes, &full_bar[s]);
+                                 A.col[c] + A.begin + bidx * (int64_t)kBlock, bytes, fb);
                 }
             }
         }
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
         int f = 0;
         for (int u = team;; u += kSumTeams) {
             const int s = u % S;
-            mbar_wait(&full_bar[s], (u / S) & 1);
+            mbar_wait(&full_bar[team][s], (u / L) & 1);  // this team's (u / L)-th use of stage s
             const int64_t bidx = s_blk[s];
             if (bidx < 0) break;
             const double* sx = stage + (int64_t)s * NC * kBlock;
