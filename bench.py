@@ -300,6 +300,15 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    # cross-check (untimed): the same NLL through the SIMT reference-tree kernel
+    # (pipeline 0) must agree with the fast kernel to rounding
+    _, fast_nll = step_local()
+    L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, 0), "pfb_ctx_set_pipeline")
+    _, simt_nll = step_local()
+    L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, 1), "pfb_ctx_set_pipeline")
+    crosscheck = abs(fast_nll - simt_nll) / abs(simt_nll)
+    if not crosscheck <= 1e-12:
+        raise SystemExit(f"NLL cross-check failed: fast kernel {fast_nll!r} vs SIMT kernel {simt_nll!r}")
 
     launches0 = ctx.launch_count()
     kernel_ms = []
@@ -406,6 +415,7 @@ def main():
                                   + (f" ({args.collective})" if world > 1 else "")},
         "nll_evals_per_s": args.steps / dev_s,
         "nll": nll_value,
+        "nll_crosscheck_rel": crosscheck,
         "wall_s": wall,
         "e2e": e2e,
         "gpu_launches": launches,
