@@ -109,3 +109,23 @@ def test_batched_points_at_scale_equal_single(pf):
                                 ctypes.byref(single), ctypes.byref(err)), "pfb_nll")
         assert out[k] == single.value, k
     L.lib().pfb_store_destroy(st)
+
+
+def test_dalitz_100m_product_kernel_matches_reference_tree_kernel(pf):
+    """C4 scale: the TMA product kernel (ratio evaluator) and the SIMT
+    reference-tree kernel agree to rounding on 100M Dalitz events."""
+    from paper_1710_08826_b200 import _lib as L
+    from paper_1710_08826_b200 import mcgen
+
+    terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
+    s12, s13 = mcgen.device_dalitz(100_000_000, terms, models.D_CHANNEL_T, 4)
+    (o12, o13), pdf, _ = models.c3()
+    ds = pf.UnbinnedDataSet.from_columns([o12, o13], [s12, s13], copy=False)
+    ctx = pf.device_context(0)
+    fast = pf.nll(pdf, ds)
+    L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, 0), "pfb_ctx_set_pipeline")
+    try:
+        ref = pf.nll(pdf, ds)
+    finally:
+        L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, 1), "pfb_ctx_set_pipeline")
+    assert abs(fast - ref) <= 1e-12 * abs(ref)
