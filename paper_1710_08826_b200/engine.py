@@ -86,7 +86,29 @@ def cached_norm(node, snap, store: NormalizationStore) -> NormalizationValue:
 
 
 def resolve_norms(root, snap, store: NormalizationStore) -> dict[int, float]:
-    return {node.id: cached_norm(node, snap, store).value for node in root.walk()}
+    """Every node's norm in post-order (reference engine.py:158-164).  Same
+    cache traffic and counters as calling cached_norm per node -- whose
+    recursion into children only ever hits the cache here, since children
+    precede their parent -- without that second pass."""
+    out: dict[int, float] = {}
+    for node in root.walk():
+        fp = node.fingerprint()
+        cached = store.get(node.id)
+        if cached is not None and cached[0] == fp:
+            out[node.id] = cached[1]
+            continue
+        hook = CACHED_NORM_HOOKS.get(node.kind)
+        if hook is not None:
+            value = float(hook(node, snap, store))
+        else:
+            value = normalize_value(node, snap, {c.id: out[c.id] for c in node.children})
+            if not node.children:
+                store.kernel_evals += 1
+        store.norm_computations += 1
+        store.recompute_counts[node.id] += 1
+        store.put(node.id, fp, value)
+        out[node.id] = NormalizationValue(value, fp).value  # positivity check as cached_norm
+    return out
 
 
 # --- device contexts ------------------------------------------------------------------
