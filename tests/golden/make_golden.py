@@ -446,8 +446,31 @@ def trees_fixture():
     np.savez_compressed(os.path.join(OUT, "trees.npz"), **out)
 
 
+def dalitz_variants_fixture():
+    """Other Dalitz structures (K = 2, 3, 5; a K pi pi channel with unequal
+    masses) -- NLLs at two coefficient points from the reference."""
+    import parafit
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from tests import models
+
+    out = {}
+    for k, name in enumerate(sorted(models.DALITZ_VARIANTS)):
+        (s12, s13), pdf, terms = models.dalitz_variant(parafit, name)
+        ds = generate_dalitz(terms, pdf.payload[1], GenSpec(n_events=2 * 4096 + 321 + k, seed=40 + k),
+                             observables=(s12, s13))
+        vals = [nll(pdf, ds, snapshot(pdf.param_closure()), Backend("serial"))]
+        terms[1].magnitude.value *= 1.1
+        terms[-1].phase.value += 0.2
+        vals.append(nll(pdf, ds, snapshot(pdf.param_closure()), Backend("serial")))
+        out[f"{name}__s12"] = ds.column("s12")
+        out[f"{name}__s13"] = ds.column("s13")
+        out[f"{name}__nll"] = np.array(vals)
+    np.savez_compressed(os.path.join(OUT, "dalitz_variants.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned", "toys", "trees"]
+    which = sys.argv[1:] or ["reduction", "c1", "c2", "c3", "shards", "errors", "fits", "binned", "toys", "trees", "dalitz_variants"]
     for name in which:
         globals()[f"{name}_fixture"]()
     for f in sorted(os.listdir(OUT)):

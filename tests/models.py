@@ -183,3 +183,40 @@ def tree_data(name, n, seed):
         lo, hi = TREE_OBS[c]
         cols[c] = rng.uniform(lo, hi, n)
     return cols
+
+
+# --- Dalitz variants (kernel dispatch coverage: K = 2, 3, 4 other structures, 5) ----
+
+DALITZ_VARIANTS = {
+    # name: (channel (M, m1, m2, m3), [(pair, m, width, spin, mag, phase)], grid)
+    "k2": ((1.86484, 0.13957, 0.13957, 0.13498),
+           [(13, 0.77511, 0.1491, 1, 1.0, 0.0), (12, 1.0, 20.0, 0, 15.0, -0.5)], (96, 96)),
+    "k3": ((1.86484, 0.13957, 0.13957, 0.13498),
+           [(13, 0.77511, 0.1491, 1, 1.0, 0.0), (23, 0.77511, 0.1491, 1, 0.73, -0.03),
+            (12, 0.77526, 0.1478, 1, 0.55, 0.28)], (96, 96)),
+    "k4_kpipi": ((1.86966, 0.493677, 0.13957, 0.13957),
+                 [(12, 0.89555, 0.0473, 1, 1.0, 0.0), (13, 0.89555, 0.0473, 1, 1.0, 0.3),
+                  (23, 0.98, 0.07, 0, 2.0, 1.2), (12, 1.425, 0.27, 0, 1.5, -0.7)], (96, 96)),
+    "k5": ((1.86484, 0.13957, 0.13957, 0.13498),
+           [(13, 0.77511, 0.1491, 1, 1.0, 0.0), (23, 0.77511, 0.1491, 1, 0.73, -0.03),
+            (12, 0.77526, 0.1478, 1, 0.55, 0.28), (12, 1.0, 20.0, 0, 20.0, -0.5),
+            (13, 1.465, 0.4, 1, 0.4, 2.0)], (96, 96)),
+}
+
+
+def dalitz_variant(mod, name):
+    """(observables, pdf, terms) of a variant with `mod`'s builders (the
+    reference package or this one)."""
+    ch_t, spec, grid = DALITZ_VARIANTS[name]
+    ch = mod.DecayChannel(*ch_t)
+    terms = []
+    for k, (pair, m, w, spin, mag, ph) in enumerate(spec):
+        terms.append(mod.ResonanceTerm(
+            pair=pair, mass=mod.Variable(f"{name}{k}_m", m, fixed=True),
+            width=mod.Variable(f"{name}{k}_w", w, fixed=True), spin=spin,
+            magnitude=mod.Variable(f"{name}{k}_mag", mag, 0.0, 100.0, fixed=(k == 0)),
+            phase=mod.Variable(f"{name}{k}_ph", ph, -2 * math.pi, 2 * math.pi, fixed=(k == 0))))
+    s12 = mod.Variable.observable("s12", *ch.s12_range)
+    s13 = mod.Variable.observable("s13", *ch.s13_range)
+    pdf = mod.dalitz_pdf(terms, ch, s12_obs=s12, s13_obs=s13, grid=grid)
+    return (s12, s13), pdf, terms
