@@ -33,6 +33,7 @@
 
 
 
+
 namespace pfb {
 
 // ln 2 split so that ex * kLn2Hi is exact for |ex| < 2^21 (fdlibm split).
@@ -321,6 +322,53 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
         const int team = warp / kSumWarps;
         const int w = warp % kSumWarps;
         int f = 0;
+        // post this warp's unit value for point m; the last of the team's
+        // eight to arrive folds the block (no barrier)
+        auto post_fold = [&](double acc, bool bad, int m, int64_t bidx) {
+            const unsigned anybad = __any_sync(0xffffffffu, bad);
+            const int slot = f % kSumRing;
+            if (lane == 0)
+                while (*reinterpret_cast<volatile int*>(&s_done[team][slot]) < f / kSumRing) __nanosleep(20);
+            __syncwarp();
+            xch[team][slot][w][lane] = acc;
+            unsigned arrived = 0;
+            if (lane == 0) {
+                xbad[team][slot][w] = anybad ? 1 : 0;
+                __threadfence_block();
+                arrived = atomicAdd(&s_cnt[team][slot], 1u);
+            }
+            arrived = __shfl_sync(0xffffffffu, arrived, 0);
+            if (arrived == kSumWarps - 1) {
+                __threadfence_block();
+                bool fbad = false;
+#pragma unroll
+                for (int q = 0; q < kSumWarps; ++q) fbad |= xbad[team][slot][q] != 0;
+                double bsum = 0.0;
+                if (!fbad) {
+                    double v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = xch[team][slot][q][lane];
+                    double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+#pragma unroll
+                    for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
+                    bsum = T;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    if (fbad) {
+                        const unsigned long long fs = atomicAdd(A.fix_counter, 1ull);
+                        A.fix_list[fs] = (A.block_base + bidx) * kMaxPts + m;
+                    } else {
+                        if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
+                        acc_add_shared(sacc[m], bsum);
+                    }
+                    s_cnt[team][slot] = 0u;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile int*>(&s_done[team][slot]) = f / kSumRing + 1;
+                }
+            }
+            ++f;
+        };
         for (int u = team;; u += kSumTeams) {
             const int s = u % S;
             mbar_wait(&full_bar[team][s], (u / L) & 1);  // this team's (u / L)-th use of stage s
@@ -378,49 +426,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[s]);
                 }
-                const unsigned anybad = __any_sync(0xffffffffu, bad);
-                const int slot = f % kSumRing;
-                if (lane == 0)
-                    while (*reinterpret_cast<volatile int*>(&s_done[team][slot]) < f / kSumRing) __nanosleep(20);
-                __syncwarp();
-                xch[team][slot][w][lane] = acc;
-                unsigned arrived = 0;
-                if (lane == 0) {
-                    xbad[team][slot][w] = anybad ? 1 : 0;
-                    __threadfence_block();
-                    arrived = atomicAdd(&s_cnt[team][slot], 1u);
-                }
-                arrived = __shfl_sync(0xffffffffu, arrived, 0);
-                if (arrived == kSumWarps - 1) {
-                    __threadfence_block();
-                    bool fbad = false;
-#pragma unroll
-                    for (int q = 0; q < kSumWarps; ++q) fbad |= xbad[team][slot][q] != 0;
-                    double bsum = 0.0;
-                    if (!fbad) {
-                        double v[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) v[q] = xch[team][slot][q][lane];
-                        double T = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-#pragma unroll
-                        for (int off = 16; off >= 1; off /= 2) T = T + __shfl_down_sync(0xffffffffu, T, off);
-                        bsum = T;
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (fbad) {
-                            const unsigned long long fs = atomicAdd(A.fix_counter, 1ull);
-                            A.fix_list[fs] = (A.block_base + bidx) * kMaxPts + m;
-                        } else {
-                            if (A.block_sums && m == 0) A.block_sums[A.block_base + bidx] = bsum;
-                            acc_add_shared(sacc[m], bsum);
-                        }
-                        s_cnt[team][slot] = 0u;
-                        __threadfence_block();
-                        *reinterpret_cast<volatile int*>(&s_done[team][slot]) = f / kSumRing + 1;
-                    }
-                }
-                ++f;
+                post_fold(acc, bad, m, bidx);
             }
         }
     }

@@ -60,3 +60,30 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def dalitz_fit(n=10_000_000):
+    import time
+
+    import paper_1710_08826_b200 as pf
+    from paper_1710_08826_b200 import mcgen
+    from paper_1710_08826_b200.fitting import FitManager
+    from tests import models
+
+    terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
+    s12, s13 = mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 3)
+    (o12, o13), pdf, rts = models.c3()
+    ds = pf.UnbinnedDataSet.from_columns([o12, o13], [s12, s13], copy=False)
+    pf.nll(pdf, ds)
+    for t in rts[1:]:
+        pf.set_value(t.magnitude, t.magnitude.value * 1.05)
+        pf.set_value(t.phase, t.phase.value + 0.05)
+    t0 = time.perf_counter()
+    r = FitManager(pdf, ds).fit()
+    dt = time.perf_counter() - t0
+    print(json.dumps({"probe": "FitManager C3 Dalitz (6 free)", "n": n, "calls": r.n_calls, "wall_s": dt,
+                      "calls_per_s": r.n_calls / dt, "status": r.status, "timing": r.timing}), flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("PFB_DALITZ_FIT"):
+    dalitz_fit()
