@@ -106,8 +106,12 @@ struct pfb_ctx {
     unsigned long long* work_counter = nullptr;
     unsigned long long* errkey = nullptr;
     double* tail_scratch = nullptr;
-    long long* res_dev = nullptr;   // kResWords
-    long long* res_host = nullptr;  // pinned mirror
+    // result words (error key, deferred count, exported accumulator): pinned
+    // host memory mapped into the device, so the finishing CTA writes the
+    // result straight to the host and a call needs no device-to-host copy
+    long long* res_dev = nullptr;   // kResWords, device view
+    long long* res_host = nullptr;  // kResWords, host view
+    bool res_mapped = false;
     unsigned long long* fix_counter = nullptr;
     int64_t* fix_list = nullptr;
     int64_t fix_cap = 0;
@@ -270,12 +274,19 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
     CK(cudaMalloc(&c->errkey, sizeof(unsigned long long)));
     CK(cudaMemset(c->errkey, 0xff, sizeof(unsigned long long)));
     CK(cudaMalloc(&c->tail_scratch, sizeof(double) * kBlock));
-    CK(cudaMalloc(&c->res_dev, sizeof(long long) * kResWords));
-    CK(cudaMemset(c->res_dev, 0, sizeof(long long) * kResWords));
     CK(cudaMalloc(&c->fix_counter, sizeof(unsigned long long)));
     CK(cudaMemset(c->fix_counter, 0, sizeof(unsigned long long)));
     CK(cudaMalloc(&c->probe_dev, sizeof(double) * 2));
+#ifndef PFB_RES_DEVICE
+    CK(cudaHostAlloc(&c->res_host, sizeof(long long) * kResWords, cudaHostAllocMapped));
+    memset(c->res_host, 0, sizeof(long long) * kResWords);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->res_dev), c->res_host, 0));
+    c->res_mapped = true;
+#else
+    CK(cudaMalloc(&c->res_dev, sizeof(long long) * kResWords));
+    CK(cudaMemset(c->res_dev, 0, sizeof(long long) * kResWords));
     CK(cudaMallocHost(&c->res_host, sizeof(long long) * kResWords));
+#endif
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     *out = c;
@@ -291,7 +302,7 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaFree(c->work_counter);
     cudaFree(c->errkey);
     cudaFree(c->tail_scratch);
-    cudaFree(c->res_dev);
+    if (!c->res_mapped) cudaFree(c->res_dev);
     cudaFree(c->fix_counter);
     cudaFree(c->fix_list);
     cudaFree(c->probe_dev);
@@ -1024,8 +1035,9 @@ static int decode_error(pfb_ctx* c, const pfb_plan* p, const NllArgs& A, unsigne
 }
 
 static int read_result(pfb_ctx* c, int npts = 1) {
-    CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * (kResHead + npts * PFB_ACC_WORDS),
-                       cudaMemcpyDeviceToHost, c->stream));
+    if (!c->res_mapped)
+        CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * (kResHead + npts * PFB_ACC_WORDS),
+                           cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     return PFB_OK;

@@ -286,12 +286,15 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
     if (warp == kSumWarps * kSumTeams) {
         if (lane == 0) {  // producer: as nll_tma_kernel's
-            int64_t it_next = (int64_t)atomicAdd(A.work_counter, 1ull);
+            // the first item is this CTA's own (no device-wide round trip
+            // before the first copy); the rest are claimed from the counter,
+            // one stage ahead
+            int64_t it_next = blockIdx.x;
             for (int u = 0;; ++u) {
                 const int s = u % S;
                 mbar_wait(&empty_bar[s], ((u / S) & 1) ^ 1);
                 const int64_t it = it_next;
-                if (it < nitems) it_next = (int64_t)atomicAdd(A.work_counter, 1ull);
+                if (it < nitems) it_next = (int64_t)gridDim.x + (int64_t)atomicAdd(A.work_counter, 1ull);
                 if (it >= nitems) {
                     // one end marker per team
                     s_blk[s] = -1;
