@@ -19,6 +19,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--profile", action="store_true", help="cProfile 20 C1 fits (host time by function)")
     args = ap.parse_args()
     import paper_1710_08826_b200 as pf
     from paper_1710_08826_b200 import mcgen
@@ -47,6 +48,18 @@ def main():
     dt = time.perf_counter() - t0
     print(json.dumps({"probe": "FitManager C1 (C5 unit)", "n": args.n, "calls": r.n_calls, "wall_s": dt,
                       "calls_per_s": r.n_calls / dt, "status": r.status, "values": list(r.values)}), flush=True)
+    if args.profile:
+        import cProfile
+        import pstats
+
+        prof = cProfile.Profile()
+        prof.enable()
+        for _ in range(20):
+            for v, val in zip(params, (4.95, 0.52, -0.29, 0.31)):
+                pf.set_value(v, val)
+            FitManager(pdf, ds).fit()
+        prof.disable()
+        pstats.Stats(prof).sort_stats("tottime").print_stats(25)
     (xx, yy), pdf2, p2 = models.c2((4.9, 1.1, -0.35))
     cx, cy = mcgen.device_prod_2d(args.n, 5.0, 1.0, -0.4, 0.0, 10.0, 2)
     ds2 = pf.UnbinnedDataSet.from_columns([xx, yy], [cx, cy], copy=False)
