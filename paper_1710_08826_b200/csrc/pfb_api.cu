@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include <fcntl.h>
@@ -93,6 +94,10 @@ static constexpr int kResHead = 2;  // [0] deferred-block count, [1] error key
 static constexpr int kResWords = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
 enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
+static constexpr int64_t kIoChunk = 4 << 20;  // doubles per staging buffer (32 MB)
+static constexpr int kDlLanes = 8;            // host threads of a large pageable download
+static constexpr int64_t kDlChunk = 1 << 20;  // doubles per lane staging buffer (8 MB)
+
 struct pfb_ctx {
     int device = 0;
     int sm_count = 148;
@@ -140,11 +145,15 @@ struct pfb_ctx {
     // file ingest staging (pfb_store_load_npy)
     double* io_pinned[2] = {nullptr, nullptr};
     cudaEvent_t io_event[2] = {nullptr, nullptr};
+    // parallel download lanes (pfb_store_download to pageable memory)
+    double* dl_pinned[kDlLanes][2] = {};
+    cudaStream_t dl_stream[kDlLanes] = {};
     // binned data scratch
     void* bin_dev = nullptr;  // bin counts / contents
     int64_t bin_cap = 0;      // bytes
     unsigned long long* bin_key = nullptr;
 };
+
 
 struct pfb_store {
     pfb_ctx* ctx = nullptr;
@@ -152,6 +161,7 @@ struct pfb_store {
     int64_t n = 0;
     double* cols[kStoreMaxCols] = {};
     bool owned = false;
+    bool pooled = false;  // columns from the device's stream-ordered pool
 };
 
 struct TermFactor {
@@ -262,6 +272,13 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
     auto* c = new pfb_ctx();
     c->device = device;
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    {
+        // keep freed pool memory for reuse by later stores (see pfb_store_create)
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+        uint64_t keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
@@ -317,6 +334,11 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     for (int b = 0; b < 2; ++b) {
         if (c->io_pinned[b]) cudaFreeHost(c->io_pinned[b]);
         if (c->io_event[b]) cudaEventDestroy(c->io_event[b]);
+    }
+    for (int t = 0; t < kDlLanes; ++t) {
+        for (int b = 0; b < 2; ++b)
+            if (c->dl_pinned[t][b]) cudaFreeHost(c->dl_pinned[t][b]);
+        if (c->dl_stream[t]) cudaStreamDestroy(c->dl_stream[t]);
     }
     for (auto& p : c->e2e_dev) cudaFree(p);
     for (auto& e : c->chunk_events) cudaEventDestroy(e);
@@ -385,15 +407,22 @@ int pfb_store_create(pfb_ctx* c, int32_t ncols, int64_t n, pfb_store** out) {
     s->n = n;
     s->owned = true;
     // pad each column to a whole number of 4096-event blocks (+2 for double2 reads)
+    // Columns come from the device's stream-ordered pool (kept, not returned
+    // to the driver, see pfb_ctx_create): a toy study that generates, fits and
+    // drops a dataset per toy reuses the same HBM instead of paying a fresh
+    // cudaMalloc (tens of ms for 100 MB-class buffers) every time.
     const int64_t padded = ((n + kBlock - 1) / kBlock) * kBlock + 2;
+    s->pooled = true;
     for (int i = 0; i < ncols; ++i) {
-        cudaError_t e = cudaMalloc(&s->cols[i], sizeof(double) * padded);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&s->cols[i]), sizeof(double) * padded, c->stream);
         if (e != cudaSuccess) {
-            for (int j = 0; j < i; ++j) cudaFree(s->cols[j]);
+            for (int j = 0; j < i; ++j) cudaFreeAsync(s->cols[j], c->stream);
             delete s;
             return cuda_fail(e);
         }
     }
+    // usable from any stream once this returns
+    CK(cudaStreamSynchronize(c->stream));
     *out = s;
     return PFB_OK;
 }
@@ -433,7 +462,12 @@ int pfb_store_destroy(pfb_store* s) {
     if (!s) return PFB_OK;
     if (s->owned) {
         cudaSetDevice(s->ctx->device);
-        for (int i = 0; i < s->ncols; ++i) cudaFree(s->cols[i]);
+        for (int i = 0; i < s->ncols; ++i) {
+            if (s->pooled)
+                cudaFreeAsync(s->cols[i], s->ctx->stream);  // after the work queued on the context
+            else
+                cudaFree(s->cols[i]);
+        }
     }
     delete s;
     return PFB_OK;
@@ -1729,10 +1763,56 @@ int pfb_gen_1d(pfb_ctx* c, int32_t kind, double mu, double sigma, double alpha, 
 int pfb_store_download(pfb_store* st, int32_t col, double* host, int64_t offset, int64_t count) {
     if (!st || !host || col < 0 || col >= st->ncols || offset < 0 || count < 0 || offset + count > st->n)
         return PFB_E_INVALID_ARGUMENT;
-    CK(cudaSetDevice(st->ctx->device));
-    CK(cudaMemcpyAsync(host, st->cols[col] + offset, sizeof(double) * count, cudaMemcpyDeviceToHost,
-                       st->ctx->stream));
-    CK(cudaStreamSynchronize(st->ctx->stream));
+    pfb_ctx* c = st->ctx;
+    CK(cudaSetDevice(c->device));
+    cudaPointerAttributes pa;
+    const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered;
+    cudaGetLastError();
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int lanes = (int)std::min<int64_t>({(int64_t)kDlLanes, (int64_t)(hw > 2 ? hw / 2 : 1),
+                                              (count + kDlChunk - 1) / kDlChunk});
+    if (pinned || lanes < 2) {
+        CK(cudaMemcpyAsync(host, st->cols[col] + offset, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return PFB_OK;
+    }
+    // Pageable destination (a fresh numpy array): one pageable cudaMemcpy is
+    // bound by a single staging copy and the page faults of the destination
+    // (~4 GB/s).  Here `lanes` host threads each stream a contiguous share
+    // through their own two pinned 8 MB buffers and stream, so the faults and
+    // copies out of staging run in parallel while the copy engine fills the
+    // other buffer.
+    CK(cudaStreamSynchronize(c->stream));  // the column is complete
+    for (int t = 0; t < lanes; ++t) {
+        for (int b = 0; b < 2; ++b)
+            if (!c->dl_pinned[t][b]) CK(cudaHostAlloc(&c->dl_pinned[t][b], sizeof(double) * kDlChunk, cudaHostAllocDefault));
+        if (!c->dl_stream[t]) CK(cudaStreamCreateWithFlags(&c->dl_stream[t], cudaStreamNonBlocking));
+    }
+    const double* src = st->cols[col] + offset;
+    std::vector<cudaError_t> errs(lanes, cudaSuccess);
+    std::vector<std::thread> pool;
+    const int64_t share = (count + lanes - 1) / lanes;
+    for (int t = 0; t < lanes; ++t) {
+        pool.emplace_back([&, t]() {
+            cudaError_t e = cudaSetDevice(c->device);
+            const int64_t b0 = std::min(count, t * share), b1 = std::min(count, b0 + share);
+            const int64_t np = (b1 - b0 + kDlChunk - 1) / kDlChunk;
+            cudaStream_t s = c->dl_stream[t];
+            auto piece = [&](int64_t k) { return std::min(kDlChunk, b1 - (b0 + k * kDlChunk)); };
+            if (e == cudaSuccess && np > 0)
+                e = cudaMemcpyAsync(c->dl_pinned[t][0], src + b0, sizeof(double) * piece(0), cudaMemcpyDeviceToHost, s);
+            for (int64_t k = 0; e == cudaSuccess && k < np; ++k) {
+                e = cudaStreamSynchronize(s);  // piece k is in buffer k & 1
+                if (e == cudaSuccess && k + 1 < np)  // the copy engine fills the other buffer meanwhile
+                    e = cudaMemcpyAsync(c->dl_pinned[t][(k + 1) & 1], src + b0 + (k + 1) * kDlChunk,
+                                        sizeof(double) * piece(k + 1), cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) memcpy(host + b0 + k * kDlChunk, c->dl_pinned[t][k & 1], sizeof(double) * piece(k));
+            }
+            errs[t] = e;
+        });
+    }
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < lanes; ++t) CK(errs[t]);
     return PFB_OK;
 }
 
@@ -2008,7 +2088,6 @@ int pfb_pcg_generate_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* 
 
 // ---- binary SoA ingest ---------------------------------------
 
-static constexpr int64_t kIoChunk = 4 << 20;  // doubles per staging buffer (32 MB)
 
 int pfb_npy_length(const char* path, int64_t* n_out) {
     if (!path || !n_out) return PFB_E_INVALID_ARGUMENT;

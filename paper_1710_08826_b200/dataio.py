@@ -93,7 +93,7 @@ def load_npy(observables: Sequence, paths, begin: int = 0, end: int | None = Non
         L.lib().pfb_store_destroy(st)
         raise
     cols = [np.load(p, mmap_mode="r")[begin:end] for p in files]
-    ctx._stores[tuple(id(a) for a in cols) + (0, n)] = (st, tuple(cols))
+    ctx.adopt(cols, st)
     ds._cols = cols
     return ds
 

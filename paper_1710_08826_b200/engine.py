@@ -142,11 +142,19 @@ class DeviceContext:
             a = np.ascontiguousarray(a, dtype=np.float64)
             if n:
                 L.check(L.lib().pfb_store_upload(st, c, L.dptr(a[begin:end]), 0, n), "pfb_store_upload")
-        if len(self._stores) >= 8:  # bounded cache: drop the oldest store
+        self.adopt(arrays, st, begin, end)
+        return st
+
+    MAX_STORES = 8
+
+    def adopt(self, arrays, st, begin: int = 0, end: int | None = None) -> None:
+        """Register `st` as the HBM copy of rows [begin, end) of `arrays`
+        (bounded cache: the oldest store is dropped first)."""
+        end = len(arrays[0]) if end is None else end
+        while len(self._stores) >= self.MAX_STORES:
             old_key = next(iter(self._stores))
             L.lib().pfb_store_destroy(self._stores.pop(old_key)[0])
-        self._stores[key] = (st, tuple(arrays))
-        return st
+        self._stores[tuple(id(a) for a in arrays) + (begin, end)] = (st, tuple(arrays))
 
     def plan_for(self, pdf, column_names) -> Plan:
         key = (id(pdf), tuple(column_names))

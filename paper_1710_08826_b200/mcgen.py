@@ -125,17 +125,30 @@ def _device_store(ctx, ncols: int, n: int):
     return st
 
 
-def _adopt(ctx, st, ncols: int, n: int):
+def _adopt(ctx, st, ncols: int, n: int, observables=None):
     """Download the generated columns and register the device store as the
-    HBM copy of those host arrays (no re-upload when the NLL runs)."""
+    HBM copy of those host arrays (no re-upload when the NLL runs).  With
+    `observables`, the dataset's strict range check (reference core.py:262-272)
+    runs on the device copy first."""
     from . import _lib as L
+    from .errors import OutOfRange
 
+    if observables is not None:
+        for c, obs in enumerate(observables):
+            bad = ctypes.c_int64()
+            val = ctypes.c_double()
+            code = L.lib().pfb_store_check_range(st, c, 0, n, float(obs.lower), float(obs.upper),
+                                                 ctypes.byref(bad), ctypes.byref(val))
+            if code or bad.value >= 0:
+                L.lib().pfb_store_destroy(st)
+                L.check(code, "pfb_store_check_range")
+                raise OutOfRange(c, float(val.value), obs.name)
     cols = []
     for c in range(ncols):
         a = np.empty(n, dtype=np.float64)
         L.check(L.lib().pfb_store_download(st, c, L.dptr(a), 0, n), "pfb_store_download")
         cols.append(a)
-    ctx._stores[tuple(id(a) for a in cols) + (0, n)] = (st, tuple(cols))
+    ctx.adopt(cols, st)
     return cols
 
 
@@ -328,8 +341,8 @@ def generate_1d(pdf, obs, spec: GenSpec, stats: dict | None = None, device: int 
                 L.lib().pfb_store_destroy(st)
                 raise EnvelopeExceeded(f"density {hit.observed} exceeded envelope {envelope} after a rescan") from None
             envelope = spec.envelope_safety * max(scan(RESCAN_POINTS), hit.observed)
-    col = _adopt(ctx, st, 1, spec.n_events)[0]
-    return UnbinnedDataSet.from_columns([obs], [col], copy=False)
+    col = _adopt(ctx, st, 1, spec.n_events, [obs])[0]
+    return UnbinnedDataSet._from_checked([obs], [col])
 
 
 def generate_dalitz(terms, ch, spec: GenSpec, observables=None, stats: dict | None = None, device: int = 0):
@@ -380,5 +393,5 @@ def generate_dalitz(terms, ch, spec: GenSpec, observables=None, stats: dict | No
                 raise EnvelopeExceeded(
                     f"intensity {hit.observed} exceeded envelope {envelope} after a rescan") from None
             envelope = spec.envelope_safety * max(scan(2048), hit.observed)
-    s12, s13 = _adopt(ctx, st, 2, spec.n_events)
-    return UnbinnedDataSet.from_columns(list(observables), [s12, s13], copy=False)
+    s12, s13 = _adopt(ctx, st, 2, spec.n_events, list(observables))
+    return UnbinnedDataSet._from_checked(list(observables), [s12, s13])
