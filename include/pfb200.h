@@ -143,7 +143,8 @@ int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
 /* Kernel structure (all modes give the NLL within rounding of the reference;
  * within a mode totals are bitwise invariant under launch shape and ranges):
  *  1 (default) TMA-fed kernels -- the unit-sum kernel for log-domain plans
- *    (C2), the TMA product kernel for two-column product evaluators
+ *    (C2; the register-window SIMT form of the same blocks up to 8 blocks
+ *    per SM), the TMA product kernel for two-column product evaluators
  *    (Dalitz), per-warp bulk prefetch for one-column ones (C1);
  *  2 the reference-tree TMA kernel for log-domain plans, per-warp bulk
  *    prefetch for every product evaluator;

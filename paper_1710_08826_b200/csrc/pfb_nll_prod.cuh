@@ -460,13 +460,25 @@ static cudaError_t launch_tma_sum(const NllArgs& A, cudaStream_t stream, int sm_
     return launch_tma_unit<Ev, false>(A, stream, sm_count);
 }
 
-template <int P, class Ev>
-__global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __grid_constant__ NllArgs A) {
+#ifndef PFB_SUM_W
+#define PFB_SUM_W 4
+#endif
+#ifndef PFB_SUM_SIMT
+#define PFB_SUM_SIMT 0
+#endif
+#ifndef PFB_SUM_MINB
+#define PFB_SUM_MINB 2
+#endif
+// PROD = false: the same kernel for log-domain evaluators (unit value = the
+// row-ordered sum of the unit's 16 terms, exactly as nll_tma_unit_kernel's
+// sum mode), one parameter point.
+template <int P, class Ev, bool PROD = true>
+__global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_prod_kernel(const __grid_constant__ NllArgs A) {
     static_assert(P == 1 || P == 2 || P == 4 || P == 8, "P");
     constexpr int NC = Ev::NC;
     constexpr int GROUPS = kThreads / (32 * P);
     constexpr int ROWS = 64 / P;  // rows per warp
-    constexpr int W = Ev::U;      // row loads kept in flight
+    constexpr int W = PROD ? Ev::U : PFB_SUM_W;  // row loads kept in flight
     static_assert(W <= ROWS && 8 % W == 0, "window");
 
     __shared__ double xch[2][GROUPS][8][32];  // unit values, double-buffered by item parity
@@ -541,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
 #pragma unroll 1
             for (int ju = 0; ju < ROWS / 8; ++ju) {
                 Unit un;
+                double acc = 0.0;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int i = 8 * ju + r;
@@ -551,13 +564,20 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                         load_full(cur_item, r0 + i + W, win[r % W]);
                     else if (has_next)
                         load_full(next_item, r0 + i + W - ROWS, win[r % W]);
-                    prod_row<Ev, false>(A, cur, 0, kBlock, un, bad, s_tab);
+                    if constexpr (PROD) {
+                        prod_row<Ev, false>(A, cur, 0, kBlock, un, bad, s_tab);
+                    } else {
+                        const double2 t = Ev::eval2(A, cur, 0, sacc, 2, bad, 0);
+                        acc = (acc + t.x) + t.y;
+                    }
                 }
-                xch[par][grp][(r0 >> 3) + ju][lane] = unit_value<Ev>(un);
+                if constexpr (PROD) acc = unit_value<Ev>(un);
+                xch[par][grp][(r0 >> 3) + ju][lane] = acc;
             }
         } else {
             // the ragged tail block (once per launch): same structure, rolled
             Unit un;
+            double acc = 0.0;
 #pragma unroll 1
             for (int i = 0; i < ROWS; ++i) {
                 double2 cur[NC];
@@ -571,10 +591,20 @@ __global__ void __launch_bounds__(kThreads, Ev::MINB) nll_prod_kernel(const __gr
                     load(cur_item, r0 + i + W, win[W - 1]);
                 else if (has_next)
                     load_full(next_item, r0 + i + W - ROWS, win[W - 1]);
-                prod_row<Ev, true>(A, cur, (r0 + i) * 64 + 2 * lane, cur_item.n, un, bad, s_tab);
+                const int e = (r0 + i) * 64 + 2 * lane;
+                if constexpr (PROD) {
+                    prod_row<Ev, true>(A, cur, e, cur_item.n, un, bad, s_tab);
+                } else if (e < cur_item.n) {  // absent events add nothing
+                    const int nv = e + 1 < cur_item.n ? 2 : 1;
+                    const double2 t = Ev::eval2(A, cur, 0, sacc, nv, bad, 0);
+                    acc = acc + t.x;
+                    if (nv == 2) acc = acc + t.y;
+                }
                 if ((i & 7) == 7) {
-                    xch[par][grp][(r0 + i) >> 3][lane] = unit_value<Ev>(un);
+                    if constexpr (PROD) acc = unit_value<Ev>(un);
+                    xch[par][grp][(r0 + i) >> 3][lane] = acc;
                     un = Unit();
+                    acc = 0.0;
                 }
             }
         }
@@ -805,11 +835,11 @@ static cudaError_t launch_prod_bulk(const NllArgs& A, cudaStream_t stream, int s
     return cudaGetLastError();
 }
 
-template <int P, class Ev>
+template <int P, class Ev, bool PROD = true>
 static cudaError_t launch_prod_one(const NllArgs& A, cudaStream_t stream, int sm_count) {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nll_prod_kernel<P, Ev>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nll_prod_kernel<P, Ev, PROD>, kThreads, 0);
         if (occ < 1) occ = 1;
     }
     constexpr int GROUPS = kThreads / (32 * P);
@@ -818,7 +848,7 @@ static cudaError_t launch_prod_one(const NllArgs& A, cudaStream_t stream, int sm
     const int64_t cap = (int64_t)sm_count * occ;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    nll_prod_kernel<P, Ev><<<(unsigned)grid, kThreads, 0, stream>>>(A);
+    nll_prod_kernel<P, Ev, PROD><<<(unsigned)grid, kThreads, 0, stream>>>(A);
     return cudaGetLastError();
 }
 
@@ -843,6 +873,18 @@ static cudaError_t launch_prod(const NllArgs& A, cudaStream_t stream, int sm_cou
         default:
             return launch_prod_one<8, Ev>(A, stream, sm_count);
     }
+}
+
+// Log-domain unit sums (C2): the register-window SIMT kernel up to ~8 blocks
+// per SM (no producer / mbarrier start-up: 1-2 us faster at 0.5-4M events,
+// measured), the TMA unit kernel above (2-6% faster at 10-100M) -- the same
+// canonical blocks, bitwise the same NLL.
+template <class Ev>
+static cudaError_t launch_unit_sum(const NllArgs& A, cudaStream_t stream, int sm_count) {
+    const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+    if (A.npts == 1 && (PFB_SUM_SIMT || nitems <= 8 * (int64_t)sm_count))
+        return launch_prod_one<8, Ev, false>(A, stream, sm_count);
+    return launch_tma_unit<Ev, false>(A, stream, sm_count);
 }
 
 }  // namespace pfb

@@ -39,7 +39,7 @@ static bool sum2ge_ok(const NllArgs& A) {
 // 0: the SIMT streaming kernel
 template <class Ev>
 static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_count) {
-    if (A.tma == 1) return launch_tma_sum<Ev>(A, stream, sm_count);
+    if (A.tma == 1) return launch_unit_sum<Ev>(A, stream, sm_count);
     if (A.tma) return launch_tma<Ev>(A, stream, sm_count);
     return launch_p<Ev>(A, stream, sm_count);
 }
