@@ -73,3 +73,9 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
 }
 
 }  // namespace pfb
+
+#ifdef PFB_TRACE
+extern "C" int pfb_debug_trace(unsigned long long* out, int nblocks) {
+    return (int)pfb::read_trace(out, nblocks);
+}
+#endif
