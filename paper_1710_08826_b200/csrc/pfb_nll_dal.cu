@@ -47,3 +47,9 @@ cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
 }
 
 }  // namespace pfb
+
+#ifdef PFB_TRACE
+extern "C" int pfb_debug_trace_dal(unsigned long long* out, int nblocks) {
+    return (int)pfb::read_trace(out, nblocks);
+}
+#endif

@@ -17,28 +17,39 @@ import paper_1710_08826_b200 as pf
 from paper_1710_08826_b200 import _lib as L, mcgen
 from tests import models
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
+cfg = sys.argv[2] if len(sys.argv) > 2 else "c2"
 ctx = pf.device_context(0)
 ctx.enable_timing(True)
-cx, cy = mcgen.device_prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, 2)
-(x, y), pdf, _ = models.c2()
-plan = ctx.plan_for(pdf, ("x", "y")); st = ctx.store_for([cx, cy])
+if cfg == "c3":
+    terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
+    cx, cy = mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 3)
+    (x, y), pdf, _ = models.c3()
+    names = ("s12", "s13")
+else:
+    cx, cy = mcgen.device_prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, 2)
+    (x, y), pdf, _ = models.c2()
+    names = ("x", "y")
+pf.nll(pdf, pf.UnbinnedDataSet.from_columns([x, y], [cx, cy], copy=False))  # grid / norms for Dalitz
+plan = ctx.plan_for(pdf, names); st = ctx.store_for([cx, cy])
 snap = pf.snapshot(pdf.param_closure()); norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
 vals, nv = plan.pack(snap, norms)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 out = ctypes.c_double(); err = L.PfbErr()
-lib = L.lib(); lib.pfb_debug_trace.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+lib = L.lib()
+read = lib.pfb_debug_trace_dal if cfg == "c3" else lib.pfb_debug_trace
+read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 for rep in range(6):
     ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * 4)
     L.check(lib.pfb_nll(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err)), "nll")
     ms = ctx.last_kernel_ms()
     tr = (ctypes.c_ulonglong * (1024 * 8))()
-    lib.pfb_debug_trace(tr, 148)
+    read(tr, 148)
     a = np.frombuffer(tr, dtype=np.uint64).reshape(1024, 8)[:148].astype(np.int64)
     t0 = a[:, 0].min()
     rel = (a - t0) / 1000.0
     rel[a == 0] = np.nan
     last = np.nanargmax(rel[:, 7]) if np.isfinite(rel[:, 7]).any() else -1
-    print(json.dumps({"n": n, "event_us": 1e3 * ms,
+    print(json.dumps({"cfg": cfg, "n": n, "event_us": 1e3 * ms,
         "entry_spread_us": float(np.nanmax(rel[:, 0])),
         "first_issue_us_med": float(np.nanmedian(rel[:, 1] - rel[:, 0])),
         "first_ready_us_med": float(np.nanmedian(rel[:, 2] - rel[:, 0])), "first_ready_us_max": float(np.nanmax(rel[:, 2])),
