@@ -42,6 +42,16 @@ static constexpr double kLn2Lo = 1.90821492927058770002e-10;
 
 // q in [2^-500, 2^500]: biased exponent in [523, 1523]; 0, subnormal, negative,
 // inf and NaN all fail.
+#ifndef PFB_UNIT_MINMAX
+#define PFB_UNIT_MINMAX 1
+#endif
+// Certified factor range with unit-level checks: every q (and r) within
+// 2^+-kSpanM, so the unit running products stay normal with a renormalisation
+// every second row (four factors of at most 2^+-250 each on a mantissa in
+// [1, 2)); the density p = q / r^POW of every event then lies within
+// 2^+-(250 * (1 + POW)) -- a normal double, as in the reference.
+constexpr int kSpanM = 250;
+
 __device__ __forceinline__ bool p_in_range(double p) {
     const int hi = __double2hiint(p);
     return (unsigned)((hi >> 20) - 523) <= 1000u;
@@ -137,6 +147,13 @@ struct EvSum2GE {
 struct Unit {
     double m = 1.0, md = 1.0, ls = 0.0;
     int ex = 0, exd = 0;
+#if PFB_UNIT_MINMAX
+    // min / max of the high words of every q and r folded in: for positive
+    // doubles the high word orders like the value, and zero, negatives, inf
+    // and NaN all fall outside any finite positive range -- one unit-level
+    // range check instead of one per event
+    int qlo = 0x7fffffff, qhi = 0, rlo = 0x7fffffff, rhi = 0;
+#endif
 };
 
 template <class Ev, class = void>
@@ -161,7 +178,7 @@ struct RatioPow<Ev, decltype((void)Ev::RATIO_POW)> {
 // mask absent tail events (TAIL), certify, multiply into the unit.
 template <class Ev, bool TAIL>
 __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev::NC], int e, int n, Unit& u,
-                                         bool& bad, const double* tab) {
+                                         bool& bad, const double* tab, bool renorm_now = true) {
     constexpr bool RATIO = IsRatio<Ev>::value;
     bool okx, oky;
     double2 l = make_double2(0.0, 0.0);
@@ -185,6 +202,25 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
             oky = true;
         }
     }
+#if PFB_UNIT_MINMAX
+    bad |= !(okx && oky);
+    {
+        const int a = __double2hiint(q.x), b = __double2hiint(q.y);
+        u.qlo = min(u.qlo, min(a, b));
+        u.qhi = max(u.qhi, max(a, b));
+    }
+    if constexpr (RATIO) {
+        const int a = __double2hiint(r.x), b = __double2hiint(r.y);
+        u.rlo = min(u.rlo, min(a, b));
+        u.rhi = max(u.rhi, max(a, b));
+        u.md = (u.md * r.x) * r.y;
+        if (renorm_now) renorm(u.md, u.exd);
+    } else {
+        u.ls = (u.ls + l.x) + l.y;
+    }
+    u.m = (u.m * q.x) * q.y;
+    if (renorm_now) renorm(u.m, u.ex);
+#else
     bool ok = okx && oky && p_in_range(q.x) && p_in_range(q.y);
     if constexpr (RATIO) {
         // r^POW in [2^-500, 2^500] (p = q / r^POW then stays within 2^+-1000)
@@ -201,6 +237,22 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
     bad |= !ok;
     u.m = (u.m * q.x) * q.y;
     renorm(u.m, u.ex);
+    (void)renorm_now;
+#endif
+}
+
+// The unit-level range check (PFB_UNIT_MINMAX): every factor within 2^+-kSpanM.
+__device__ __forceinline__ bool unit_in_range(const Unit& u, bool ratio) {
+#if PFB_UNIT_MINMAX
+    constexpr int lo = (1023 - kSpanM) << 20, hi = (1023 + kSpanM + 1) << 20;
+    bool ok = u.qlo >= lo && u.qhi < hi;
+    if (ratio) ok = ok && u.rlo >= lo && u.rhi < hi;
+    return ok;
+#else
+    (void)u;
+    (void)ratio;
+    return true;
+#endif
 }
 
 template <class Ev>
@@ -248,7 +300,7 @@ constexpr int kSumRing = 4;
 // at [0] entry, [1] first copy issued, [2] first stage ready (team 0),
 // [3] team 0 done, [4] team 1 done, [5] finish entry, [6] ticket taken,
 // [7] export done (last CTA only).
-__device__ unsigned long long g_trace[1024][8];
+__device__ unsigned long long g_trace[1024][12];  // [8..9] ns waited for data per team, [10..11] blocks per team
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -285,6 +337,9 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     const int lane = tid & 31;
     const int warp = tid >> 5;
     if (tid == 0) PFB_T(0);
+#ifdef PFB_TRACE
+    if (tid < 4) g_trace[blockIdx.x][8 + tid] = 0;
+#endif
     // Start-up: the producer warp initialises the mbarriers and starts copying
     // at once; it only *arrives* on named barrier 1, which the consumers
     // sync on after zeroing their state -- so the first copy is not queued
@@ -400,9 +455,16 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
         };
         for (int u = team;; u += kSumTeams) {
             const int s = u % S;
+#ifdef PFB_TRACE
+            const unsigned long long tw0 = gtimer();
+#endif
             mbar_wait(&full_bar[team][s], (u / L) & 1);  // this team's (u / L)-th use of stage s
             const int64_t bidx = s_blk[s];
 #ifdef PFB_TRACE
+            if (w == 0 && lane == 0 && team < 2 && u >= kSumTeams && bidx >= 0) {
+                g_trace[blockIdx.x][8 + team] += gtimer() - tw0;
+                g_trace[blockIdx.x][10 + team] += 1;
+            }
             if (u == 0 && w == 0 && lane == 0) PFB_T(2);
             if (bidx < 0 && w == 0 && lane == 0 && team < 2) PFB_T(3 + team);
 #endif
@@ -422,7 +484,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
 #pragma unroll
                         for (int c = 0; c < NC; ++c) x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
                         if constexpr (PROD) {
-                            prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab);
+                            prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab, (r & 1) != 0);
                         } else {
                             const double2 t = Ev::eval2(A, x, 0, sacc[0], 2, bad, m);
                             acc = (acc + t.x) + t.y;
@@ -454,7 +516,10 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                         }
                     }
                 }
-                if constexpr (PROD) acc = unit_value<Ev>(un);
+                if constexpr (PROD) {
+                    bad |= !unit_in_range(un, IsRatio<Ev>::value);
+                    acc = unit_value<Ev>(un);
+                }
                 if (m == A.npts - 1) {  // the stage is no longer read by this warp
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -602,13 +667,16 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
                     else if (has_next)
                         load_full(next_item, r0 + i + W - ROWS, win[r % W]);
                     if constexpr (PROD) {
-                        prod_row<Ev, false>(A, cur, 0, kBlock, un, bad, s_tab);
+                        prod_row<Ev, false>(A, cur, 0, kBlock, un, bad, s_tab, (r & 1) != 0);
                     } else {
                         const double2 t = Ev::eval2(A, cur, 0, sacc, 2, bad, 0);
                         acc = (acc + t.x) + t.y;
                     }
                 }
-                if constexpr (PROD) acc = unit_value<Ev>(un);
+                if constexpr (PROD) {
+                    bad |= !unit_in_range(un, IsRatio<Ev>::value);
+                    acc = unit_value<Ev>(un);
+                }
                 xch[par][grp][(r0 >> 3) + ju][lane] = acc;
             }
         } else {
@@ -638,7 +706,10 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
                     if (nv == 2) acc = acc + t.y;
                 }
                 if ((i & 7) == 7) {
-                    if constexpr (PROD) acc = unit_value<Ev>(un);
+                    if constexpr (PROD) {
+                    bad |= !unit_in_range(un, IsRatio<Ev>::value);
+                    acc = unit_value<Ev>(un);
+                }
                     xch[par][grp][(r0 + i) >> 3][lane] = acc;
                     un = Unit();
                     acc = 0.0;
@@ -782,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
                     x[c] = *reinterpret_cast<const double2*>(xb + c * kUnitEvents + r * 64 + 2 * lane);
-                prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab);
+                prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab, (r & 1) != 0);
             }
         } else {
             const int n = A.tail;
@@ -804,6 +875,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
                 prod_row<Ev, true>(A, x, e, n, un, bad, s_tab);
             }
         }
+        bad |= !unit_in_range(un, IsRatio<Ev>::value);
         // No barrier: every warp posts its unit value into ring slot j % R and
         // the last of the 8 to arrive folds the block (warps never wait for
         // each other; a warp R items ahead waits for the slot to be folded).
@@ -926,7 +998,7 @@ static cudaError_t launch_unit_sum(const NllArgs& A, cudaStream_t stream, int sm
 
 #ifdef PFB_TRACE
 inline cudaError_t read_trace(unsigned long long* host, int nblocks) {
-    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 8 * nblocks);
+    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 12 * nblocks);
 }
 #endif
 

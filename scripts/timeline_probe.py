@@ -42,9 +42,10 @@ for rep in range(6):
     ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * 4)
     L.check(lib.pfb_nll(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err)), "nll")
     ms = ctx.last_kernel_ms()
-    tr = (ctypes.c_ulonglong * (1024 * 8))()
+    tr = (ctypes.c_ulonglong * (1024 * 12))()
     read(tr, 148)
-    a = np.frombuffer(tr, dtype=np.uint64).reshape(1024, 8)[:148].astype(np.int64)
+    full = np.frombuffer(tr, dtype=np.uint64).reshape(1024, 12)[:148].astype(np.int64)
+    a = full[:, :8]
     t0 = a[:, 0].min()
     rel = (a - t0) / 1000.0
     rel[a == 0] = np.nan
@@ -56,4 +57,6 @@ for rep in range(6):
         "team_done_min": float(np.nanmin(np.fmax(rel[:, 3], rel[:, 4]))), "team_done_med": float(np.nanmedian(np.fmax(rel[:, 3], rel[:, 4]))), "team_done_max": float(np.nanmax(np.fmax(rel[:, 3], rel[:, 4]))),
         "team_gap_med": float(np.nanmedian(np.abs(rel[:, 3] - rel[:, 4]))),
         "finish_entry_max": float(np.nanmax(rel[:, 5])), "ticket_max_nonlast": float(np.nanmax(rel[:, 6])),
-        "export_done": float(rel[last, 7]) if last >= 0 else None}), flush=True)
+        "export_done": float(rel[last, 7]) if last >= 0 else None,
+        "steady_wait_us_per_team_med": float(np.median(full[:, 8:10]) / 1000.0),
+        "blocks_per_team_med": float(np.median(full[:, 10:12]))}), flush=True)
