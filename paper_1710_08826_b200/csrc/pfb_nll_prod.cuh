@@ -294,6 +294,22 @@ struct UnitTeams {
     static constexpr int value = Ev::NC == 1 ? PFB_UNIT_TEAMS1 : PFB_UNIT_TEAMS2;
 };
 constexpr int kSumRing = 4;
+#ifndef PFB_PRODUCER_SLEEP
+#define PFB_PRODUCER_SLEEP 1
+#endif
+#ifndef PFB_CONSUMER_SLEEP
+#define PFB_CONSUMER_SLEEP 0
+#endif
+#if PFB_CONSUMER_SLEEP
+#define PFB_CONSUMER_WAIT mbar_wait_sleep
+#else
+#define PFB_CONSUMER_WAIT mbar_wait
+#endif
+#if PFB_PRODUCER_SLEEP
+#define PFB_PRODUCER_WAIT mbar_wait_sleep
+#else
+#define PFB_PRODUCER_WAIT mbar_wait
+#endif
 
 #ifdef PFB_TRACE
 // Per-CTA timeline of the TMA unit kernel (debug builds only): %globaltimer ns
@@ -365,7 +381,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
             int64_t it_next = blockIdx.x;
             for (int u = 0;; ++u) {
                 const int s = u % S;
-                mbar_wait(&empty_bar[s], ((u / S) & 1) ^ 1);
+                PFB_PRODUCER_WAIT(&empty_bar[s], ((u / S) & 1) ^ 1);
                 const int64_t it = it_next;
                 if (it < nitems) it_next = (int64_t)gridDim.x + (int64_t)atomicAdd(A.work_counter, 1ull);
                 if (it >= nitems) {
@@ -374,7 +390,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                     mbar_arrive(&full_bar[u % kSumTeams][s]);
                     for (int extra = 1; extra < kSumTeams; ++extra) {
                         const int v = u + extra, s2 = v % S;
-                        mbar_wait(&empty_bar[s2], ((v / S) & 1) ^ 1);
+                        PFB_PRODUCER_WAIT(&empty_bar[s2], ((v / S) & 1) ^ 1);
                         s_blk[s2] = -1;
                         mbar_arrive(&full_bar[v % kSumTeams][s2]);
                     }
@@ -458,7 +474,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
 #ifdef PFB_TRACE
             const unsigned long long tw0 = gtimer();
 #endif
-            mbar_wait(&full_bar[team][s], (u / L) & 1);  // this team's (u / L)-th use of stage s
+            PFB_CONSUMER_WAIT(&full_bar[team][s], (u / L) & 1);  // this team's (u / L)-th use of stage s
             const int64_t bidx = s_blk[s];
 #ifdef PFB_TRACE
             if (w == 0 && lane == 0 && team < 2 && u >= kSumTeams && bidx >= 0) {

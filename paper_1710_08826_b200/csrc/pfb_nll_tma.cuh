@@ -45,6 +45,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
                  : "memory");
 }
 
+#ifndef PFB_WAIT_HINT_NS
+#define PFB_WAIT_HINT_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
         "{\n"
@@ -54,6 +57,23 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         " @!p bra PFB_WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+
+// The same wait with a suspend-time hint: the waiting thread is parked until
+// the phase completes (or the hint elapses) instead of re-issuing try_wait in
+// a tight loop -- for waits that are long and not latency-critical (the
+// producer waiting for a free stage while consumers compute) the spin would
+// otherwise take issue slots from the consumer warps on its scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "PFB_WAITS_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra PFB_WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(PFB_WAIT_HINT_NS)
         : "memory");
 }
 
