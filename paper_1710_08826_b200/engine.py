@@ -168,6 +168,11 @@ class DeviceContext:
     def set_warps_per_block(self, warps: int) -> None:
         L.check(L.lib().pfb_ctx_set_warps_per_block(self.handle, int(warps)), "pfb_ctx_set_warps_per_block")
 
+    def set_pipeline(self, mode: int) -> None:
+        """Kernel structure (include/pfb200.h pfb_ctx_set_pipeline): 1 default,
+        2 / 3 alternative TMA layouts, 0 the SIMT reference-tree kernels."""
+        L.check(L.lib().pfb_ctx_set_pipeline(self.handle, int(mode)), "pfb_ctx_set_pipeline")
+
     def launch_count(self) -> int:
         out = ctypes.c_int64()
         L.check(L.lib().pfb_ctx_launch_count(self.handle, ctypes.byref(out)), "pfb_ctx_launch_count")
