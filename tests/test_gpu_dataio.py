@@ -71,3 +71,36 @@ def test_range_check_matches_reference_error(pf, tmp_path):
     except E.OutOfRange as exc:
         want = exc
     assert want is not None and (ei.value.index, ei.value.value, ei.value.name) == (want.index, want.value, want.name)
+
+
+def test_store_round_trip_pageable_and_pinned(pf):
+    """pfb_store_upload / pfb_store_download move columns bit for bit: the
+    multi-lane pinned-staged download into pageable memory (sizes that split
+    unevenly over the lanes and staging chunks) and the direct copy into
+    pinned memory."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1710_08826_b200 import _lib as L
+
+    ctx = pf.device_context(0)
+    rng = np.random.default_rng(7)
+    for n in (3, 1_048_577, 5_000_003):
+        src = rng.normal(size=n)
+        st = ctypes.c_void_p()
+        L.check(L.lib().pfb_store_create(ctx.handle, 1, n, ctypes.byref(st)), "pfb_store_create")
+        try:
+            L.check(L.lib().pfb_store_upload(st, 0, L.dptr(src), 0, n), "pfb_store_upload")
+            out = np.empty(n)
+            L.check(L.lib().pfb_store_download(st, 0, L.dptr(out), 0, n), "pfb_store_download")
+            assert out.tobytes() == src.tobytes()
+            pinned = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+            L.check(L.lib().pfb_store_download(st, 0, L.dptr(pinned), 0, n), "pfb_store_download")
+            assert pinned.tobytes() == src.tobytes()
+            part = np.empty(n - 1)
+            L.check(L.lib().pfb_store_download(st, 0, L.dptr(part), 1, n - 1), "pfb_store_download")
+            assert part.tobytes() == src[1:].tobytes()
+        finally:
+            L.lib().pfb_store_destroy(st)
