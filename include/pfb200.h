@@ -315,6 +315,19 @@ int pfb_peer_open(pfb_ctx* ctx, const uint8_t* handles);
 int pfb_peer_attach(pfb_ctx* ctx, const void* const* mailboxes);
 int pfb_peer_mailbox(pfb_ctx* ctx, void** out);
 int pfb_peer_allreduce(pfb_ctx* ctx, int64_t* dev_acc, double timeout_s);
+/* One NLL call over this rank's shard [begin, end) with the exchange fused
+ * into the kernel: the CTA that finishes the launch trades the 72-limb
+ * accumulator with every rank's mailbox over NVLink peer memory and exports
+ * the global sum -- one launch per call, no separate collective (replaces
+ * pfb_nll_partial_async + pfb_peer_allreduce / NCCL + pfb_finalize on the
+ * common path).  Collective: every rank calls it with the same parameters.
+ * *out_slow = 1 (and PFB_OK) when some rank deferred blocks to the exact
+ * fix-up or hit an error: every rank then sees 1 and must redo the call on
+ * the unfused path, which runs the fix-up and reports errors with their
+ * global indices.  PFB_E_PEER_TIMEOUT if a peer does not post in timeout_s. */
+int pfb_nll_peer(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* store, int64_t begin, int64_t end,
+                 int64_t index_offset, const double* values, int32_t nvalues, const double* norms,
+                 int32_t nnorms, double timeout_s, double* out_nll, int32_t* out_slow);
 
 /* ---- sharding ------------------------------------------------------------------ */
 /* Reference shard() bounds: bounds[0..workers] (sharding.py:80-85). */

@@ -148,6 +148,8 @@ _SIGNATURES = [
     ("pfb_peer_attach", c_int, [_PTR, _PTR]),
     ("pfb_peer_mailbox", c_int, [_PTR, POINTER(_PTR)]),
     ("pfb_peer_allreduce", c_int, [_PTR, _PTR, c_double]),
+    ("pfb_nll_peer", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, c_int64, _DBL_P, c_int32, _DBL_P, c_int32,
+                             c_double, POINTER(c_double), POINTER(c_int32)]),
     ("pfb_read_bw", c_int, [_PTR, _PTR, c_int64, c_int32, c_int32, c_int32, _DBL_P]),
     ("pfb_overhead_probe", c_int, [_PTR, c_int32, c_int32, _DBL_P]),
     ("pfb_npy_length", c_int, [ctypes.c_char_p, _I64_P]),

@@ -90,7 +90,7 @@ static int cuda_fail(cudaError_t e) {
 
 static constexpr int kStoreMaxCols = 16;
 // result words: [0, 72) exported accumulator, [72] deferred-block count, [73] error key
-static constexpr int kResHead = 2;  // [0] deferred-block count, [1] error key
+static constexpr int kResHead = 4;  // [0] deferred-block count, [1] error key, [2] [3] fused exchange status
 static constexpr int kResWords = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
 enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
@@ -2217,9 +2217,18 @@ int pfb_read_bw(pfb_ctx* c, const double* buf, int64_t bytes, int32_t mode, int3
 // ---- cross-GPU accumulator exchange over peer memory ---------------
 
 int pfb_peer_create(pfb_ctx* c, int32_t rank, int32_t world, uint8_t* out_handle) {
-    if (!c || world < 1 || world > peer_max() || rank < 0 || rank >= world || c->peer_world)
-        return PFB_E_INVALID_ARGUMENT;
+    if (!c || world < 1 || world > peer_max() || rank < 0 || rank >= world) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    if (c->peer_world) {  // already a member: the same group again is a no-op
+        if (c->peer_world != world || c->peer_rank != rank) return PFB_E_INVALID_ARGUMENT;
+        if (out_handle) {
+            cudaIpcMemHandle_t h;
+            memset(&h, 0, sizeof(h));
+            if (world > 1) CK(cudaIpcGetMemHandle(&h, c->peer_ptr[rank]));
+            memcpy(out_handle, &h, sizeof(h));
+        }
+        return PFB_OK;
+    }
     long long* m = nullptr;
     CK(cudaMalloc(&m, peer_mailbox_bytes()));
     CK(cudaMemset(m, 0, peer_mailbox_bytes()));
@@ -2263,6 +2272,53 @@ int pfb_peer_mailbox(pfb_ctx* c, void** out) {
     if (!c || !out || !c->peer_world) return PFB_E_INVALID_ARGUMENT;
     *out = c->peer_ptr[c->peer_rank];
     return PFB_OK;
+}
+
+int pfb_nll_peer(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin, int64_t end,
+                 int64_t index_offset, const double* values, int32_t nvalues, const double* norms,
+                 int32_t nnorms, double timeout_s, double* out_nll, int32_t* out_slow) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || !out_nll || !out_slow || p->ctx != c || st->ctx != c ||
+        !c->peer_world || !(timeout_s > 0.0))
+        return PFB_E_INVALID_ARGUMENT;
+    for (int q = 0; q < c->peer_world; ++q)
+        if (!c->peer_ptr[q]) return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (begin < 0 || end <= begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    (void)index_offset;  // errors take the unfused path, which reports them with their offsets
+    *out_slow = 0;
+    CK(cudaSetDevice(c->device));
+    pfb_store staged;
+    const bool restaged = !range_aligned(p, st, begin);
+    if (restaged) {
+        const int rs = restage(c, p, st, begin, end, &staged);
+        if (rs) return rs;
+        st = &staged;
+        end -= begin;
+        begin = 0;
+    }
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
+    if (rc) return rc;
+    auto A = std::make_unique<NllArgs>();
+    pack_args(p, st, begin, end, values, norms, A.get());
+    A->mode = MODE_EXPORT;
+    int khz = 0;
+    CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device));
+    for (int q = 0; q < c->peer_world; ++q) A->peer_mbox[q] = c->peer_ptr[q];
+    A->peer_world = c->peer_world;
+    A->peer_rank = c->peer_rank;
+    A->peer_seq = ++c->peer_seq;
+    A->peer_timeout = (long long)(timeout_s * (double)khz * 1e3);
+    rc = launch_eval(p, st, begin, end, A.get(), !restaged);
+    if (rc) return rc;
+    rc = read_result(c);
+    if (rc) return rc;
+    if (c->res_host[3]) return PFB_E_PEER_TIMEOUT;
+    if (c->res_host[2]) {  // a rank deferred blocks or failed: the caller redoes the call unfused
+        *out_slow = 1;
+        return PFB_OK;
+    }
+    return round_result(c, out_nll);
 }
 
 int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {

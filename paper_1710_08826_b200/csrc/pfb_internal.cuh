@@ -39,6 +39,8 @@ constexpr int kMaxTerms = 4;             // sum-of-products terms (fast path)
 constexpr int kMaxDal = PFB_MAX_DALITZ_TERMS;
 constexpr int kThreads = 256;            // CTA size of the NLL kernels
 constexpr int kMaxPts = 16;              // parameter points evaluated in one pass
+constexpr int kMaxPeers = 16;            // ranks of a peer-memory exchange
+constexpr int kPeerSlotWords = 80;       // mailbox slot: 72 limbs + status word, padded
 constexpr int kPtLeafWords = 16;         // per-point leaf values (mu, 1/sigma, alpha, coeffs)
 constexpr int kPtWords = kPtLeafWords + 2 * kMaxTerms;  // + (log coef, threshold) per term
 
@@ -142,7 +144,35 @@ struct NllArgs {
     // dalitz
     double inv_norm;          // 1/norm_root (fast paths)
     DalDesc dal;
+    // fused cross-GPU exchange of the exact accumulator (pfb_nll_peer): the
+    // CTA that finishes the launch trades its limbs with every rank's
+    // mailbox over NVLink peer memory and exports the global sum
+    long long* peer_mbox[kMaxPeers];
+    int32_t peer_world;       // 0: no exchange
+    int32_t peer_rank;
+    unsigned long long peer_seq;
+    long long peer_timeout;   // clock64 cycles of the bounded wait
 };
+
+// Peer mailbox layout (64-bit words): data [2][kMaxPeers][kPeerSlotWords],
+// flags [2][kMaxPeers]; parity = call sequence number & 1.
+__host__ __device__ constexpr size_t peer_mbox_words() {
+    return 2 * kMaxPeers * kPeerSlotWords + 2 * kMaxPeers;
+}
+__device__ __forceinline__ long long* peer_slot(long long* m, int par, int r) {
+    return m + ((size_t)par * kMaxPeers + r) * kPeerSlotWords;
+}
+__device__ __forceinline__ unsigned long long* peer_flag(long long* m, int par, int r) {
+    return reinterpret_cast<unsigned long long*>(m + 2 * kMaxPeers * kPeerSlotWords) + par * kMaxPeers + r;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Synthetic-event generators (pfb_gen.cu).
 struct GenDalitz {

@@ -786,6 +786,68 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* t) {
     return old;
 }
 
+// Fused exchange (A.peer_world > 0, single point, export mode), run by every
+// thread of the CTA that finishes the launch, after the ticket: this rank's
+// 72 limbs and a status word (deferred blocks or an error on this rank) go
+// into slot [seq & 1][rank] of every rank's mailbox (NVLink P2P stores), a
+// system-scope release raises flag [seq & 1][rank] = seq in every mailbox,
+// the CTA waits (acquire, bounded) for all flags of its own mailbox and sums
+// the slots in rank order -- integer limbs, so every rank exports the
+// single-GPU accumulator bit for bit, with no separate collective launch.
+// result_i[2] = number of ranks that need the slow path (deferred blocks or
+// an error: the host then redoes the call unfused), result_i[3] = 1 on a
+// peer timeout.  Parity alternation: a rank can be at most one call ahead
+// (it cannot pass call s+1's wait before every rank has posted s+1, i.e.
+// finished reading call s), so it never overwrites a slot still being read.
+__device__ __forceinline__ void peer_finish(const NllArgs& A) {
+    __shared__ long long s_loc[PFB_ACC_WORDS + 1];
+    __shared__ int s_timeout;
+    const int t = threadIdx.x;
+    if (t == 0) s_timeout = 0;
+    if (t < PFB_ACC_WORDS) s_loc[t] = (long long)atomicExch(A.acc + t, 0ull);
+    if (t == PFB_ACC_WORDS) {
+        const long long fx = (long long)atomicExch(A.fix_counter, 0ull);
+        const unsigned long long ek = atomicExch(A.errkey, ~0ull);
+        A.result_i[0] = fx;
+        A.result_i[1] = (long long)ek;
+        s_loc[PFB_ACC_WORDS] = (fx != 0 || ek != ~0ull) ? 1 : 0;
+    }
+    __syncthreads();
+    const int par = (int)(A.peer_seq & 1ull);
+    if (t <= PFB_ACC_WORDS) {
+        const long long v = s_loc[t];
+        for (int q = 0; q < A.peer_world; ++q) peer_slot(A.peer_mbox[q], par, A.peer_rank)[t] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (t < A.peer_world) st_release_sys(peer_flag(A.peer_mbox[t], par, A.peer_rank), A.peer_seq);
+    if (t < A.peer_world) {
+        const unsigned long long* f = peer_flag(A.peer_mbox[A.peer_rank], par, t);
+        const long long t0 = clock64();
+        while (ld_acquire_sys(f) != A.peer_seq) {
+            if (clock64() - t0 > A.peer_timeout) {
+                atomicExch(&s_timeout, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    if (s_timeout) {
+        if (t == 0) A.result_i[3] = 1;
+        return;
+    }
+    if (t <= PFB_ACC_WORDS) {
+        long long sum = 0;
+        for (int q = 0; q < A.peer_world; ++q) sum += peer_slot(A.peer_mbox[A.peer_rank], par, q)[t];
+        if (t < PFB_ACC_WORDS)
+            A.acc_out[t] = sum;
+        else
+            A.result_i[2] = sum;
+    }
+    if (t == 0) A.result_i[3] = 0;
+}
+
 // Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and
 // resets the launch-scoped counters.  Shared by every fast kernel.
 template <bool LIST>
@@ -805,6 +867,10 @@ __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc,
         *A.ticket = 0u;
     }
     if (A.mode == MODE_ACCUM) return;
+    if (!LIST && A.peer_world > 0 && A.mode == MODE_EXPORT) {
+        peer_finish(A);
+        return;
+    }
     if (t == nt - 2 && !LIST)  // hand the deferred-block count to the fix-up launch
         A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
     if (t == nt - 3) A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);

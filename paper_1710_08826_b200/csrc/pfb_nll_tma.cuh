@@ -107,6 +107,10 @@ __device__ __forceinline__ void finish_launch_pts(const NllArgs& A, long long* s
         *A.ticket = 0u;
     }
     if (A.mode == MODE_ACCUM) return;
+    if (A.peer_world > 0 && A.mode == MODE_EXPORT && nwords == PFB_ACC_WORDS) {
+        peer_finish(A);
+        return;
+    }
     if (tid == nt - 2) A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
     if (tid == nt - 3) A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
     for (int i = tid; i < nwords; i += nt) {

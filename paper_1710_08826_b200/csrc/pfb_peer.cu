@@ -17,33 +17,14 @@
 
 namespace pfb {
 
-constexpr int kMaxPeers = 16;
-constexpr int kSlotWords = 80;  // 72 limbs, padded
-
+// the mailbox layout and the release / acquire helpers are in pfb_internal.cuh
+// (shared with the fused exchange in the NLL kernels' epilogue)
 struct PeerArgs {
     long long* mbox[kMaxPeers];  // every rank's mailbox (mbox[rank] is local)
     int world, rank;
     unsigned long long seq;
     long long timeout_cycles;
 };
-
-// mailbox layout (64-bit words): data [2][kMaxPeers][kSlotWords], flags [2][kMaxPeers]
-__host__ __device__ constexpr size_t mbox_words() { return 2 * kMaxPeers * kSlotWords + 2 * kMaxPeers; }
-__device__ __forceinline__ long long* slot_of(long long* m, int par, int r) {
-    return m + ((size_t)par * kMaxPeers + r) * kSlotWords;
-}
-__device__ __forceinline__ unsigned long long* flag_of(long long* m, int par, int r) {
-    return reinterpret_cast<unsigned long long*>(m + 2 * kMaxPeers * kSlotWords) + par * kMaxPeers + r;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 __global__ void __launch_bounds__(128) peer_allreduce_kernel(const __grid_constant__ PeerArgs P, long long* acc,
                                                              unsigned long long* status) {
@@ -54,15 +35,15 @@ __global__ void __launch_bounds__(128) peer_allreduce_kernel(const __grid_consta
     // 1. this rank's limbs into slot [par][rank] of every mailbox
     if (tid < PFB_ACC_WORDS) {
         const long long v = acc[tid];
-        for (int q = 0; q < P.world; ++q) slot_of(P.mbox[q], par, P.rank)[tid] = v;
+        for (int q = 0; q < P.world; ++q) peer_slot(P.mbox[q], par, P.rank)[tid] = v;
     }
     __threadfence_system();
     __syncthreads();
     // 2. announce
-    if (tid < P.world) st_release_sys(flag_of(P.mbox[tid], par, P.rank), P.seq);
+    if (tid < P.world) st_release_sys(peer_flag(P.mbox[tid], par, P.rank), P.seq);
     // 3. wait for every rank's announcement in the local mailbox (bounded)
     if (tid < P.world) {
-        const unsigned long long* f = flag_of(P.mbox[P.rank], par, tid);
+        const unsigned long long* f = peer_flag(P.mbox[P.rank], par, tid);
         const long long t0 = clock64();
         while (ld_acquire_sys(f) != P.seq) {
             if (clock64() - t0 > P.timeout_cycles) {
@@ -80,7 +61,7 @@ __global__ void __launch_bounds__(128) peer_allreduce_kernel(const __grid_consta
     // 4. the sum over ranks, in rank order (integer: exact)
     if (tid < PFB_ACC_WORDS) {
         long long s = 0;
-        for (int q = 0; q < P.world; ++q) s += slot_of(P.mbox[P.rank], par, q)[tid];
+        for (int q = 0; q < P.world; ++q) s += peer_slot(P.mbox[P.rank], par, q)[tid];
         acc[tid] = s;
     }
     if (tid == 0) *status = 0ull;
@@ -100,7 +81,7 @@ cudaError_t launch_peer_allreduce(long long* const* mbox, int world, int rank, u
     return cudaGetLastError();
 }
 
-size_t peer_mailbox_bytes() { return mbox_words() * sizeof(long long); }
+size_t peer_mailbox_bytes() { return peer_mbox_words() * sizeof(long long); }
 int peer_max() { return kMaxPeers; }
 
 }  // namespace pfb

@@ -198,8 +198,8 @@ class ShardedNll:
 
         from . import engine
 
-        if collective not in ("nccl", "peer"):
-            raise ValueError("collective must be 'nccl' or 'peer'")
+        if collective not in ("nccl", "peer", "fused"):
+            raise ValueError("collective must be 'nccl', 'peer' or 'fused'")
 
         self.pdf = pdf
         self.rank, self.world, self.group = int(rank), int(world), group
@@ -215,7 +215,10 @@ class ShardedNll:
         self.store = self.ctx.store_for(self.arrays)
         self.acc = torch.zeros(L.PFB_ACC_WORDS, dtype=torch.int64, device=f"cuda:{device}")
         self.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
-        self.peers = PeerGroup(self.ctx, rank, world, group) if collective == "peer" else None
+        # "fused": the exchange runs inside the NLL kernel (pfb_nll_peer), the
+        # unfused peer kernel only on the rare slow path
+        self.fused = collective == "fused"
+        self.peers = PeerGroup(self.ctx, rank, world, group) if collective in ("peer", "fused") else None
 
     def launch(self, snap, norms):
         """Enqueue the local partial (no host sync)."""
@@ -244,6 +247,20 @@ class ShardedNll:
         return out.value
 
     def __call__(self, snap, norms) -> float:
+        if self.fused:
+            vals, nv = self.plan.pack(snap, norms)
+            out, slow = ctypes.c_double(), ctypes.c_int32()
+            code = L.lib().pfb_nll_peer(self.ctx.handle, self.plan.handle, self.store, 0, self.end - self.begin,
+                                        self.begin, L.dptr(vals), len(vals), L.dptr(nv), len(nv),
+                                        self.peers.timeout_s, ctypes.byref(out), ctypes.byref(slow))
+            if code == L.E_PEER_TIMEOUT:
+                raise TimeoutError(f"rank {self.rank}: a peer did not post its accumulator "
+                                   f"within {self.peers.timeout_s} s")
+            L.check(code, "pfb_nll_peer")
+            if not slow.value:
+                return out.value
+            # some rank deferred blocks or failed: every rank saw the same
+            # global status word and redoes the call unfused (fix-up, errors)
         self.launch(snap, norms)
         return self.finish()
 

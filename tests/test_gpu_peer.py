@@ -113,3 +113,109 @@ def test_missing_peer_times_out(pf):
         assert L.lib().pfb_peer_allreduce(h, ctypes.c_void_p(acc.data_ptr()), 0.01) == L.E_PEER_TIMEOUT
     finally:
         L.lib().pfb_ctx_destroy(h)
+
+
+# ---- the exchange fused into the NLL kernel's epilogue (pfb_nll_peer) ----------------
+
+
+def test_fused_single_rank_equals_nll(pf):
+    from paper_1710_08826_b200.sharding import ShardedNll
+
+    rng = np.random.default_rng(4)
+    n = 3 * 4096 * 50 + 777
+    (x, y), pdf, _ = models.c2()
+    ds = models.dataset([x, y], [np.clip(rng.normal(5, 1, n), 0, 10), np.clip(rng.exponential(2.5, n), 0, 10)])
+    sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
+    snap = pf.snapshot(pdf.param_closure())
+    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    ref = pf.nll(pdf, ds)
+    for _ in range(5):  # parity alternates call to call
+        assert sn(snap, norms) == ref
+
+
+def test_fused_with_preposted_peer(pf):
+    """Rank 0 of 2 evaluates its shard with the exchange fused into the NLL
+    kernel; rank 1's limbs (the other shard's exact partial) are pre-posted in
+    rank 0's mailbox.  The fused call returns the whole dataset's NLL bit for
+    bit and leaves rank 0's limbs + status word + flag in rank 1's mailbox."""
+    import torch
+
+    from paper_1710_08826_b200 import _lib as L
+    from paper_1710_08826_b200 import sharding
+    from paper_1710_08826_b200.engine import DeviceContext
+
+    rng = np.random.default_rng(5)
+    n = 4096 * 300 + 1001
+    (x, y), pdf, _ = models.c2((4.9, 1.05, -0.38))
+    cx, cy = np.clip(rng.normal(5, 1, n), 0, 10), np.clip(rng.exponential(2.5, n), 0, 10)
+    ds = models.dataset([x, y], [cx, cy])
+    whole = pf.nll(pdf, ds)
+    b = sharding.shard_bounds(n, 2)
+    ctx = DeviceContext(0)
+    try:
+        plan = ctx.plan_for(pdf, ("x", "y"))
+        snap = pf.snapshot(pdf.param_closure())
+        norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+        vals, nv = plan.pack(snap, norms)
+        # rank 1's exact partial over its shard
+        st1 = ctx.store_for([np.ascontiguousarray(cx[b[1]:]), np.ascontiguousarray(cy[b[1]:])])
+        acc1 = torch.zeros(72, dtype=torch.int64, device="cuda")
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        L.check(L.lib().pfb_nll_partial_async(ctx.handle, plan.handle, st1, 0, n - b[1], b[1], L.dptr(vals),
+                                              len(vals), L.dptr(nv), len(nv), ctypes.c_void_p(acc1.data_ptr())),
+                "pfb_nll_partial_async")
+        torch.cuda.synchronize()
+        theirs = acc1.cpu().numpy()
+        # wire rank 0 to a stand-in mailbox for rank 1 and pre-post rank 1's call 1
+        L.check(L.lib().pfb_peer_create(ctx.handle, 0, 2, None), "pfb_peer_create")
+        other = torch.zeros(2 * PEERS * SLOT + 2 * PEERS, dtype=torch.int64, device="cuda")
+        ptrs = (ctypes.c_void_p * 2)(None, ctypes.c_void_p(other.data_ptr()))
+        L.check(L.lib().pfb_peer_attach(ctx.handle, ptrs), "pfb_peer_attach")
+        mb = ctypes.c_void_p()
+        L.check(L.lib().pfb_peer_mailbox(ctx.handle, ctypes.byref(mb)), "pfb_peer_mailbox")
+        nwords = 2 * PEERS * SLOT + 2 * PEERS
+        host = np.zeros(nwords, dtype=np.int64)
+        host[slot_word(1, 1):slot_word(1, 1) + 72] = theirs
+        host[slot_word(1, 1) + 72] = 0  # rank 1: no deferred blocks, no error
+        host[flag_word(1, 1)] = 1
+        box = torch.from_numpy(host).cuda()
+        torch.cuda.synchronize()
+        _copy_d2d(mb.value, box.data_ptr(), nwords * 8)
+        st0 = ctx.store_for([np.ascontiguousarray(cx[:b[1]]), np.ascontiguousarray(cy[:b[1]])])
+        out, slow = ctypes.c_double(), ctypes.c_int32()
+        code = L.lib().pfb_nll_peer(ctx.handle, plan.handle, st0, 0, b[1], 0, L.dptr(vals), len(vals), L.dptr(nv),
+                                    len(nv), 5.0, ctypes.byref(out), ctypes.byref(slow))
+        assert code == L.OK and slow.value == 0
+        assert out.value == whole
+        o = other.cpu().numpy()
+        mine = o[slot_word(1, 0):slot_word(1, 0) + 72]
+        assert sharding.round_acc(mine + theirs) == whole
+        assert o[slot_word(1, 0) + 72] == 0 and o[flag_word(1, 0)] == 1
+        # a peer that never posts call 2: bounded wait, no hung GPU
+        code = L.lib().pfb_nll_peer(ctx.handle, plan.handle, st0, 0, b[1], 0, L.dptr(vals), len(vals), L.dptr(nv),
+                                    len(nv), 0.01, ctypes.byref(out), ctypes.byref(slow))
+        assert code == L.E_PEER_TIMEOUT
+    finally:
+        ctx.close()
+
+
+def test_fused_slow_path_reports_the_reference_error(pf):
+    """An event with zero density: the fused call flags the slow path and the
+    unfused redo raises the reference's NonPositiveDensity (global index)."""
+    from paper_1710_08826_b200 import errors as E
+    from paper_1710_08826_b200.sharding import ShardedNll
+
+    rng = np.random.default_rng(6)
+    n = 4096 * 20 + 5
+    x = np.clip(rng.normal(5, 0.1, n), 0, 10)
+    x[4321] = 9.999  # 50 sigma from the mean of a pure gaussian: the density underflows to 0
+    xv, pdf, params = models.c1((5.0, 0.1, -0.3, 1.0))
+    ds = models.dataset([xv], [x])
+    with pytest.raises(E.NonPositiveDensity) as ref:
+        pf.nll(pdf, ds)
+    sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
+    snap = pf.snapshot(pdf.param_closure())
+    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    with pytest.raises(E.NonPositiveDensity) as got:
+        sn(snap, norms)
+    assert got.value.index == ref.value.index == 4321
