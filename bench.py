@@ -180,8 +180,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override events per GPU")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1: accumulator all-reduce through NCCL or the peer-memory kernel (pfb_peer_*)")
+    ap.add_argument("--collective", default="fused", choices=["fused", "nccl", "peer"],
+                    help="N > 1: the accumulator exchange fused into the NLL kernel over NVLink peer memory "
+                         "(pfb_nll_peer; NCCL if the peer set-up fails or disagrees), an NCCL all-reduce, "
+                         "or the separate peer-memory kernel (pfb_peer_allreduce)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -266,10 +268,15 @@ def main():
     err = L.PfbErr()
 
     peers = None
-    if world > 1 and args.collective == "peer":
+    collective = args.collective if world > 1 else "none"
+    if world > 1 and collective in ("peer", "fused"):
         from paper_1710_08826_b200.sharding import PeerGroup
 
-        peers = PeerGroup(ctx, rank, world)
+        try:  # collective on every rank: a failure raises everywhere, nobody hangs
+            peers = PeerGroup(ctx, rank, world, timeout_s=5.0)
+        except Exception as exc:  # no CUDA IPC / peer access: the NCCL path still measures the step
+            log(f"[rank {rank}] peer-memory set-up failed ({exc}); using NCCL")
+            collective = "nccl (peer set-up failed)"
     ev_a = torch.cuda.Event(enable_timing=True)
     ev_b = torch.cuda.Event(enable_timing=True)
 
@@ -280,12 +287,22 @@ def main():
                                    L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err))
             L.check(code, "pfb_nll")
             return ctx.last_kernel_ms(), out.value
+        if collective == "fused":
+            # N > 1, fused: one launch per step, the exchange of the 72-word
+            # exact accumulator over NVLink peer memory inside the kernel
+            slow = ctypes.c_int32()
+            code = L.lib().pfb_nll_peer(ctx.handle, plan.handle, store, 0, n_per, 0, L.dptr(vals), len(vals),
+                                        L.dptr(nv), len(nv), peers.timeout_s, ctypes.byref(out), ctypes.byref(slow))
+            L.check(code, "pfb_nll_peer")
+            if slow.value:
+                raise SystemExit("fused step took the slow path (deferred blocks or an error on a rank)")
+            return ctx.last_kernel_ms(), out.value
         # N > 1: the step is the fused kernel plus the all-reduce of the 72-word
         # exact accumulator, timed together with CUDA events on this stream
         ev_a.record()
         L.check(L.lib().pfb_nll_partial_async(ctx.handle, plan.handle, store, 0, n_per, 0, L.dptr(vals), len(vals),
                                               L.dptr(nv), len(nv), ctypes.c_void_p(acc.data_ptr())), "partial")
-        if peers is not None:
+        if peers is not None and collective == "peer":
             peers.allreduce(acc)
         else:
             torch.distributed.all_reduce(acc)
@@ -295,9 +312,25 @@ def main():
                                      ctypes.byref(fails)), "finalize")
         return ev_a.elapsed_time(ev_b), out.value
 
-    for _ in range(max(3, args.warmup)):
-        flush.zero_()
-        step_local()
+    def warm_up():
+        for _ in range(max(3, args.warmup)):
+            flush.zero_()
+            step_local()
+
+    if collective == "fused":
+        try:
+            warm_up()
+            ok = 1
+        except Exception as exc:  # a peer timeout or error: decide together, fall back to NCCL
+            log(f"[rank {rank}] fused warm-up failed ({exc})")
+            ok = 0
+        t_ok = torch.tensor([ok], device=dev)
+        torch.distributed.all_reduce(t_ok, op=torch.distributed.ReduceOp.MIN)
+        if int(t_ok.item()) == 0:
+            collective = "nccl (fused exchange failed in warm-up)"
+            warm_up()
+    else:
+        warm_up()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -310,6 +343,15 @@ def main():
     crosscheck = abs(fast_nll - simt_nll) / abs(simt_nll)
     if not crosscheck <= 1e-12:
         raise SystemExit(f"NLL cross-check failed: fast kernel {fast_nll!r} vs SIMT kernel {simt_nll!r}")
+    if collective == "fused":
+        # the exchange inside the kernel must give the NCCL path's bits (every
+        # rank sees the same two global values, so all ranks decide alike)
+        _, fused_nll = step_local()
+        collective = "nccl"
+        _, nccl_nll = step_local()
+        collective = "fused" if fused_nll == nccl_nll else "nccl (fused exchange disagreed)"
+        if collective != "fused":
+            log(f"[rank {rank}] fused exchange {fused_nll!r} != NCCL {nccl_nll!r}; timing the NCCL path")
 
     launches0 = ctx.launch_count()
     kernel_ms = []
@@ -324,6 +366,8 @@ def main():
             # events around the kernel time the kernel, not launch latency
             # (pfb_ctx_spin: same shared-memory carveout as the NLL kernels,
             # as in a fit loop where only NLL launches reach the GPU)
+            if world > 1:  # ranks start each step together (outside the event window)
+                torch.distributed.barrier()
             ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * flush.element_size())
             ms, nll_value = step_local()
             kernel_ms.append(ms)
@@ -416,7 +460,7 @@ def main():
         "config": {"workload": CONFIGS[cfg]["workload"], "n_events_per_gpu": n_per,
                    "evaluator": plan.evaluator, "l2": "flushed (256 MB read) before every step",
                    "parallelism": f"events sharded over {world} GPU(s), 1 all-reduce of 72 int64 per call"
-                                  + (f" ({args.collective})" if world > 1 else "")},
+                                  + (f" ({collective})" if world > 1 else "")},
         "nll_evals_per_s": args.steps / dev_s,
         "nll": nll_value,
         "nll_crosscheck_rel": crosscheck,

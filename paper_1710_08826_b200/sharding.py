@@ -168,15 +168,33 @@ class PeerGroup:
     def __init__(self, ctx, rank: int, world: int, group=None, timeout_s: float = 10.0):
         self.ctx, self.rank, self.world, self.timeout_s = ctx, int(rank), int(world), float(timeout_s)
         handle = (ctypes.c_uint8 * 64)()
-        L.check(L.lib().pfb_peer_create(ctx.handle, self.rank, self.world, handle), "pfb_peer_create")
-        handles = [bytes(handle)]
+        # every rank takes part in every collective below even if its own
+        # step failed, so a failure raises on all ranks instead of hanging one
+        code = L.lib().pfb_peer_create(ctx.handle, self.rank, self.world, handle)
+        mine = bytes(handle) if code == L.OK else None
+        handles = [mine]
         if self.world > 1:
             import torch.distributed as dist
 
             handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(handle), group=group)
+            dist.all_gather_object(handles, mine, group=group)
+        if any(h is None for h in handles):
+            L.check(code, "pfb_peer_create")
+            raise RuntimeError("peer-memory set-up failed on another rank")
         buf = (ctypes.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(handles))
-        L.check(L.lib().pfb_peer_open(ctx.handle, buf), "pfb_peer_open")
+        code = L.lib().pfb_peer_open(ctx.handle, buf)
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            ok = torch.tensor([1 if code == L.OK else 0], dtype=torch.int64)
+            if dist.get_backend(group) == "nccl":
+                ok = ok.cuda()
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) == 0:
+                L.check(code, "pfb_peer_open")
+                raise RuntimeError("peer-memory set-up failed on another rank")
+        L.check(code, "pfb_peer_open")
 
     def allreduce(self, acc) -> None:
         code = L.lib().pfb_peer_allreduce(self.ctx.handle, ctypes.c_void_p(acc.data_ptr()), self.timeout_s)
