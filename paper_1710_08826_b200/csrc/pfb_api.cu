@@ -1794,27 +1794,36 @@ static int download_to_host(pfb_ctx* c, const double* dev, double* host, int64_t
     std::vector<cudaError_t> errs(lanes, cudaSuccess);
     std::vector<std::thread> pool;
     const int64_t share = (count + lanes - 1) / lanes;
+    auto lane = [&](int t) {
+        cudaError_t e = cudaSetDevice(c->device);
+        const int64_t b0 = std::min(count, t * share), b1 = std::min(count, b0 + share);
+        const int64_t np = (b1 - b0 + kDlChunk - 1) / kDlChunk;
+        cudaStream_t s = c->dl_stream[t];
+        double* const* buf = c->dl_pinned[t];
+        auto piece = [&](int64_t k) { return std::min(kDlChunk, b1 - (b0 + k * kDlChunk)); };
+        auto at = [&](int64_t k) { return b0 + k * kDlChunk; };
+        if (e == cudaSuccess && np > 0)
+            e = cudaMemcpyAsync(buf[0], dev + at(0), sizeof(double) * piece(0), cudaMemcpyDeviceToHost, s);
+        for (int64_t k = 0; e == cudaSuccess && k < np; ++k) {
+            e = cudaStreamSynchronize(s);  // piece k is in buffer k & 1
+            if (e == cudaSuccess && k + 1 < np)
+                e = cudaMemcpyAsync(buf[(k + 1) & 1], dev + at(k + 1), sizeof(double) * piece(k + 1),
+                                    cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) memcpy(host + at(k), buf[k & 1], sizeof(double) * piece(k));
+        }
+        errs[t] = e;
+    };
+    // no exception may cross the C ABI: a lane whose thread cannot be
+    // started runs on this thread after the others are launched
+    std::vector<int> inline_lanes;
     for (int t = 0; t < lanes; ++t) {
-        pool.emplace_back([&, t]() {
-            cudaError_t e = cudaSetDevice(c->device);
-            const int64_t b0 = std::min(count, t * share), b1 = std::min(count, b0 + share);
-            const int64_t np = (b1 - b0 + kDlChunk - 1) / kDlChunk;
-            cudaStream_t s = c->dl_stream[t];
-            double* const* buf = c->dl_pinned[t];
-            auto piece = [&](int64_t k) { return std::min(kDlChunk, b1 - (b0 + k * kDlChunk)); };
-            auto at = [&](int64_t k) { return b0 + k * kDlChunk; };
-            if (e == cudaSuccess && np > 0)
-                e = cudaMemcpyAsync(buf[0], dev + at(0), sizeof(double) * piece(0), cudaMemcpyDeviceToHost, s);
-            for (int64_t k = 0; e == cudaSuccess && k < np; ++k) {
-                e = cudaStreamSynchronize(s);  // piece k is in buffer k & 1
-                if (e == cudaSuccess && k + 1 < np)
-                    e = cudaMemcpyAsync(buf[(k + 1) & 1], dev + at(k + 1), sizeof(double) * piece(k + 1),
-                                        cudaMemcpyDeviceToHost, s);
-                if (e == cudaSuccess) memcpy(host + at(k), buf[k & 1], sizeof(double) * piece(k));
-            }
-            errs[t] = e;
-        });
+        try {
+            pool.emplace_back(lane, t);
+        } catch (...) {
+            inline_lanes.push_back(t);
+        }
     }
+    for (int t : inline_lanes) lane(t);
     for (auto& th : pool) th.join();
     for (int t = 0; t < lanes; ++t) CK(errs[t]);
     return PFB_OK;
