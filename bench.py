@@ -459,8 +459,8 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIGS[cfg]["workload"], "n_events_per_gpu": n_per,
                    "evaluator": plan.evaluator, "l2": "flushed (256 MB read) before every step",
-                   "parallelism": f"events sharded over {world} GPU(s), 1 all-reduce of 72 int64 per call"
-                                  + (f" ({collective})" if world > 1 else "")},
+                   "parallelism": (f"events sharded over {world} GPUs, one exchange of the 72-limb exact "
+                                   f"accumulator per call ({collective})" if world > 1 else "one GPU, no exchange")},
         "nll_evals_per_s": args.steps / dev_s,
         "nll": nll_value,
         "nll_crosscheck_rel": crosscheck,
