@@ -80,3 +80,36 @@ def test_backend_rejects_a_foreign_block_size():
     backend = ProtocolBackend(models.c2_spec((5.0, 1.0, -0.4)))
     with pytest.raises(ValueError):
         backend.map(lambda *a: None, [(None, {}, None, {}, 0, 10, 1024)])
+
+
+def test_reference_fitmanager_with_the_backend_protocol(golden_dir):
+    """The reference FitManager (fitting.py:410) on the C2 golden events with
+    the protocol backend converges to the reference's own fit (fits.json)."""
+    import json
+
+    core, engine, rpdf = _reference()
+    from parafit.fitting import FitManager
+
+    with open(os.path.join(golden_dir, "fits.json")) as fh:
+        ref = json.load(fh)["c2"]
+    g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
+    x = core.Variable.observable("x", 0.0, 10.0)
+    y = core.Variable.observable("y", 0.0, 10.0)
+    mu = core.Variable("mu", ref["start"][0], 0.0, 10.0, step=0.01)
+    sigma = core.Variable("sigma", ref["start"][1], 0.01, 5.0, step=1e-3)
+    alpha = core.Variable("alpha", ref["start"][2], -5.0, 5.0, step=1e-3)
+    pdf = rpdf.prod_pdf([rpdf.gaussian(x, mu, sigma), rpdf.exponential(y, alpha)])
+    ds = core.UnbinnedDataSet([x, y])
+    ds.extend([g["x"], g["y"]])
+
+    class FitBackend(ProtocolBackend):
+        def evaluate(self, pdf_, columns, snap, norms, start, stop, index_offset=0):
+            spec = models.c2_spec(tuple(snap.value_of(v) for v in (mu, sigma, alpha)))
+            cols = {k: np.asarray(v)[start:stop] for k, v in columns.items()}
+            return O.nll(spec, cols)
+
+    r = FitManager(pdf, ds, backend=FitBackend(None)).fit()
+    assert r.status == "converged" and list(r.names) == ref["names"]
+    for v, e, rv, re in zip(r.values, r.errors, ref["values"], ref["errors"]):
+        assert abs(v - rv) <= max(1e-6 * abs(rv), 1e-3 * re)
+    assert abs(r.nll_min - ref["nll_min"]) <= 1e-10 * abs(ref["nll_min"])
