@@ -313,3 +313,19 @@ def test_c2_uncertified_blocks_take_the_exact_fixup(pf):
     got = pf.nll(pdf, ds)
     assert ctx.launch_count() - before == 2
     assert rel(got, O.nll(models.c2_spec((5.0, 0.13, -0.4)), {"x": xs, "y": ys})) <= RTOL
+
+
+def test_c1_narrow_pure_gaussian_far_tails(pf):
+    """Densities down to ~2^-290 (a narrow pure gaussian, f = 1, over a wide
+    range): whichever kernel the plan takes, the NLL equals the reference's."""
+    rng = np.random.default_rng(23)
+    n = 6 * 4096 + 17
+    xs = np.concatenate([rng.normal(5.0, 0.1, n - 2000), rng.uniform(3.0, 7.0, 2000)])
+    rng.shuffle(xs)
+    xs = np.clip(xs, 0.0, 10.0)
+    point = (5.0, 0.1, -0.3, 1.0)
+    x, pdf, _ = models.c1(point)
+    ds = models.dataset([x], [xs])
+    got = pf.nll(pdf, ds)
+    want = O.nll(models.c1_spec(point), {"x": xs})
+    assert rel(got, want) <= RTOL
