@@ -19,28 +19,35 @@ static int signature_of(const DalDesc& D) {
     return sig | (D.need12 ? 1 << 12 : 0) | (D.need13 ? 1 << 13 : 0) | (D.need23 ? 1 << 14 : 0);
 }
 
-// Recompute-path evaluators run in product mode (one log per 16 events,
-// pfb_nll_prod.cuh) unless the pipeline is switched off (log-domain kernel).
-template <class Ev>
-static cudaError_t launch_dal(const NllArgs& A, cudaStream_t stream, int sm_count) {
-    if (A.tma) return launch_prod<Ev>(A, stream, sm_count);
-    return launch_p<Ev>(A, stream, sm_count);
-}
-
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.evaluator == EV_DALITZ_CACHED) return launch_p<EvDalitzCached>(A, stream, sm_count);
+    const bool d0 = A.dal.K == 4 && signature_of(A.dal) == kSigD0;
+    if (A.tma) {
+        // product kernels.  D0 -> pi+ pi- pi0 (C3/C4): the reciprocal-free
+        // ratio form with the term structure fixed at compile time.  Other
+        // models with 2..4 terms: the batch-inverted form (the ratio form with
+        // the structure read at run time measured 14-40% slower there);
+        // 5..6 terms: the run-time ratio form (1.9x faster than the per-term
+        // reciprocal kernel they used before, K = 5 measured)
+        if (d0) return launch_prod<EvDalitzR<4, kSigD0>>(A, stream, sm_count);
+        switch (A.dal.K) {
+            case 2: return launch_prod<EvDalitz<2>>(A, stream, sm_count);
+            case 3: return launch_prod<EvDalitz<3>>(A, stream, sm_count);
+            case 4: return launch_prod<EvDalitz<4>>(A, stream, sm_count);
+            case 5: return launch_prod<EvDalitzR<5>>(A, stream, sm_count);
+            case 6: return launch_prod<EvDalitzR<6>>(A, stream, sm_count);
+            default: break;
+        }
+    }
+    // pipeline 0 (log-domain SIMT kernels) and K > 6
     switch (A.dal.K) {
         case 2:
-            return launch_dal<EvDalitz<2>>(A, stream, sm_count);
+            return launch_p<EvDalitz<2>>(A, stream, sm_count);
         case 3:
-            return launch_dal<EvDalitz<3>>(A, stream, sm_count);
+            return launch_p<EvDalitz<3>>(A, stream, sm_count);
         case 4:
-            if (signature_of(A.dal) == kSigD0) {
-                // product kernels: the reciprocal-free ratio form
-                if (A.tma) return launch_prod<EvDalitzR<kSigD0>>(A, stream, sm_count);
-                return launch_p<EvDalitz<4, kSigD0>>(A, stream, sm_count);
-            }
-            return launch_dal<EvDalitz<4>>(A, stream, sm_count);
+            if (d0) return launch_p<EvDalitz<4, kSigD0>>(A, stream, sm_count);
+            return launch_p<EvDalitz<4>>(A, stream, sm_count);
         default:  // any K: per-term reciprocals, no cache rows
             return launch_p<EvDalitzCached>(A, stream, sm_count);
     }

@@ -495,44 +495,67 @@ struct EvDalitz {
 // square is taken on the unit's logarithm), and 1/norm rides in the
 // coefficients (sqrt(1/norm) each).  ~47 FP64 operations per event against
 // ~57 plus a reciprocal for EvDalitz.
-template <int SIG>
+template <int K_, int SIG = -1>
 struct EvDalitzR {
     static constexpr int NC = 2;
     static constexpr int U = 2;
     static constexpr int MINB = PFB_DALR_MINB;
     static constexpr bool RATIO = true;
     static constexpr int RATIO_POW = 2;  // p = num / den^2
-    static constexpr int K = 4;
-    static_assert(SIG >= 0, "compile-time term structure required");
+    static constexpr int K = K_;
+    // SIG >= 0: (pair, spin) per term and the needed 1/s_pair fixed at compile
+    // time (C3/C4); SIG < 0: the same algebra with the structure read from the
+    // term table at run time (any model with K terms)
+    static constexpr bool RT = SIG < 0;
+    static_assert(K >= 2 && K <= 6, "ratio form instantiated for 2..6 terms");
 
-    __host__ __device__ static constexpr int pcode(int k) { return (SIG >> (3 * k)) & 3; }
-    __host__ __device__ static constexpr int spin(int k) { return (SIG >> (3 * k + 2)) & 1; }
-    __host__ __device__ static constexpr bool need(int p) { return (SIG >> (12 + p)) & 1; }
+    __device__ static __forceinline__ int pcode(const DalDesc& D, int k) {
+        if constexpr (RT) return dal_pair_code(D.t[k].pair);
+        else return (SIG >> (3 * k)) & 3;
+    }
+    __device__ static __forceinline__ int spin(const DalDesc& D, int k) {
+        if constexpr (RT) return D.t[k].spin;
+        else return (SIG >> (3 * k + 2)) & 1;
+    }
+    __device__ static __forceinline__ bool need(const DalDesc& D, int p) {
+        if constexpr (RT) return p == 0 ? D.need12 != 0 : (p == 1 ? D.need13 != 0 : D.need23 != 0);
+        else return (SIG >> (12 + p)) & 1;
+    }
+    __device__ static __forceinline__ double pick(int p, double a, double b, double c) {
+        return p == 0 ? a : (p == 1 ? b : c);
+    }
 
     __device__ static __forceinline__ void one(const NllArgs& A, double s12, double s13, double& num,
                                                double& den) {
         const DalDesc& D = A.dal;
         const double s23 = (D.mss - s12) - s13;
-        const double sp[3] = {s12, s13, s23};
-        const double dd[3] = {s13 - s23, s12 - s23, s12 - s13};  // Zemach differences for pairs 12, 13, 23
-        const double zc[3] = {D.zc12, D.zc13, D.zc23};
+        const double dd12 = s13 - s23, dd13 = s12 - s23, dd23 = s12 - s13;  // Zemach differences
         double d[K], sv[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            sv[k] = sp[pcode(k)];
+            sv[k] = pick(pcode(D, k), s12, s13, s23);
             const double a = D.t[k].m2 - sv[k];
             d[k] = fma(a, a, D.t[k].mg2);
         }
         // exclusive products prod_{j != k} d_j (prefix x suffix)
-        const double pre2 = d[0] * d[1], pre3 = pre2 * d[2];
-        const double suf1 = d[2] * d[3], suf0 = d[1] * suf1;
-        const double ex[K] = {suf0, d[0] * suf1, pre2 * d[3], pre3};
+        double pre[K], suf[K];
+        pre[0] = 1.0;
+#pragma unroll
+        for (int k = 1; k < K; ++k) pre[k] = k == 1 ? d[0] : pre[k - 1] * d[k - 1];
+        suf[K - 1] = 1.0;
+#pragma unroll
+        for (int k = K - 2; k >= 0; --k) suf[k] = k == K - 2 ? d[K - 1] : suf[k + 1] * d[k + 1];
+        double ex[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) ex[k] = k == 0 ? suf[0] : (k == K - 1 ? pre[K - 1] : pre[k] * suf[k]);
+        // sigma = product of the needed s_pair
         double sig = 1.0;
         bool any = false;
 #pragma unroll
         for (int p = 0; p < 3; ++p)
-            if (need(p)) {
-                sig = any ? sig * sp[p] : sp[p];
+            if (need(D, p)) {
+                const double sp = pick(p, s12, s13, s23);
+                sig = any ? sig * sp : sp;
                 any = true;
             }
         double tr = 0.0, ti = 0.0;
@@ -540,24 +563,26 @@ struct EvDalitzR {
         for (int k = 0; k < K; ++k) {
             const DalTerm& T = D.t[k];
             double F;
-            if (spin(k) == 0) {
+            if (spin(D, k) == 0) {
                 F = sig;
             } else {
-                const int p = pcode(k);
-                if (need(p)) {
+                const int p = pcode(D, k);
+                const double ddp = pick(p, dd12, dd13, dd23);
+                if (need(D, p)) {
                     // Z sigma = (d_pair s_pair + zc) * prod of the other needed s
                     double others = 1.0;
                     bool anyo = false;
 #pragma unroll
                     for (int q = 0; q < 3; ++q)
-                        if (need(q) && q != p) {
-                            others = anyo ? others * sp[q] : sp[q];
+                        if (need(D, q) && q != p) {
+                            const double sq = pick(q, s12, s13, s23);
+                            others = anyo ? others * sq : sq;
                             anyo = true;
                         }
-                    const double zp = fma(dd[p], sp[p], zc[p]);
+                    const double zp = fma(ddp, pick(p, s12, s13, s23), pick(p, D.zc12, D.zc13, D.zc23));
                     F = anyo ? zp * others : zp;
                 } else {
-                    F = any ? dd[p] * sig : dd[p];
+                    F = any ? ddp * sig : ddp;
                 }
             }
             const double E = ex[k] * F;
@@ -565,7 +590,7 @@ struct EvDalitzR {
             ti = fma(E, fma(-T.scim, sv[k], T.sbeta), ti);
         }
         num = fma(tr, tr, ti * ti);
-        den = any ? (pre3 * d[3]) * sig : pre3 * d[3];  // D'; the kernel squares at the unit end
+        den = any ? (pre[K - 1] * d[K - 1]) * sig : pre[K - 1] * d[K - 1];  // D'; the kernel squares at the unit end
     }
 
     __device__ static __forceinline__ double2 prob2r(const NllArgs& A, const double2 (&x)[2], bool& okx,
