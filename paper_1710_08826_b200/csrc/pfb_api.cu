@@ -101,6 +101,7 @@ static constexpr int64_t kDlChunk = 1 << 20;  // doubles per lane staging buffer
 struct pfb_ctx {
     int device = 0;
     int sm_count = 148;
+    int clock_khz = 1965000;  // SM clock for the bounded peer waits (queried once)
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
@@ -272,6 +273,7 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
     auto* c = new pfb_ctx();
     c->device = device;
     CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device));
     {
         // keep freed pool memory for reuse by later stores (see pfb_store_create)
         cudaMemPool_t pool;
@@ -2311,8 +2313,7 @@ int pfb_nll_peer(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t be
     auto A = std::make_unique<NllArgs>();
     pack_args(p, st, begin, end, values, norms, A.get());
     A->mode = MODE_EXPORT;
-    int khz = 0;
-    CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device));
+    const int khz = c->clock_khz;  // a per-call attribute query would stall the queue
     for (int q = 0; q < c->peer_world; ++q) A->peer_mbox[q] = c->peer_ptr[q];
     A->peer_world = c->peer_world;
     A->peer_rank = c->peer_rank;
@@ -2335,8 +2336,7 @@ int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {
     for (int q = 0; q < c->peer_world; ++q)
         if (!c->peer_ptr[q]) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
-    int khz = 0;
-    CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, c->device));
+    const int khz = c->clock_khz;  // a per-call attribute query would stall the queue
     const long long cycles = (long long)(timeout_s * (double)khz * 1e3);
     const unsigned long long seq = ++c->peer_seq;
     CK(launch_peer_allreduce(c->peer_ptr, c->peer_world, c->peer_rank, seq, cycles,

@@ -824,8 +824,13 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* t) {
 // peer timeout.  Parity alternation: a rank can be at most one call ahead
 // (it cannot pass call s+1's wait before every rank has posted s+1, i.e.
 // finished reading call s), so it never overwrites a slot still being read.
+#ifndef PFB_PEER_ON
+#define PFB_PEER_ON 1
+#endif
 __device__ __forceinline__ void peer_finish(const NllArgs& A) {
     __shared__ long long s_loc[PFB_ACC_WORDS + 1];
+    __shared__ long long s_fx;
+    __shared__ unsigned long long s_ek;
     __shared__ int s_timeout;
     const int t = threadIdx.x;
     if (t == 0) s_timeout = 0;
@@ -833,8 +838,8 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
     if (t == PFB_ACC_WORDS) {
         const long long fx = (long long)atomicExch(A.fix_counter, 0ull);
         const unsigned long long ek = atomicExch(A.errkey, ~0ull);
-        A.result_i[0] = fx;
-        A.result_i[1] = (long long)ek;
+        s_fx = fx;
+        s_ek = ek;
         s_loc[PFB_ACC_WORDS] = (fx != 0 || ek != ~0ull) ? 1 : 0;
     }
     __syncthreads();
@@ -842,8 +847,11 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
     if (t <= PFB_ACC_WORDS) {
         const long long v = s_loc[t];
         for (int q = 0; q < A.peer_world; ++q) peer_slot(A.peer_mbox[q], par, A.peer_rank)[t] = v;
+        // this thread's slot stores are ordered before the flags raised below
+        // (no host-memory writes are pending here: the result block is
+        // written only after the exchange, so the fence does not wait on PCIe)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
     }
-    __threadfence_system();
     __syncthreads();
     if (t < A.peer_world) st_release_sys(peer_flag(A.peer_mbox[t], par, A.peer_rank), A.peer_seq);
     if (t < A.peer_world) {
@@ -858,10 +866,12 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
         }
     }
     __syncthreads();
-    if (s_timeout) {
-        if (t == 0) A.result_i[3] = 1;
-        return;
+    if (t == 0) {
+        A.result_i[0] = s_fx;
+        A.result_i[1] = (long long)s_ek;
+        A.result_i[3] = s_timeout ? 1 : 0;
     }
+    if (s_timeout) return;
     if (t <= PFB_ACC_WORDS) {
         long long sum = 0;
         for (int q = 0; q < A.peer_world; ++q) sum += peer_slot(A.peer_mbox[A.peer_rank], par, q)[t];
@@ -870,7 +880,6 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
         else
             A.result_i[2] = sum;
     }
-    if (t == 0) A.result_i[3] = 0;
 }
 
 // Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and
@@ -892,7 +901,7 @@ __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc,
         *A.ticket = 0u;
     }
     if (A.mode == MODE_ACCUM) return;
-    if (!LIST && A.peer_world > 0 && A.mode == MODE_EXPORT) {
+    if (!LIST && PFB_PEER_ON && A.peer_world > 0 && A.mode == MODE_EXPORT) {
         peer_finish(A);
         return;
     }

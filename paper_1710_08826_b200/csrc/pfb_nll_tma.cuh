@@ -107,7 +107,7 @@ __device__ __forceinline__ void finish_launch_pts(const NllArgs& A, long long* s
         *A.ticket = 0u;
     }
     if (A.mode == MODE_ACCUM) return;
-    if (A.peer_world > 0 && A.mode == MODE_EXPORT && nwords == PFB_ACC_WORDS) {
+    if (PFB_PEER_ON && A.peer_world > 0 && A.mode == MODE_EXPORT && nwords == PFB_ACC_WORDS) {
         peer_finish(A);
         return;
     }

@@ -18,6 +18,7 @@ from paper_1710_08826_b200 import _lib as L, mcgen
 from tests import models
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
 cfg = sys.argv[2] if len(sys.argv) > 2 else "c2"
+fused = len(sys.argv) > 3 and sys.argv[3] == "fused"
 ctx = pf.device_context(0)
 ctx.enable_timing(True)
 if cfg == "c3":
@@ -36,11 +37,18 @@ vals, nv = plan.pack(snap, norms)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 out = ctypes.c_double(); err = L.PfbErr()
 lib = L.lib()
+if fused:
+    from paper_1710_08826_b200.sharding import PeerGroup
+    PeerGroup(ctx, 0, 1)
 read = lib.pfb_debug_trace_dal if cfg == "c3" else lib.pfb_debug_trace
 read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 for rep in range(6):
     ctx.spin(1_000_000, flush.data_ptr(), flush.numel() * 4)
-    L.check(lib.pfb_nll(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err)), "nll")
+    if fused:
+        slow = ctypes.c_int32()
+        L.check(lib.pfb_nll_peer(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), 5.0, ctypes.byref(out), ctypes.byref(slow)), "nll_peer")
+    else:
+        L.check(lib.pfb_nll(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err)), "nll")
     ms = ctx.last_kernel_ms()
     tr = (ctypes.c_ulonglong * (1024 * 12))()
     read(tr, 148)
@@ -50,7 +58,7 @@ for rep in range(6):
     rel = (a - t0) / 1000.0
     rel[a == 0] = np.nan
     last = np.nanargmax(rel[:, 7]) if np.isfinite(rel[:, 7]).any() else -1
-    print(json.dumps({"cfg": cfg, "n": n, "event_us": 1e3 * ms,
+    print(json.dumps({"cfg": cfg, "fused": fused, "n": n, "event_us": 1e3 * ms,
         "entry_spread_us": float(np.nanmax(rel[:, 0])),
         "first_issue_us_med": float(np.nanmedian(rel[:, 1] - rel[:, 0])),
         "first_ready_us_med": float(np.nanmedian(rel[:, 2] - rel[:, 0])), "first_ready_us_max": float(np.nanmax(rel[:, 2])),
