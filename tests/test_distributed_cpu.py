@@ -75,3 +75,55 @@ def test_gloo_allreduce_of_exact_partials(world):
     for rank, total, first in results:
         assert total == want, rank
         assert first[:2] == (1, 1001)
+
+
+def _peer_setup_worker(rank, world, port, q):
+    """PeerGroup set-up where rank 0's mailbox creation 'succeeds' (a stand-in
+    that returns OK) and rank 1's fails (no GPU here): every rank must raise,
+    none may hang in the handle exchange."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1710_08826_b200 import _lib as L
+        from paper_1710_08826_b200 import sharding
+
+        class FakeCtx:
+            handle = None
+
+        if rank == 0:
+            class Lib:
+                def __getattr__(self, name):
+                    return getattr(L.lib(), name)
+
+                @staticmethod
+                def pfb_peer_create(h, r, w, out):
+                    return L.OK
+
+            real = L.lib
+            L.lib = lambda: Lib()
+        try:
+            sharding.PeerGroup(FakeCtx(), rank, world)
+            q.put((rank, "no error"))
+        except Exception as exc:  # noqa: BLE001
+            q.put((rank, type(exc).__name__))
+        finally:
+            if rank == 0:
+                L.lib = real
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_setup_failure_raises_on_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_setup_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results[0] == "RuntimeError"   # "failed on another rank"
+    assert results[1] != "no error"       # its own pfb_peer_create error
