@@ -812,74 +812,98 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* t) {
 }
 
 // Fused exchange (A.peer_world > 0, single point, export mode), run by every
-// thread of the CTA that finishes the launch, after the ticket: this rank's
-// 72 limbs and a status word (deferred blocks or an error on this rank) go
-// into slot [seq & 1][rank] of every rank's mailbox (NVLink P2P stores), a
-// system-scope release raises flag [seq & 1][rank] = seq in every mailbox,
-// the CTA waits (acquire, bounded) for all flags of its own mailbox and sums
-// the slots in rank order -- integer limbs, so every rank exports the
-// single-GPU accumulator bit for bit, with no separate collective launch.
+// thread of the CTA that finishes the launch, after the ticket: thread t
+// stores word t of this rank's 72 limbs (t = 72: a status word, deferred
+// blocks or an error on this rank) as a flag-in-line 16-byte line {lo, seq,
+// hi, seq} into line [seq & 1][rank][t] of every rank's mailbox (NVLink P2P
+// stores), then polls line [seq & 1][q][t] of its own mailbox for every rank
+// q until both halves carry seq (bounded) and sums in rank order -- integer
+// limbs, so every rank exports the single-GPU accumulator bit for bit, with no
+// separate collective launch and no system-scope fence on the critical path.
 // result_i[2] = number of ranks that need the slow path (deferred blocks or
 // an error: the host then redoes the call unfused), result_i[3] = 1 on a
 // peer timeout.  Parity alternation: a rank can be at most one call ahead
 // (it cannot pass call s+1's wait before every rank has posted s+1, i.e.
 // finished reading call s), so it never overwrites a slot still being read.
+#ifdef PFB_TRACE
+// Per-CTA timeline of the TMA unit kernel (debug builds only): %globaltimer ns
+// at [0] entry, [1] first copy issued, [2] first stage ready (team 0),
+// [3] team 0 done, [4] team 1 done, [5] finish entry, [6] ticket taken,
+// [7] export done (last CTA only).
+__device__ unsigned long long g_trace[1024][16];  // [8..9] ns waited for data per team, [10..11] blocks per team, [12..15] fused-exchange phases (last CTA)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PFB_T(slot) g_trace[blockIdx.x][slot] = gtimer()
+#else
+#define PFB_T(slot) ((void)0)
+#endif
+
 #ifndef PFB_PEER_ON
 #define PFB_PEER_ON 1
 #endif
 __device__ __forceinline__ void peer_finish(const NllArgs& A) {
-    __shared__ long long s_loc[PFB_ACC_WORDS + 1];
     __shared__ long long s_fx;
     __shared__ unsigned long long s_ek;
     __shared__ int s_timeout;
     const int t = threadIdx.x;
     if (t == 0) s_timeout = 0;
-    if (t < PFB_ACC_WORDS) s_loc[t] = (long long)atomicExch(A.acc + t, 0ull);
+    long long v = 0;
+    if (t < PFB_ACC_WORDS) v = (long long)atomicExch(A.acc + t, 0ull);
     if (t == PFB_ACC_WORDS) {
         const long long fx = (long long)atomicExch(A.fix_counter, 0ull);
         const unsigned long long ek = atomicExch(A.errkey, ~0ull);
         s_fx = fx;
         s_ek = ek;
-        s_loc[PFB_ACC_WORDS] = (fx != 0 || ek != ~0ull) ? 1 : 0;
+        v = (fx != 0 || ek != ~0ull) ? 1 : 0;
     }
+#ifdef PFB_TRACE
     __syncthreads();
+    if (t == 0) PFB_T(12);
+#endif
     const int par = (int)(A.peer_seq & 1ull);
+    const unsigned seq = (unsigned)A.peer_seq;
+    long long sum = 0;
     if (t <= PFB_ACC_WORDS) {
-        const long long v = s_loc[t];
-        for (int q = 0; q < A.peer_world; ++q) peer_slot(A.peer_mbox[q], par, A.peer_rank)[t] = v;
-        // this thread's slot stores are ordered before the flags raised below
-        // (no host-memory writes are pending here: the result block is
-        // written only after the exchange, so the fence does not wait on PCIe)
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-    }
-    __syncthreads();
-    if (t < A.peer_world) st_release_sys(peer_flag(A.peer_mbox[t], par, A.peer_rank), A.peer_seq);
-    if (t < A.peer_world) {
-        const unsigned long long* f = peer_flag(A.peer_mbox[A.peer_rank], par, t);
+        // word t of this rank's limbs (+ status word) to every rank's mailbox
+        for (int q = 0; q < A.peer_world; ++q) st_line(peer_line(A.peer_mbox[q], par, A.peer_rank, t), v, seq);
+        // word t of every rank, in rank order (integer: exact, bitwise the
+        // single-GPU accumulator on every rank); bounded wait per line
         const long long t0 = clock64();
-        while (ld_acquire_sys(f) != A.peer_seq) {
-            if (clock64() - t0 > A.peer_timeout) {
-                atomicExch(&s_timeout, 1);
-                break;
+        for (int q = 0; q < A.peer_world; ++q) {
+            const uint4* line = peer_line(A.peer_mbox[A.peer_rank], par, q, t);
+            long long w;
+            while (!ld_line(line, seq, &w)) {
+                if (clock64() - t0 > A.peer_timeout) {
+                    atomicExch(&s_timeout, 1);
+                    w = 0;
+                    break;
+                }
+                __nanosleep(32);
             }
-            __nanosleep(64);
+            sum += w;
         }
     }
     __syncthreads();
+#ifdef PFB_TRACE
+    if (t == 0) PFB_T(14);
+#endif
     if (t == 0) {
         A.result_i[0] = s_fx;
         A.result_i[1] = (long long)s_ek;
         A.result_i[3] = s_timeout ? 1 : 0;
     }
     if (s_timeout) return;
-    if (t <= PFB_ACC_WORDS) {
-        long long sum = 0;
-        for (int q = 0; q < A.peer_world; ++q) sum += peer_slot(A.peer_mbox[A.peer_rank], par, q)[t];
-        if (t < PFB_ACC_WORDS)
-            A.acc_out[t] = sum;
-        else
-            A.result_i[2] = sum;
-    }
+    if (t < PFB_ACC_WORDS)
+        A.acc_out[t] = sum;
+    else if (t == PFB_ACC_WORDS)
+        A.result_i[2] = sum;
+#ifdef PFB_TRACE
+    __syncthreads();
+    if (t == 0) PFB_T(15);
+#endif
 }
 
 // Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and

@@ -311,21 +311,7 @@ constexpr int kSumRing = 4;
 #define PFB_PRODUCER_WAIT mbar_wait
 #endif
 
-#ifdef PFB_TRACE
-// Per-CTA timeline of the TMA unit kernel (debug builds only): %globaltimer ns
-// at [0] entry, [1] first copy issued, [2] first stage ready (team 0),
-// [3] team 0 done, [4] team 1 done, [5] finish entry, [6] ticket taken,
-// [7] export done (last CTA only).
-__device__ unsigned long long g_trace[1024][12];  // [8..9] ns waited for data per team, [10..11] blocks per team
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define PFB_T(slot) g_trace[blockIdx.x][slot] = gtimer()
-#else
-#define PFB_T(slot) ((void)0)
-#endif
+// PFB_TRACE timeline helpers: pfb_nll_kernel.cuh
 
 template <class Ev, int S, bool PROD, int TEAMS = UnitTeams<Ev>::value>
 __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_kernel(const __grid_constant__ NllArgs A) {
@@ -1014,7 +1000,7 @@ static cudaError_t launch_unit_sum(const NllArgs& A, cudaStream_t stream, int sm
 
 #ifdef PFB_TRACE
 inline cudaError_t read_trace(unsigned long long* host, int nblocks) {
-    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 12 * nblocks);
+    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 16 * nblocks);
 }
 #endif
 

@@ -50,9 +50,9 @@ for rep in range(6):
     else:
         L.check(lib.pfb_nll(ctx.handle, plan.handle, st, 0, n, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv), ctypes.byref(out), ctypes.byref(err)), "nll")
     ms = ctx.last_kernel_ms()
-    tr = (ctypes.c_ulonglong * (1024 * 12))()
+    tr = (ctypes.c_ulonglong * (1024 * 16))()
     read(tr, 148)
-    full = np.frombuffer(tr, dtype=np.uint64).reshape(1024, 12)[:148].astype(np.int64)
+    full = np.frombuffer(tr, dtype=np.uint64).reshape(1024, 16)[:148].astype(np.int64)
     a = full[:, :8]
     t0 = a[:, 0].min()
     rel = (a - t0) / 1000.0
@@ -67,4 +67,9 @@ for rep in range(6):
         "finish_entry_max": float(np.nanmax(rel[:, 5])), "ticket_max_nonlast": float(np.nanmax(rel[:, 6])),
         "export_done": float(rel[last, 7]) if last >= 0 else None,
         "steady_wait_us_per_team_med": float(np.median(full[:, 8:10]) / 1000.0),
-        "blocks_per_team_med": float(np.median(full[:, 10:12]))}), flush=True)
+        "blocks_per_team_med": float(np.median(full[:, 10:12])),
+        # fused exchange, last CTA: finish entry -> limbs read, -> all ranks' lines summed, -> exported
+        "fused_phases_us": [float((full[last, 12] - full[last, 5]) / 1000.0),
+                            float((full[last, 14] - full[last, 12]) / 1000.0),
+                            float((full[last, 15] - full[last, 14]) / 1000.0)] if fused and last >= 0 else None}),
+        flush=True)

@@ -23,6 +23,29 @@ def flag_word(par, r):
     return 2 * PEERS * SLOT + par * PEERS + r
 
 
+LINE_BASE = 2 * PEERS * SLOT + 2 * PEERS      # flag-in-line region of the fused exchange
+MBOX_WORDS = LINE_BASE + 2 * 2 * PEERS * SLOT  # whole mailbox, 64-bit words
+
+
+def line_word(par, r, w):
+    return LINE_BASE + 2 * ((par * PEERS + r) * SLOT + w)
+
+
+def put_line(host, par, r, w, value, seq):
+    u = int(value) & ((1 << 64) - 1)
+    lo, hi = u & 0xFFFFFFFF, u >> 32
+    host[line_word(par, r, w)] = np.int64(np.uint64((seq << 32) | lo).astype(np.int64))
+    host[line_word(par, r, w) + 1] = np.int64(np.uint64((seq << 32) | hi).astype(np.int64))
+
+
+def get_line(arr, par, r, w):
+    a = int(np.uint64(arr[line_word(par, r, w)].astype(np.uint64)))
+    b = int(np.uint64(arr[line_word(par, r, w) + 1].astype(np.uint64)))
+    seq1, seq2 = a >> 32, b >> 32
+    v = ((b & 0xFFFFFFFF) << 32) | (a & 0xFFFFFFFF)
+    return np.int64(np.uint64(v).astype(np.int64)), seq1, seq2
+
+
 @pytest.fixture(scope="module")
 def pf():
     import paper_1710_08826_b200 as pf
@@ -69,7 +92,7 @@ def test_protocol_with_preposted_peer(pf):
     h = raw_ctx()
     try:
         L.check(L.lib().pfb_peer_create(h, 0, 2, None), "pfb_peer_create")
-        other = torch.zeros(2 * PEERS * SLOT + 2 * PEERS, dtype=torch.int64, device="cuda")
+        other = torch.zeros(MBOX_WORDS, dtype=torch.int64, device="cuda")
         ptrs = (ctypes.c_void_p * 2)(None, ctypes.c_void_p(other.data_ptr()))
         L.check(L.lib().pfb_peer_attach(h, ptrs), "pfb_peer_attach")
         mb = ctypes.c_void_p()
@@ -77,7 +100,7 @@ def test_protocol_with_preposted_peer(pf):
         mine = np.arange(72, dtype=np.int64) * 3 - 50
         theirs = np.arange(72, dtype=np.int64) * -7 + (1 << 40)
         # rank 1 has already posted call 1 (parity 1) into rank 0's mailbox
-        nwords = 2 * PEERS * SLOT + 2 * PEERS
+        nwords = MBOX_WORDS
         host = np.zeros(nwords, dtype=np.int64)
         host[slot_word(1, 1):slot_word(1, 1) + 72] = theirs
         host[flag_word(1, 1)] = 1
@@ -105,7 +128,7 @@ def test_missing_peer_times_out(pf):
     h = raw_ctx()
     try:
         L.check(L.lib().pfb_peer_create(h, 0, 2, None), "pfb_peer_create")
-        other = torch.zeros(2 * PEERS * SLOT + 2 * PEERS, dtype=torch.int64, device="cuda")
+        other = torch.zeros(MBOX_WORDS, dtype=torch.int64, device="cuda")
         ptrs = (ctypes.c_void_p * 2)(None, ctypes.c_void_p(other.data_ptr()))
         L.check(L.lib().pfb_peer_attach(h, ptrs), "pfb_peer_attach")
         acc = torch.ones(72, dtype=torch.int64, device="cuda")
@@ -168,16 +191,16 @@ def test_fused_with_preposted_peer(pf):
         theirs = acc1.cpu().numpy()
         # wire rank 0 to a stand-in mailbox for rank 1 and pre-post rank 1's call 1
         L.check(L.lib().pfb_peer_create(ctx.handle, 0, 2, None), "pfb_peer_create")
-        other = torch.zeros(2 * PEERS * SLOT + 2 * PEERS, dtype=torch.int64, device="cuda")
+        other = torch.zeros(MBOX_WORDS, dtype=torch.int64, device="cuda")
         ptrs = (ctypes.c_void_p * 2)(None, ctypes.c_void_p(other.data_ptr()))
         L.check(L.lib().pfb_peer_attach(ctx.handle, ptrs), "pfb_peer_attach")
         mb = ctypes.c_void_p()
         L.check(L.lib().pfb_peer_mailbox(ctx.handle, ctypes.byref(mb)), "pfb_peer_mailbox")
-        nwords = 2 * PEERS * SLOT + 2 * PEERS
+        nwords = MBOX_WORDS
         host = np.zeros(nwords, dtype=np.int64)
-        host[slot_word(1, 1):slot_word(1, 1) + 72] = theirs
-        host[slot_word(1, 1) + 72] = 0  # rank 1: no deferred blocks, no error
-        host[flag_word(1, 1)] = 1
+        for w in range(72):
+            put_line(host, 1, 1, w, theirs[w], 1)
+        put_line(host, 1, 1, 72, 0, 1)  # rank 1: no deferred blocks, no error
         box = torch.from_numpy(host).cuda()
         torch.cuda.synchronize()
         _copy_d2d(mb.value, box.data_ptr(), nwords * 8)
@@ -188,9 +211,11 @@ def test_fused_with_preposted_peer(pf):
         assert code == L.OK and slow.value == 0
         assert out.value == whole
         o = other.cpu().numpy()
-        mine = o[slot_word(1, 0):slot_word(1, 0) + 72]
+        lines = [get_line(o, 1, 0, w) for w in range(73)]
+        assert all(s1 == 1 and s2 == 1 for _, s1, s2 in lines)
+        mine = np.array([v for v, _, _ in lines[:72]], dtype=np.int64)
         assert sharding.round_acc(mine + theirs) == whole
-        assert o[slot_word(1, 0) + 72] == 0 and o[flag_word(1, 0)] == 1
+        assert lines[72][0] == 0
         # a peer that never posts call 2: bounded wait, no hung GPU
         code = L.lib().pfb_nll_peer(ctx.handle, plan.handle, st0, 0, b[1], 0, L.dptr(vals), len(vals), L.dptr(nv),
                                     len(nv), 0.01, ctypes.byref(out), ctypes.byref(slow))
