@@ -244,3 +244,32 @@ def test_fused_slow_path_reports_the_reference_error(pf):
     with pytest.raises(E.NonPositiveDensity) as got:
         sn(snap, norms)
     assert got.value.index == ref.value.index == 4321
+
+
+@pytest.mark.parametrize("cfg,n", [("c1", 4096 * 40 + 3), ("c1", 2_000_001), ("c2", 6_000_123), ("c3", 300_007)])
+def test_fused_single_rank_every_kernel_family(pf, cfg, n):
+    """The fused epilogue sits in both finish paths (finish_launch: bulk /
+    SIMT kernels; finish_launch_pts: TMA unit kernels): world = 1 equals the
+    plain NLL bit for bit for each family, ragged sizes included."""
+    from paper_1710_08826_b200 import mcgen
+    from paper_1710_08826_b200.sharding import ShardedNll
+
+    if cfg == "c1":
+        x, pdf, _ = models.c1()
+        col = mcgen.device_sumpdf_1d(n, 5.0, 0.5, -0.3, 0.3, 0.0, 10.0, 31)
+        ds = pf.UnbinnedDataSet.from_columns([x], [col], copy=False)
+    elif cfg == "c2":
+        (x, y), pdf, _ = models.c2()
+        cx, cy = mcgen.device_prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, 32)
+        ds = pf.UnbinnedDataSet.from_columns([x, y], [cx, cy], copy=False)
+    else:
+        terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
+        a, b = mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 33)
+        (o12, o13), pdf, _ = models.c3()
+        ds = pf.UnbinnedDataSet.from_columns([o12, o13], [a, b], copy=False)
+    ref = pf.nll(pdf, ds)
+    sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
+    snap = pf.snapshot(pdf.param_closure())
+    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    for _ in range(3):
+        assert sn(snap, norms) == ref
