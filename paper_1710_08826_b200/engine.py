@@ -269,8 +269,8 @@ def _evaluate(ctx: DeviceContext, pdf, arrays, names, snap, norms, begin, end, i
         raise_for(err, code, pdf, "pfb_nll_block_sums")
         return out
     total = ctypes.c_double()
-    code = L.lib().pfb_nll(ctx.handle, plan.handle, st, begin, end, index_offset, L.dptr(vals), len(vals),
-                           L.dptr(nv), len(nv), ctypes.byref(total), ctypes.byref(err))
+    code = L.lib().pfb_nll(ctx.handle, plan.handle, st, begin, end, index_offset, plan.values_ptr, len(vals),
+                           plan.norms_ptr, len(nv), ctypes.byref(total), ctypes.byref(err))
     raise_for(err, code, pdf, "pfb_nll")
     return total.value
 
