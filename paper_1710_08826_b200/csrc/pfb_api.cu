@@ -1,5 +1,6 @@
 // pfb_api.cu -- C ABI: contexts, device event stores, plan compilation,
 // per-call argument packing, error decoding and the Dalitz grid object.
+#include <atomic>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -27,6 +28,8 @@ cudaError_t launch_bin_fill(const BinAxes& B, int64_t begin, int64_t n, unsigned
                             cudaStream_t stream, int sm_count);
 cudaError_t launch_binned_nll(const NllArgs& A, const double* contents, int64_t nbins, double total,
                               double volume, unsigned long long* expkey, cudaStream_t stream, int sm_count);
+cudaError_t launch_quadrature(const NllArgs& A, const double* weights, int64_t n, cudaStream_t stream,
+                              int sm_count);
 cudaError_t launch_binned_probe(const NllArgs& A, int64_t b, double total, double volume, double* out,
                                 cudaStream_t stream);
 cudaError_t launch_fp64_peak(double* out, int blocks, int threads, int iters, cudaStream_t stream);
@@ -163,7 +166,15 @@ struct pfb_store {
     double* cols[kStoreMaxCols] = {};
     bool owned = false;
     bool pooled = false;  // columns from the device's stream-ordered pool
+    // content generation: a fresh process-wide number whenever the columns
+    // may have changed (create, upload, load, generate, writable pointer
+    // handed out).  Caches of per-event data (the Dalitz lineshape cache)
+    // key on it, never on the store's address, which the allocator recycles.
+    uint64_t gen = 0;
 };
+
+static std::atomic<uint64_t> g_store_gen{0};
+static inline void store_touched(pfb_store* s) { s->gen = ++g_store_gen; }
 
 struct TermFactor {
     int type;  // 0: weight (node, child index), 1: 1/norm(node)
@@ -198,7 +209,7 @@ struct pfb_plan {
     int lineshape_mode = 0;
     double2* cache = nullptr;
     int64_t cache_cap = 0;
-    const pfb_store* cache_store = nullptr;
+    uint64_t cache_gen = 0;  // pfb_store::gen the cache was computed from (0: none)
     int64_t cache_begin = -1, cache_end = -1;
     bool cache_valid[kMaxDal] = {};
     double cache_mw[kMaxDal][2] = {};
@@ -425,6 +436,7 @@ int pfb_store_create(pfb_ctx* c, int32_t ncols, int64_t n, pfb_store** out) {
     }
     // usable from any stream once this returns
     CK(cudaStreamSynchronize(c->stream));
+    store_touched(s);
     *out = s;
     return PFB_OK;
 }
@@ -436,6 +448,7 @@ int pfb_store_upload(pfb_store* s, int32_t col, const double* host, int64_t offs
     // a single pageable copy: the source pages are already resident, and the
     // driver's own staging (~10 GB/s measured) beats host_copy's lanes here
     CK(cudaSetDevice(s->ctx->device));
+    store_touched(s);
     CK(cudaMemcpyAsync(s->cols[col] + offset, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                        s->ctx->stream));
     CK(cudaStreamSynchronize(s->ctx->stream));
@@ -452,12 +465,14 @@ int pfb_store_wrap(pfb_ctx* c, int32_t ncols, int64_t n, const double* const* de
     s->n = n;
     s->owned = false;
     for (int i = 0; i < ncols; ++i) s->cols[i] = const_cast<double*>(dev_cols[i]);
+    store_touched(s);
     *out = s;
     return PFB_OK;
 }
 
 int pfb_store_device_ptr(pfb_store* s, int32_t col, void** out) {
     if (!s || !out || col < 0 || col >= s->ncols) return PFB_E_INVALID_ARGUMENT;
+    store_touched(s);  // the caller may write through the pointer
     *out = s->cols[col];
     return PFB_OK;
 }
@@ -958,6 +973,7 @@ static int restage(pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int64_t b
     }
     tmp->ctx = c;
     tmp->owned = false;
+    store_touched(tmp);  // staging holds a different range every call
     tmp->n = n;
     tmp->ncols = st->ncols;
     for (int i = 0; i < kStoreMaxCols; ++i) tmp->cols[i] = nullptr;
@@ -977,7 +993,7 @@ static int ensure_cache(pfb_plan* p, const pfb_store* st, int64_t begin, int64_t
     pfb_ctx* c = p->ctx;
     const int K = A->dal.K;
     const int64_t n = end - begin;
-    if (p->cache_store != st || p->cache_begin != begin || p->cache_end != end) {
+    if (p->cache_gen != st->gen || p->cache_begin != begin || p->cache_end != end) {
         if (p->cache_cap < (int64_t)K * n) {
             if (p->cache) cudaFree(p->cache);
             p->cache = nullptr;
@@ -985,7 +1001,7 @@ static int ensure_cache(pfb_plan* p, const pfb_store* st, int64_t begin, int64_t
             CK(cudaMalloc(&p->cache, sizeof(double2) * (size_t)K * (size_t)(n > 0 ? n : 1)));
             p->cache_cap = (int64_t)K * n;
         }
-        p->cache_store = st;
+        p->cache_gen = st->gen;
         p->cache_begin = begin;
         p->cache_end = end;
         for (int k = 0; k < kMaxDal; ++k) p->cache_valid[k] = false;
@@ -1223,7 +1239,8 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
         end -= begin;
         begin = 0;
     }
-    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
+    // the batched kernels list one deferred entry per (block, point) pair
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock * npts);
     if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
     int frac0 = pack_args(p, st, begin, end, values, norms, A.get());
@@ -1329,8 +1346,16 @@ int pfb_finalize(pfb_ctx* c, const int64_t* dev_acc, double* out_nll, int64_t* o
     double r = 0.0;
     const int st = acc_round(h, &r);
     if (out_nll) *out_nll = r;
-    if (out_fails) *out_fails = (int64_t)h[PFB_ACC_FAILS];
+    // failed events/blocks of every rank, plus this call's fraction check
+    // (host-side, so it never reaches the accumulator)
+    if (out_fails) *out_fails = (int64_t)h[PFB_ACC_FAILS] + (c->last_frac_rank >= 0 ? 1 : 0);
     return st;
+}
+
+int pfb_ctx_last_fraction_failure(pfb_ctx* c, int32_t* out) {
+    if (!c || !out) return PFB_E_INVALID_ARGUMENT;
+    *out = (c->last_args && c->last_frac_rank >= 0) ? 1 : 0;
+    return PFB_OK;
 }
 
 int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
@@ -1734,6 +1759,7 @@ int pfb_gen_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term_valu
     G.envelope = envelope;
     G.seed_lo = (uint32_t)seed;
     G.seed_hi = (uint32_t)(seed >> 32);
+    store_touched(out);
     if (n == 0) return PFB_OK;
     CK(run_gen_dalitz(G, n, out->cols[0], out->cols[1], c->stream, c->sm_count, candidates));
     c->launches += 3;
@@ -1757,6 +1783,7 @@ int pfb_gen_1d(pfb_ctx* c, int32_t kind, double mu, double sigma, double alpha, 
     G.hi = hi;
     G.seed_lo = (uint32_t)seed;
     G.seed_hi = (uint32_t)(seed >> 32);
+    store_touched(out);
     if (n == 0) return PFB_OK;
     CK(launch_gen_1d(G, n, out->cols[0], kind == 1 ? out->cols[1] : nullptr, c->stream, c->sm_count));
     ++c->launches;
@@ -1927,6 +1954,35 @@ int pfb_bin_fill(pfb_ctx* c, const pfb_store* st, int64_t begin, int64_t end, in
     return PFB_OK;
 }
 
+int pfb_quadrature(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int32_t weight_col, const double* values,
+                   int32_t nvalues, const double* norms, int32_t nnorms, double* out, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || !out || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (weight_col < 0 || weight_col >= st->ncols || st->n < 1) return PFB_E_INVALID_ARGUMENT;
+    for (int s = 0; s < p->nslots; ++s)
+        if (p->slot_col[s] >= st->ncols || p->slot_col[s] == weight_col) return PFB_E_INVALID_ARGUMENT;
+    clear_err(out_err);
+    CK(cudaSetDevice(c->device));
+    auto A = std::make_unique<NllArgs>();
+    const int frac = pack_args(p, st, 0, st->n, values, norms, A.get());
+    if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
+    CK(launch_quadrature(*A, st->cols[weight_col], st->n, c->stream, c->sm_count));
+    ++c->launches;
+    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
+    int rc = read_result(c);
+    if (rc) return rc;
+    pfb_err e;
+    int code = decode_error(c, p, *A, (unsigned long long)c->res_host[1], frac, 0, &e);
+    double r = 0.0;
+    if (!code) code = acc_round(c->res_host + kResHead, &r);
+    e.code = code;
+    *out = r;
+    if (out_err) *out_err = e;
+    return code;
+}
+
 int pfb_binned_nll(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, const double* contents, int64_t nbins,
                    double total, double volume, const double* values, int32_t nvalues, const double* norms,
                    int32_t nnorms, double* out_nll, pfb_err* out_err) {
@@ -2076,6 +2132,7 @@ int pfb_pcg_generate_1d(pfb_ctx* c, const pfb_plan* p, const double* values, int
     int rc = pack_density_args(c, p, values, nvalues, norms, nnorms, A.get());
     if (rc) return rc;
     const double box[4] = {lo, hi - lo, 0.0, 0.0};
+    store_touched(out);
     PcgHostResult R;
     CK(pcg_generate_entry(*A, 0, box, envelope, nullptr, stream->state_hi, stream->state_lo, stream->inc_hi,
                           stream->inc_lo, n_wanted, budget, out->cols[0] + out_offset, nullptr, c->stream, &R));
@@ -2100,6 +2157,7 @@ int pfb_pcg_generate_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* 
     const double hi13 = b13 * b13;
     // uniform(lo, hi): scale = hi - lo as numpy computes it
     const double box[4] = {g.lo12, g.hi12 - g.lo12, g.lo13, hi13 - g.lo13};
+    store_touched(out);
     PcgHostResult R;
     CK(pcg_generate_entry(*A, 1, box, envelope, &g, stream->state_hi, stream->state_lo, stream->inc_hi,
                           stream->inc_lo, n_wanted, budget, out->cols[0] + out_offset, out->cols[1] + out_offset,
@@ -2130,6 +2188,7 @@ int pfb_store_load_npy(pfb_store* st, int32_t col, const char* path, int64_t src
         dst_offset + count > st->n)
         return PFB_E_INVALID_ARGUMENT;
     pfb_ctx* c = st->ctx;
+    store_touched(st);
     const int fd = open(path, O_RDONLY);
     if (fd < 0) return PFB_E_INVALID_ARGUMENT;
     std::unique_ptr<int, void (*)(int*)> fd_guard(new int(fd), [](int* f) {
@@ -2311,7 +2370,13 @@ int pfb_nll_peer(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t be
     int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
     if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
-    pack_args(p, st, begin, end, values, norms, A.get());
+    if (pack_args(p, st, begin, end, values, norms, A.get()) >= 0) {
+        // FractionOutOfRange (pdf.py:205-210) is a property of the parameter
+        // point, the same on every rank: no rank launches, every rank takes
+        // the unfused path, which reports it in reference evaluation order
+        *out_slow = 1;
+        return PFB_OK;
+    }
     A->mode = MODE_EXPORT;
     const int khz = c->clock_khz;  // a per-call attribute query would stall the queue
     for (int q = 0; q < c->peer_world; ++q) A->peer_mbox[q] = c->peer_ptr[q];

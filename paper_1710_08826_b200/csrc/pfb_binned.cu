@@ -67,6 +67,32 @@ __global__ void __launch_bounds__(kThreads) binned_nll_kernel(const __grid_const
     finish_launch<false>(A, sacc, &s_last);
 }
 
+// Normalisation integral by quadrature (north_star item 4): sum_j w_j * f(x_j)
+// over the abscissas of a store (one column per observable), f = the plan's
+// literal density with the root norm set to 1 (pdf._polynomial_norm,
+// pdf.py:192-199, or any subtree over a tensor grid).  Each product is
+// rounded once and the sum is exact (accumulator), i.e. the correctly
+// rounded dot product.  Node-kernel errors are keyed by abscissa index as the
+// reference's kernel on the abscissa array reports them.
+__global__ void __launch_bounds__(kThreads) quadrature_kernel(const __grid_constant__ NllArgs A,
+                                                               const double* weights, int64_t n) {
+    __shared__ long long sacc[PFB_ACC_WORDS];
+    __shared__ unsigned int s_last;
+    for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
+    __syncthreads();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int rank = -1;
+        double val = 0.0;
+        const double f = literal_density(A, A.begin + j, &rank, &val);
+        if (rank >= 0) {
+            record_failure(A, rank, j, sacc);
+            continue;
+        }
+        acc_add_shared(sacc, Mul(weights[j], f));
+    }
+    finish_launch<false>(A, sacc, &s_last);
+}
+
 // nu of one bin (the NonPositiveExpectation value).
 __global__ void binned_probe_kernel(const __grid_constant__ NllArgs A, int64_t b, double total, double volume,
                                     double* out) {
@@ -91,6 +117,15 @@ cudaError_t launch_binned_nll(const NllArgs& A, const double* contents, int64_t 
     if (grid > (int64_t)sm_count * 2) grid = (int64_t)sm_count * 2;
     if (grid < 1) grid = 1;
     binned_nll_kernel<<<(unsigned)grid, kThreads, 0, stream>>>(A, contents, nbins, total, volume, expkey);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quadrature(const NllArgs& A, const double* weights, int64_t n, cudaStream_t stream,
+                              int sm_count) {
+    int64_t grid = (n + kThreads - 1) / kThreads;
+    if (grid > (int64_t)sm_count * 2) grid = (int64_t)sm_count * 2;
+    if (grid < 1) grid = 1;
+    quadrature_kernel<<<(unsigned)grid, kThreads, 0, stream>>>(A, weights, n);
     return cudaGetLastError();
 }
 

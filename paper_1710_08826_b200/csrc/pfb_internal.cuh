@@ -157,31 +157,31 @@ struct NllArgs {
 // Peer mailbox layout (64-bit words): data [2][kMaxPeers][kPeerSlotWords],
 // flags [2][kMaxPeers] (the separate exchange kernel), then the fused
 // exchange's flag-in-line region [2][kMaxPeers][kPeerSlotWords] 16-byte lines
-// {lo32, seq, hi32, seq}; parity = call sequence number & 1.
+// {(seq << 32) | lo32, (seq << 32) | hi32}; parity = call sequence number & 1.
 constexpr size_t kPeerLineBase = 2 * kMaxPeers * kPeerSlotWords + 2 * kMaxPeers;  // in 64-bit words
 __host__ __device__ constexpr size_t peer_mbox_words() {
     return kPeerLineBase + 2 * 2 * kMaxPeers * kPeerSlotWords;
 }
-__device__ __forceinline__ uint4* peer_line(long long* m, int par, int r, int w) {
-    return reinterpret_cast<uint4*>(m + kPeerLineBase) + ((size_t)par * kMaxPeers + r) * kPeerSlotWords + w;
+__device__ __forceinline__ ulonglong2* peer_line(long long* m, int par, int r, int w) {
+    return reinterpret_cast<ulonglong2*>(m + kPeerLineBase) + ((size_t)par * kMaxPeers + r) * kPeerSlotWords + w;
 }
-// One limb with its call number in both 8-byte halves: a reader that sees
-// seq in both halves has the whole value (8-byte stores are single-copy
-// atomic), so no fence or separate flag orders data before a flag.
-__device__ __forceinline__ void st_line(uint4* p, long long v, unsigned seq) {
+// One limb split into two 64-bit elements, each carrying the call number in
+// its high half.  A vector access is a set of element accesses in no
+// particular order, but each 64-bit element is single-copy atomic: a reader
+// that sees seq in both elements has both halves of this call's value, so no
+// fence or separate flag orders data before a flag.
+__device__ __forceinline__ void st_line(ulonglong2* p, long long v, unsigned seq) {
     const unsigned long long u = (unsigned long long)v;
-    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)u), "r"(seq),
-                 "r"((unsigned)(u >> 32)), "r"(seq)
+    const unsigned long long tag = (unsigned long long)seq << 32;
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(tag | (u & 0xffffffffull)),
+                 "l"(tag | (u >> 32))
                  : "memory");
 }
-__device__ __forceinline__ bool ld_line(const uint4* p, unsigned seq, long long* v) {
-    unsigned a, f1, b, f2;
-    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(a), "=r"(f1), "=r"(b), "=r"(f2)
-                 : "l"(p)
-                 : "memory");
-    if (f1 != seq || f2 != seq) return false;
-    *v = (long long)(((unsigned long long)b << 32) | a);
+__device__ __forceinline__ bool ld_line(const ulonglong2* p, unsigned seq, long long* v) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    if ((unsigned)(a >> 32) != seq || (unsigned)(b >> 32) != seq) return false;
+    *v = (long long)(((b & 0xffffffffull) << 32) | (a & 0xffffffffull));
     return true;
 }
 __device__ __forceinline__ long long* peer_slot(long long* m, int par, int r) {

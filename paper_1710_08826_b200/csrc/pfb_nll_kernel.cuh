@@ -873,7 +873,7 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
         // single-GPU accumulator on every rank); bounded wait per line
         const long long t0 = clock64();
         for (int q = 0; q < A.peer_world; ++q) {
-            const uint4* line = peer_line(A.peer_mbox[A.peer_rank], par, q, t);
+            const ulonglong2* line = peer_line(A.peer_mbox[A.peer_rank], par, q, t);
             long long w;
             while (!ld_line(line, seq, &w)) {
                 if (clock64() - t0 > A.peer_timeout) {

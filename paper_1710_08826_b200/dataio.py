@@ -20,7 +20,10 @@ from typing import Mapping, Sequence
 import numpy as np
 
 from . import _lib as L
-from .errors import OutOfRange, ShapeMismatch
+from ._reference import errors as _E
+from .datasets import DeviceDataSet
+
+OutOfRange, ShapeMismatch = _E.OutOfRange, _E.ShapeMismatch
 
 
 def save_npy(ds, directory: str) -> dict[str, str]:
@@ -57,8 +60,7 @@ def _paths_for(observables, paths) -> list[str]:
 def load_npy(observables: Sequence, paths, begin: int = 0, end: int | None = None, device: int = 0,
              check: bool = True):
     """Rows [begin, end) of the observables' column files as an
-    UnbinnedDataSet whose device copy is already in HBM."""
-    from .core import UnbinnedDataSet
+    DeviceDataSet whose device copy is already in HBM."""
     from .engine import device_context
     from .mcgen import _device_store
 
@@ -73,9 +75,8 @@ def load_npy(observables: Sequence, paths, begin: int = 0, end: int | None = Non
     if not 0 <= begin <= end <= total:
         raise ValueError(f"rows [{begin}, {end}) outside [0, {total})")
     n = end - begin
-    ds = UnbinnedDataSet(observables)
     if n == 0:
-        return ds
+        return DeviceDataSet.from_columns(observables, [np.empty(0) for _ in files], device=None)
     ctx = device_context(device)
     st = _device_store(ctx, len(files), n)
     try:
@@ -93,15 +94,13 @@ def load_npy(observables: Sequence, paths, begin: int = 0, end: int | None = Non
         L.lib().pfb_store_destroy(st)
         raise
     cols = [np.load(p, mmap_mode="r")[begin:end] for p in files]
-    ctx.adopt(cols, st)
-    ds._cols = cols
-    return ds
+    return DeviceDataSet.adopt_store(observables, cols, ctx, st)
 
 
 def load_npy_shard(observables: Sequence, paths, rank: int, world: int, device: int = 0, check: bool = True):
     """This rank's shard (reference shard() bounds, sharding.py:80-85) of the
     column files -- each GPU reads only its own rows."""
-    from .sharding import shard_bounds
+    from .engine import shard_bounds
 
     files = _paths_for(list(observables), paths)
     b = shard_bounds(npy_length(files[0]), world)

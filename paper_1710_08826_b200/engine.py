@@ -1,114 +1,34 @@
-"""Device engine: contexts, HBM event stores, the NLL entry point and the
-reference-compatible backend.
+"""Device engine: CUDA contexts, HBM event stores and the reference-facing
+``Backend``.
 
-The reference's ``nll`` (engine.py:214-243) resolves norms on the host, then
-maps ``nll_block_sums`` over block-aligned chunks and combines the block sums
-with ``math.fsum``.  Here the whole map + reduce is one fused kernel launch
-(libpfb200.so) over a device-resident copy of the columns:
+The reference's ``nll`` (P/engine.py:214-243) resolves norms through its own
+cache, then maps ``nll_block_sums`` over ``backend.chunk_ranges`` and combines
+the block sums with ``math.fsum``.  :class:`DeviceBackend` answers that
+protocol (``block``, ``chunk_ranges``, ``map``; P/engine.py:229,235-239) with
+ONE fused kernel launch (libpfb200.so) over a device-resident copy of the
+columns: ``chunk_ranges`` returns one chunk and ``map`` a one-element array
+holding the exactly rounded total, so ``math.fsum([total]) == total`` and the
+unmodified reference ``nll`` / ``FitManager`` / ``eval-nll`` run on the GPU.
 
-* :class:`DeviceBackend` is a drop-in for the reference ``Backend``: it answers
-  ``chunk_ranges`` with one chunk and ``map`` with a one-element list holding
-  the exact total, so the *unmodified* reference ``nll`` (and therefore its
-  FitManager) runs on the GPU and ``math.fsum([total]) == total``.
-* :func:`nll` is this package's own entry point with the reference's
-  signature and semantics (EmptyDataSet, default snapshot, norm cache).
-
-Normalisation caching (engine.py:103-164) is mirrored verbatim: per-node
-values keyed on parameter generations, with the Dalitz hook from
-:mod:`.dalitz` computing its overlap integrals on the GPU.
+Everything above the backend -- ``Variable``, snapshots, ``PdfNode`` trees,
+the normalisation cache and its counters -- is the reference's own code
+(``paper_1710_08826_b200._reference``); only the device norm hooks in
+:mod:`.norms` plug into its ``register_cached_norm``.
 """
 
 from __future__ import annotations
 
 import ctypes
-import math
-import os
-import weakref
-from collections import defaultdict
-from typing import Callable, Mapping
+from typing import Mapping
 
 import numpy as np
 
 from . import _lib as L
-from .errors import EmptyDataSet, error_module_for
-from .pdf import NormalizationValue, normalize_value
+from ._reference import engine as ref_engine
+from ._reference import errors as ref_errors
 from .plan import Plan, layout
 
 DEFAULT_BLOCK = L.PFB_BLOCK
-
-
-# --- normalisation cache (reference engine.py:103-164) -------------------------------
-
-
-class NormalizationStore:
-    """Per-node normalisation cache keyed on parameter generations."""
-
-    def __init__(self):
-        self._entries: dict[object, tuple[tuple, object]] = {}
-        self.kernel_evals = 0
-        self.norm_computations = 0
-        self.recompute_counts: dict[int, int] = defaultdict(int)
-
-    def get(self, key):
-        return self._entries.get(key)
-
-    def put(self, key, fingerprint: tuple, payload) -> None:
-        self._entries[key] = (fingerprint, payload)
-
-    def clear(self) -> None:
-        self._entries.clear()
-
-
-CACHED_NORM_HOOKS: dict[str, Callable] = {}
-
-
-def register_cached_norm(kind: str, hook: Callable) -> None:
-    CACHED_NORM_HOOKS[kind] = hook
-
-
-def cached_norm(node, snap, store: NormalizationStore) -> NormalizationValue:
-    fp = node.fingerprint()
-    cached = store.get(node.id)
-    if cached is not None and cached[0] == fp:
-        return NormalizationValue(cached[1], fp)
-    child_norms = {c.id: cached_norm(c, snap, store).value for c in node.children}
-    hook = CACHED_NORM_HOOKS.get(node.kind)
-    if hook is not None:
-        value = float(hook(node, snap, store))
-    else:
-        value = normalize_value(node, snap, child_norms)
-        if not node.children:
-            store.kernel_evals += 1
-    store.norm_computations += 1
-    store.recompute_counts[node.id] += 1
-    store.put(node.id, fp, value)
-    return NormalizationValue(value, fp)
-
-
-def resolve_norms(root, snap, store: NormalizationStore) -> dict[int, float]:
-    """Every node's norm in post-order (reference engine.py:158-164).  Same
-    cache traffic and counters as calling cached_norm per node -- whose
-    recursion into children only ever hits the cache here, since children
-    precede their parent -- without that second pass."""
-    out: dict[int, float] = {}
-    for node in root.walk():
-        fp = node.fingerprint()
-        cached = store.get(node.id)
-        if cached is not None and cached[0] == fp:
-            out[node.id] = cached[1]
-            continue
-        hook = CACHED_NORM_HOOKS.get(node.kind)
-        if hook is not None:
-            value = float(hook(node, snap, store))
-        else:
-            value = normalize_value(node, snap, {c.id: out[c.id] for c in node.children})
-            if not node.children:
-                store.kernel_evals += 1
-        store.norm_computations += 1
-        store.recompute_counts[node.id] += 1
-        store.put(node.id, fp, value)
-        out[node.id] = NormalizationValue(value, fp).value  # positivity check as cached_norm
-    return out
 
 
 # --- device contexts ------------------------------------------------------------------
@@ -116,6 +36,8 @@ def resolve_norms(root, snap, store: NormalizationStore) -> dict[int, float]:
 
 class DeviceContext:
     """One CUDA device: a pfb_ctx plus its caches of stores, plans and grids."""
+
+    MAX_STORES = 8
 
     def __init__(self, device: int = 0):
         handle = ctypes.c_void_p()
@@ -127,7 +49,7 @@ class DeviceContext:
         self.grids: dict[tuple, object] = {}
 
     # stores: device copies of host columns, keyed by array identity (the
-    # arrays are kept alive by the cache, so ids cannot be recycled)
+    # cache holds the arrays, so an id cannot be recycled while cached)
     def store_for(self, arrays, begin: int = 0, end: int | None = None):
         n_all = len(arrays[0])
         end = n_all if end is None else end
@@ -145,8 +67,6 @@ class DeviceContext:
         self.adopt(arrays, st, begin, end)
         return st
 
-    MAX_STORES = 8
-
     def adopt(self, arrays, st, begin: int = 0, end: int | None = None) -> None:
         """Register `st` as the HBM copy of rows [begin, end) of `arrays`
         (bounded cache: the oldest store is dropped first)."""
@@ -155,6 +75,10 @@ class DeviceContext:
             old_key = next(iter(self._stores))
             L.lib().pfb_store_destroy(self._stores.pop(old_key)[0])
         self._stores[tuple(id(a) for a in arrays) + (begin, end)] = (st, tuple(arrays))
+
+    def has_store(self, arrays, begin: int = 0, end: int | None = None) -> bool:
+        end = len(arrays[0]) if end is None else end
+        return (tuple(id(a) for a in arrays) + (begin, end)) in self._stores
 
     def plan_for(self, pdf, column_names) -> Plan:
         key = (id(pdf), tuple(column_names))
@@ -219,9 +143,18 @@ _contexts: dict[int, DeviceContext] = {}
 
 
 def device_context(device: int = 0) -> DeviceContext:
+    """The process's context on `device`.  Creating the first one registers
+    the device normalisation hooks (:func:`.norms.install`) in the
+    reference's registry -- the engine is then active for every norm the
+    reference caches; ``norms.uninstall()`` / ``norms.reference_norms()``
+    restore the reference's own."""
     ctx = _contexts.get(device)
     if ctx is None:
+        from . import norms
+
         ctx = DeviceContext(device)
+        if not _contexts and not norms.installed():
+            norms.install(device)
         _contexts[device] = ctx
     return ctx
 
@@ -229,16 +162,16 @@ def device_context(device: int = 0) -> DeviceContext:
 # --- error translation ------------------------------------------------------------------
 
 
-def raise_for(err: L.PfbErr, code: int, node, where: str) -> None:
-    """Map a native status onto the reference exception the caller expects."""
+def raise_for(err: L.PfbErr, code: int, where: str) -> None:
+    """Raise the reference's own exception for a native status (P/errors.py:54-108):
+    the reference line search treats any ParafitError as +inf (P/fitting.py:339-342)."""
     if code == L.OK:
         return
-    E = error_module_for(node)
+    E = ref_errors
     if code == L.E_NONPOSITIVE_DENSITY:
         raise E.NonPositiveDensity(int(err.index), float(err.value))
     if code == L.E_NONFINITE_DENSITY:
-        kind = "density"
-        raise E.NonFiniteDensity(int(err.index), f"{kind} kernel produced a non-finite value")
+        raise E.NonFiniteDensity(int(err.index), "density kernel produced a non-finite value")
     if code == L.E_NEGATIVE_DENSITY:
         raise E.NegativeDensity(int(err.index), float(err.value))
     if code == L.E_FRACTION_OUT_OF_RANGE:
@@ -249,11 +182,14 @@ def raise_for(err: L.PfbErr, code: int, node, where: str) -> None:
         raise ValueError("-inf + inf in exact NLL sum")
     if code == L.E_NONPOSITIVE_EXPECTATION:
         raise E.NonPositiveExpectation(int(err.index), float(err.value))
+    if code == L.E_NONPOSITIVE_NORM:
+        raise E.NonPositiveNorm(f"normalization {float(err.value)!r} is not positive and finite")
     raise L.NativeError(code, where)
 
 
-def _evaluate(ctx: DeviceContext, pdf, arrays, names, snap, norms, begin, end, index_offset=0,
-              block_sums=False, lineshape_cache=0):
+def evaluate(ctx: DeviceContext, pdf, arrays, names, snap, norms, begin, end, index_offset=0,
+             block_sums=False, lineshape_cache=0):
+    """One fused NLL launch over rows [begin, end) of `arrays` (device copy cached)."""
     plan = ctx.plan_for(pdf, names)
     if lineshape_cache:
         plan.set_lineshape_cache(lineshape_cache)
@@ -266,25 +202,47 @@ def _evaluate(ctx: DeviceContext, pdf, arrays, names, snap, norms, begin, end, i
         code = L.lib().pfb_nll_block_sums(ctx.handle, plan.handle, st, begin, end, index_offset,
                                           L.dptr(vals), len(vals), L.dptr(nv), len(nv), L.dptr(out),
                                           nb, ctypes.byref(err))
-        raise_for(err, code, pdf, "pfb_nll_block_sums")
+        raise_for(err, code, "pfb_nll_block_sums")
         return out
     total = ctypes.c_double()
     code = L.lib().pfb_nll(ctx.handle, plan.handle, st, begin, end, index_offset, plan.values_ptr, len(vals),
                            plan.norms_ptr, len(nv), ctypes.byref(total), ctypes.byref(err))
-    raise_for(err, code, pdf, "pfb_nll")
+    raise_for(err, code, "pfb_nll")
     return total.value
+
+
+def shard_bounds(n: int, workers: int, block: int = DEFAULT_BLOCK) -> list[int]:
+    """[b0=0, b1, ..., bW=n]: the reference shard() integers (P/sharding.py:80-85),
+    computed by the native pfb_shard_bounds."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    out = (ctypes.c_int64 * (workers + 1))()
+    L.check(L.lib().pfb_shard_bounds(int(n), int(workers), int(block), out), "pfb_shard_bounds")
+    return list(out)
+
+
+def round_acc(acc) -> float:
+    """Correctly rounded value of a 72-word exact accumulator (== math.fsum)."""
+    a = np.ascontiguousarray(np.asarray(acc, dtype=np.int64))
+    out = ctypes.c_double()
+    code = L.lib().pfb_acc_round(a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(out))
+    if code == L.E_INVALID_SUM:
+        raise ValueError("-inf + inf in exact sum")
+    L.check(code, "pfb_acc_round")
+    return out.value
 
 
 # --- the reference-compatible backend ---------------------------------------------------
 
 
 class DeviceBackend:
-    """Duck-typed replacement for the reference ``Backend`` (engine.py:32-97).
+    """Duck-typed replacement for the reference ``Backend`` (P/engine.py:32-97).
 
-    ``devices`` lists CUDA devices to use inside this process; the event range
-    is split into block-aligned contiguous ranges, one per device, each device
-    produces its exact integer partial, and the partials are summed and
-    rounded once -- so any device count gives the single-GPU bits.
+    ``devices`` lists the CUDA devices used inside this process.  With several,
+    the event range is split at the reference ``shard()`` bounds
+    (P/sharding.py:80-85), each device produces its exact integer partial,
+    and the partials are summed and rounded once: any device count gives the
+    single-GPU bits.  (One process per GPU is :class:`.sharding.ShardedNll`.)
     """
 
     mode = "device"
@@ -310,7 +268,7 @@ class DeviceBackend:
     def close(self) -> None:
         pass
 
-    # reference protocol ------------------------------------------------------
+    # reference protocol (P/engine.py:235-239) ---------------------------------
     def chunk_ranges(self, n_events: int) -> list[tuple[int, int]]:
         return [(0, n_events)] if n_events > 0 else []
 
@@ -324,15 +282,15 @@ class DeviceBackend:
             out.append(np.array([self.evaluate(pdf, columns, snap, norms, start, stop, offset)]))
         return out
 
-    # direct API --------------------------------------------------------------
+    # direct API ---------------------------------------------------------------
     def evaluate(self, pdf, columns: Mapping[str, np.ndarray], snap, norms, start: int, stop: int,
                  index_offset: int = 0) -> float:
         names = tuple(columns.keys())
         arrays = [columns[k] for k in names]
         if len(self.contexts) == 1:
-            # NonPositiveDensity carries offset + start + i (reference engine.py:177-186)
-            return _evaluate(self.contexts[0], pdf, arrays, names, snap, norms, start, stop,
-                             index_offset + start, lineshape_cache=self.lineshape_cache)
+            # NonPositiveDensity carries offset + start + i (P/engine.py:177-186)
+            return evaluate(self.contexts[0], pdf, arrays, names, snap, norms, start, stop,
+                            index_offset + start, lineshape_cache=self.lineshape_cache)
         return self._evaluate_multi(pdf, arrays, names, snap, norms, start, stop, index_offset)
 
     MAX_BATCH = 16
@@ -364,7 +322,7 @@ class DeviceBackend:
                 raise L.NativeError(code, "pfb_nll_batch")
             for k in range(m):
                 if errs[k].code:
-                    out.append(self._try(lambda e=errs[k]: raise_for(e, e.code, pdf, "pfb_nll_batch")))
+                    out.append(self._try(lambda e=errs[k]: raise_for(e, e.code, "pfb_nll_batch")))
                 else:
                     out.append(float(res[k]))
         return out
@@ -377,26 +335,19 @@ class DeviceBackend:
             return exc
 
     def block_sums(self, pdf, columns, snap, norms, start: int, stop: int, index_offset: int = 0):
+        """Per-4096-event block sums (P/engine.py:190-202, P/reduction.py:59-75)."""
         names = tuple(columns.keys())
         arrays = [columns[k] for k in names]
-        return _evaluate(self.contexts[0], pdf, arrays, names, snap, norms, start, stop,
-                         index_offset + start, block_sums=True)
+        return evaluate(self.contexts[0], pdf, arrays, names, snap, norms, start, stop,
+                        index_offset + start, block_sums=True)
 
     def _evaluate_multi(self, pdf, arrays, names, snap, norms, start, stop, index_offset):
         import torch  # device buffers for the per-device accumulators (plumbing only)
 
-        n = stop - start
-        nblocks = -(-n // self.block)
-        k = min(len(self.contexts), max(nblocks, 1))
-        base, extra = divmod(nblocks, k)
-        parts = []
-        b0 = 0
-        for i in range(k):
-            b1 = b0 + base + (1 if i < extra else 0)
-            parts.append((start + b0 * self.block, min(start + b1 * self.block, stop)))
-            b0 = b1
-        accs = []
-        for ctx, (b, e) in zip(self.contexts, parts):
+        bounds = shard_bounds(stop - start, len(self.contexts), self.block)
+        launched = []
+        for i, ctx in enumerate(self.contexts):
+            b, e = start + bounds[i], start + bounds[i + 1]
             plan = ctx.plan_for(pdf, names)
             st = ctx.store_for(arrays, b, e)
             vals, nv = plan.pack(snap, norms)
@@ -404,26 +355,25 @@ class DeviceBackend:
             L.check(L.lib().pfb_nll_partial_async(ctx.handle, plan.handle, st, 0, e - b, index_offset + b,
                                                   L.dptr(vals), len(vals), L.dptr(nv), len(nv),
                                                   ctypes.c_void_p(acc.data_ptr())), "pfb_nll_partial_async")
-            accs.append((ctx, acc, b - start))
+            launched.append((ctx, acc, b - start))
         total = np.zeros(L.PFB_ACC_WORDS, dtype=np.int64)
         first_err = None
-        for ctx, acc, off in accs:
+        for ctx, acc, off in launched:  # shards in order: the first failing shard's error wins
             torch.cuda.synchronize(ctx.device)
             a = acc.cpu().numpy()
             total += a
-            if a[L.PFB_ACC_FAILS] and first_err is None:
+            frac = ctypes.c_int32()
+            L.check(L.lib().pfb_ctx_last_fraction_failure(ctx.handle, ctypes.byref(frac)),
+                    "pfb_ctx_last_fraction_failure")
+            if (a[L.PFB_ACC_FAILS] or frac.value) and first_err is None:
                 err = L.PfbErr()
                 L.check(L.lib().pfb_last_error(ctx.handle, ctypes.byref(err)), "pfb_last_error")
                 if err.code in (L.E_NONFINITE_DENSITY, L.E_NEGATIVE_DENSITY):
                     err.index += off  # chunk-local in the reference: one chunk here
                 first_err = err
         if first_err is not None:
-            raise_for(first_err, first_err.code, pdf, "pfb_nll (multi-device)")
-        out = ctypes.c_double()
-        code = L.lib().pfb_acc_round(total.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(out))
-        if code == L.E_INVALID_SUM:
-            raise ValueError("-inf + inf in exact NLL sum")
-        return out.value
+            raise_for(first_err, first_err.code, "pfb_nll (multi-device)")
+        return round_acc(total)
 
 
 _default_backend: DeviceBackend | None = None
@@ -436,71 +386,16 @@ def default_backend() -> DeviceBackend:
     return _default_backend
 
 
-def _needed_columns(pdf, ds) -> dict[str, np.ndarray]:
-    needed = {name for node in pdf.walk() for name in node.observable_names()}
-    available = ds.columns()
-    missing = needed - set(available)
-    if missing:
-        raise KeyError(f"dataset lacks observables {sorted(missing)}")
-    return {name: available[name] for name in sorted(needed)}
-
-
-def nll(pdf, ds, snap=None, backend=None, store: NormalizationStore | None = None) -> float:
-    """-sum_i ln(eval(x_i)/norm) on the GPU (reference engine.nll, engine.py:214-243)."""
-    from .core import snapshot
-
-    if ds.n_events == 0:
-        raise EmptyDataSet("cannot evaluate an NLL over zero events")
-    backend = backend or default_backend()
-    store = store if store is not None else NormalizationStore()
-    if snap is None:
-        snap = snapshot(pdf.param_closure())
-    norms = resolve_norms(pdf, snap, store)
-    columns = _needed_columns(pdf, ds)
-    if isinstance(backend, DeviceBackend):
-        return backend.evaluate(pdf, columns, snap, norms, 0, ds.n_events)
-    ranges = backend.chunk_ranges(ds.n_events)
-    chunks = backend.map(None, [(pdf, columns, snap, norms, a, b, backend.block) for a, b in ranges])
-    return math.fsum(v for c in chunks for v in np.asarray(c).tolist())
+def nll(pdf, ds, snap=None, backend=None, store=None) -> float:
+    """The reference ``nll`` (P/engine.py:214-243) with the device backend as
+    its default: norms through the reference's cache (with the device hooks
+    of :mod:`.norms`), evaluation + exact reduction on the GPU."""
+    return ref_engine.nll(pdf, ds, snap, backend or default_backend(), store)
 
 
 def nll_block_sums(pdf, columns, snap, norms, start, stop, block=DEFAULT_BLOCK, offset=0, backend=None):
-    """Per-block sums of -ln(p) (reference engine.nll_block_sums, engine.py:190-202)."""
+    """Device ``nll_block_sums`` (P/engine.py:190-202): per-block sums of -ln p."""
     backend = backend or default_backend()
     if block != DEFAULT_BLOCK:
         raise ValueError(f"the device reduction block is fixed at {DEFAULT_BLOCK}")
     return backend.block_sums(pdf, columns, snap, norms, start, stop, offset)
-
-
-def binned_nll(pdf, ds, snap=None, backend=None, store: NormalizationStore | None = None) -> float:
-    """Poisson NLL over bins, sum_b [nu_b - n_b ln nu_b] (reference engine.binned_nll,
-    engine.py:246-276): densities at the bin centres and the exact sum on the GPU
-    (pfb_binned_nll), nu_b = total * p_b * bin volume as the reference computes it."""
-    from .core import snapshot
-
-    total = ds.total
-    if total <= 0:
-        raise error_module_for(pdf).EmptyDataSet("binned dataset has no content")
-    store = store if store is not None else NormalizationStore()
-    if snap is None:
-        snap = snapshot(pdf.param_closure())
-    norms = resolve_norms(pdf, snap, store)
-    device = backend.devices[0] if isinstance(backend, DeviceBackend) else 0
-    ctx = device_context(device)
-    centers = ds.device_centers()
-    needed = sorted({name for node in pdf.walk() for name in node.observable_names()})
-    missing = set(needed) - set(centers)
-    if missing:
-        raise KeyError(f"binned dataset lacks observables {sorted(missing)}")
-    arrays = [centers[name] for name in needed]
-    plan = ctx.plan_for(pdf, tuple(needed))
-    st = ctx.store_for(arrays)
-    vals, nv = plan.pack(snap, norms)
-    contents = np.ascontiguousarray(ds.contents, dtype=np.float64)
-    out = ctypes.c_double()
-    err = L.PfbErr()
-    code = L.lib().pfb_binned_nll(ctx.handle, plan.handle, st, L.dptr(contents), contents.size, float(total),
-                                  float(ds.bin_volume()), L.dptr(vals), len(vals), L.dptr(nv), len(nv),
-                                  ctypes.byref(out), ctypes.byref(err))
-    raise_for(err, code, pdf, "pfb_binned_nll")
-    return out.value

@@ -1,9 +1,11 @@
 """Toy event generation.
 
-* generate_1d / generate_dalitz (+ GenSpec): the reference's generators
-  (mcgen.py:35-257) on the GPU, stream for stream: the same numpy PCG64
-  streams (SeedSequence spawning), the same chunked accept-reject, the same
-  envelope / rescan / budget semantics -> the same events (pfb_pcg_*).
+* generate_1d / generate_dalitz: the reference's generators (P/mcgen.py:58-257,
+  taking the reference's model nodes and ``GenSpec``) on the GPU, stream for
+  stream: the same numpy PCG64 streams (SeedSequence spawning), the same
+  chunked accept-reject, the same envelope / rescan / budget semantics -> the
+  same events (pfb_pcg_*), returned as a :class:`~.datasets.DeviceDataSet`
+  whose HBM copy is the generated store.
 * device_*: fast Philox-based samplers for benchmark inputs (pfb_gen_*).
 * sumpdf_1d / prod_2d / dalitz: host numpy samplers for small test inputs.
 """
@@ -14,6 +16,8 @@ import ctypes
 import math
 
 import numpy as np
+
+from .datasets import DeviceDataSet
 
 
 def truncated_gaussian(n: int, mu: float, sigma: float, lo: float, hi: float, rng) -> np.ndarray:
@@ -131,7 +135,9 @@ def _adopt(ctx, st, ncols: int, n: int, observables=None):
     `observables`, the dataset's strict range check (reference core.py:262-272)
     runs on the device copy first."""
     from . import _lib as L
-    from .errors import OutOfRange
+    from ._reference import errors as E
+
+    OutOfRange = E.OutOfRange
 
     if observables is not None:
         for c, obs in enumerate(observables):
@@ -216,30 +222,12 @@ RESCAN_POINTS = 4 * SCAN_POINTS
 CHUNK = 8192
 
 
-from dataclasses import dataclass  # noqa: E402
+from ._reference import mcgen as _ref_mcgen  # noqa: E402
+
+GenSpec = _ref_mcgen.GenSpec  # the reference's spec (P/mcgen.py:34-50)
 
 
-@dataclass(frozen=True)
-class GenSpec:
-    """How many events to draw, from which seed, under which safety margins
-    (reference mcgen.py:35-50)."""
-
-    n_events: int
-    seed: int = 0
-    envelope_safety: float = 1.1
-    max_attempts_factor: int = 1000
-    streams: int = 1
-
-    def __post_init__(self):
-        if self.n_events < 1:
-            raise ValueError("n_events must be >= 1")
-        if self.envelope_safety < 1.0:
-            raise ValueError("envelope_safety must be >= 1")
-        if self.streams < 1:
-            raise ValueError("streams must be >= 1")
-
-
-def _stream_states(spec: GenSpec):
+def _stream_states(spec):
     """PCG64 states of SeedSequence(seed).spawn(streams) (mcgen.py:57-59)."""
     from . import _lib as L
 
@@ -268,7 +256,9 @@ def _run_streams(spec, budget, gen_one, stats, dalitz: bool):
     """The per-stream loop of _generate_streams / _dalitz_streams: events of
     stream i follow those of stream i-1."""
     from . import _lib as L
-    from .errors import AttemptsExhausted
+    from ._reference import errors as E
+
+    AttemptsExhausted = E.AttemptsExhausted
 
     states = _stream_states(spec)
     counts = _split_counts(spec.n_events, spec.streams)
@@ -295,14 +285,15 @@ def _run_streams(spec, budget, gen_one, stats, dalitz: bool):
         offset += cnt
 
 
-def generate_1d(pdf, obs, spec: GenSpec, stats: dict | None = None, device: int = 0):
+def generate_1d(pdf, obs, spec, stats: dict | None = None, device: int = 0):
     """Reference generate_1d (mcgen.py:108-153) on the GPU: the same events
     for the same spec (see pfb_pcg.cu for the one caveat)."""
     from . import _lib as L
-    from .core import UnbinnedDataSet
+    from ._reference import errors as E
+    from ._reference import pdf as ref_pdf
     from .engine import device_context
-    from .errors import EnvelopeExceeded, UnboundedObservable
-    from .pdf import normalize
+
+    EnvelopeExceeded, UnboundedObservable, normalize = E.EnvelopeExceeded, E.UnboundedObservable, ref_pdf.normalize
 
     lo, hi = obs.lower, obs.upper
     if not (math.isfinite(lo) and math.isfinite(hi)):
@@ -342,16 +333,18 @@ def generate_1d(pdf, obs, spec: GenSpec, stats: dict | None = None, device: int 
                 raise EnvelopeExceeded(f"density {hit.observed} exceeded envelope {envelope} after a rescan") from None
             envelope = spec.envelope_safety * max(scan(RESCAN_POINTS), hit.observed)
     col = _adopt(ctx, st, 1, spec.n_events, [obs])[0]
-    return UnbinnedDataSet._from_checked([obs], [col])
+    return DeviceDataSet.adopt_store([obs], [col])
 
 
-def generate_dalitz(terms, ch, spec: GenSpec, observables=None, stats: dict | None = None, device: int = 0):
+def generate_dalitz(terms, ch, spec, observables=None, stats: dict | None = None, device: int = 0):
     """Reference generate_dalitz (mcgen.py:155-199) on the GPU: flat phase
     space over the (s12, s13) box, boundary filter, intensity accept-reject."""
     from . import _lib as L
-    from .core import UnbinnedDataSet, Variable
+    from ._reference import core as ref_core
+    from ._reference import errors as E
     from .engine import device_context
-    from .errors import EnvelopeExceeded
+
+    EnvelopeExceeded, Variable = E.EnvelopeExceeded, ref_core.Variable
 
     if not terms:
         raise ValueError("need at least one resonance term")
@@ -394,4 +387,4 @@ def generate_dalitz(terms, ch, spec: GenSpec, observables=None, stats: dict | No
                     f"intensity {hit.observed} exceeded envelope {envelope} after a rescan") from None
             envelope = spec.envelope_safety * max(scan(2048), hit.observed)
     s12, s13 = _adopt(ctx, st, 2, spec.n_events, list(observables))
-    return UnbinnedDataSet._from_checked(list(observables), [s12, s13])
+    return DeviceDataSet.adopt_store(list(observables), [s12, s13])

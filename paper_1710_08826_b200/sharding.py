@@ -1,85 +1,71 @@
 """Event sharding across GPUs and the exact cross-shard reduction.
 
-Reference semantics (sharding.py:68-146):
+The shard plan, the ``Shard``/``PartialSum`` records and ``reduce_partials``
+are the reference's own (P/sharding.py:43-131); this module supplies the
+device side of them:
 
-* ``shard(ds, W, block)``: contiguous ceil/floor split, interior bounds
-  aligned down to the block when N >= W*block -- computed by the native
-  ``pfb_shard_bounds`` so the integers are identical.
-* ``partial_nll``: one shard's exact partial.  The reference ships a
-  Shewchuk expansion; here the partial *is* the 72-word integer accumulator
-  of its block sums, which sums associatively.
-* ``reduce_partials``: every shard exactly once (MissingShard /
-  DuplicateShard), then one rounding -- bitwise the single-process total
-  whenever the shards are block-aligned.
-
-Multi-GPU (one process per GPU, torch.distributed): :class:`ShardedNll` keeps
-each rank's shard resident in its HBM; one NLL call is one fused kernel that
-writes the shard's accumulator, ONE all-reduce of 72 int64 (NCCL over
-NVLink), one rounding kernel.  The same code runs over gloo on CPU tensors for
-the host-side tests (accumulators produced by the host digit split).
+* :func:`partial_nll` -- one shard's partial on the GPU, returned as the
+  reference ``PartialSum`` whose ``components`` are an exact non-overlapping
+  expansion of the shard's 72-word integer accumulator
+  (:func:`components_from_acc`), so the reference's ``reduce_partials``
+  (``math.fsum`` of all components, P/sharding.py:117-131) merges device
+  partials -- and device with host partials -- bit for bit;
+* :func:`sharded_nll` -- the driver-side convenience (P/sharding.py:134-146)
+  with device partials;
+* :class:`ShardedNll` -- one process per GPU (torch.distributed): each rank
+  keeps its ``shard()`` rows resident in HBM; one NLL call is one fused kernel
+  that writes the shard's accumulator, ONE all-reduce of 72 int64 (NCCL over
+  NVLink, or the NVLink peer exchange fused into the kernel), one rounding.
+  Integer limbs add associatively, so every rank returns the single-GPU bits.
 """
 
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
-from typing import Mapping, Sequence
+import math
+from typing import Sequence
 
 import numpy as np
 
 from . import _lib as L
-from .errors import DuplicateShard, MissingShard
+from ._reference import engine as ref_engine
+from ._reference import sharding as ref_sharding
+from .engine import round_acc, shard_bounds  # noqa: F401  (re-exported)
 
 DEFAULT_BLOCK = L.PFB_BLOCK
+Shard = ref_sharding.Shard
+PartialSum = ref_sharding.PartialSum
+shard = ref_sharding.shard
+reduce_partials = ref_sharding.reduce_partials
 
 
-def shard_bounds(n: int, workers: int, block: int = DEFAULT_BLOCK) -> list[int]:
-    """[b0=0, b1, ..., bW=n] exactly as the reference shard() (sharding.py:80-85)."""
-    if workers < 1:
-        raise ValueError("workers must be >= 1")
-    out = (ctypes.c_int64 * (workers + 1))()
-    L.check(L.lib().pfb_shard_bounds(int(n), int(workers), int(block), out), "pfb_shard_bounds")
-    return list(out)
-
-
-@dataclass(frozen=True)
-class Shard:
-    index: int
-    begin: int
-    end: int
-    columns: Mapping[str, np.ndarray]
-
-    @property
-    def size(self) -> int:
-        return self.end - self.begin
-
-
-@dataclass(frozen=True)
-class PartialSum:
-    """One shard's contribution: rounded sum plus its exact integer accumulator."""
-
-    shard_index: int
-    count: int
-    sum: float
-    acc: tuple[int, ...] = ()
-
-
-def shard(ds, workers: int, block: int = DEFAULT_BLOCK) -> list[Shard]:
-    n = ds.n_events
-    columns = ds.columns() if n else {o.name: np.empty(0) for o in ds.observables}
-    b = shard_bounds(n, workers, block)
-    return [Shard(k, b[k], b[k + 1], {name: col[b[k]:b[k + 1]] for name, col in columns.items()})
-            for k in range(workers)]
-
-
-def round_acc(acc) -> float:
-    a = np.ascontiguousarray(np.asarray(acc, dtype=np.int64))
-    out = ctypes.c_double()
-    code = L.lib().pfb_acc_round(a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(out))
-    if code == L.E_INVALID_SUM:
-        raise ValueError("-inf + inf in exact sum")
-    L.check(code, "pfb_acc_round")
-    return out.value
+def components_from_acc(acc) -> tuple[float, ...]:
+    """An exact expansion of the accumulator's value: non-overlapping doubles
+    in increasing magnitude whose real sum is exactly the accumulated sum (the
+    contract of the reference ``ExactAccumulator.partials``,
+    P/reduction.py:78-118), so ``math.fsum(components)`` is its correctly
+    rounded value.  Limb i of the first 68 carries weight 2^(32 i - 1074);
+    words 68..70 count +inf / -inf / NaN terms."""
+    a = [int(v) for v in np.asarray(acc, dtype=np.int64).tolist()]
+    if a[L.PFB_NLIMBS + 2] > 0:
+        return (math.nan,)
+    pinf, ninf = a[L.PFB_NLIMBS] > 0, a[L.PFB_NLIMBS + 1] > 0
+    if pinf or ninf:
+        return tuple(([math.inf] if pinf else []) + ([-math.inf] if ninf else []))
+    value = 0
+    for i in range(L.PFB_NLIMBS - 1, -1, -1):
+        value = (value << 32) + a[i]
+    sign = -1.0 if value < 0 else 1.0
+    mag = -value if value < 0 else value
+    out = []
+    j = 0
+    while mag:
+        chunk = mag & ((1 << 53) - 1)
+        if chunk:
+            out.append(sign * math.ldexp(float(chunk), 53 * j - 1074))
+        mag >>= 53
+        j += 1
+    return tuple(out)
 
 
 def acc_of_values(values) -> np.ndarray:
@@ -91,22 +77,22 @@ def acc_of_values(values) -> np.ndarray:
     return acc
 
 
-def partial_nll(sh: Shard, pdf, snap, norms=None, block: int = DEFAULT_BLOCK, ctx=None) -> PartialSum:
-    """Exact partial of one shard on the GPU (reference sharding.py:94-114)."""
+def partial_accumulator(sh, pdf, snap, norms=None, block: int = DEFAULT_BLOCK, ctx=None) -> np.ndarray:
+    """The shard's exact 72-word accumulator of -ln p, on the GPU; errors carry
+    global indices (offset = shard begin, P/sharding.py:110-113)."""
     import torch
 
     from . import engine
 
     if norms is None:
-        norms = engine.resolve_norms(pdf, snap, engine.NormalizationStore())
-    if sh.size == 0:
-        return PartialSum(sh.index, 0, 0.0, tuple([0] * L.PFB_ACC_WORDS))
+        norms = ref_engine.resolve_norms(pdf, snap, ref_engine.NormalizationStore())
     if block != DEFAULT_BLOCK:
         raise ValueError(f"the device reduction block is fixed at {DEFAULT_BLOCK}")
+    if sh.size == 0:
+        return np.zeros(L.PFB_ACC_WORDS, dtype=np.int64)
     ctx = ctx or engine.device_context(0)
-    names = tuple(sorted(sh.columns))
     needed = {nm for node in pdf.walk() for nm in node.observable_names()}
-    names = tuple(nm for nm in names if nm in needed)
+    names = tuple(nm for nm in sorted(sh.columns) if nm in needed)
     arrays = [sh.columns[k] for k in names]
     plan = ctx.plan_for(pdf, names)
     st = ctx.store_for(arrays)
@@ -117,33 +103,29 @@ def partial_nll(sh: Shard, pdf, snap, norms=None, block: int = DEFAULT_BLOCK, ct
             "pfb_nll_partial_async")
     L.check(L.lib().pfb_ctx_synchronize(ctx.handle), "pfb_ctx_synchronize")
     a = acc.cpu().numpy()
-    if a[L.PFB_ACC_FAILS]:
+    frac = ctypes.c_int32()
+    L.check(L.lib().pfb_ctx_last_fraction_failure(ctx.handle, ctypes.byref(frac)), "pfb_ctx_last_fraction_failure")
+    if a[L.PFB_ACC_FAILS] or frac.value:
         err = L.PfbErr()
         L.check(L.lib().pfb_last_error(ctx.handle, ctypes.byref(err)), "pfb_last_error")
-        engine.raise_for(err, err.code, pdf, "partial_nll")
-    return PartialSum(sh.index, sh.size, round_acc(a), tuple(int(x) for x in a))
+        engine.raise_for(err, err.code, "partial_nll")
+    return a
 
 
-def reduce_partials(partials: Sequence[PartialSum]) -> float:
-    """Exact merge in shard order (reference sharding.py:117-131)."""
-    seen = sorted(partials, key=lambda p: p.shard_index)
-    indices = [p.shard_index for p in seen]
-    for k, idx in enumerate(indices):
-        if indices.count(idx) > 1:
-            raise DuplicateShard(f"shard index {idx} appears more than once")
-        if idx != k:
-            raise MissingShard(f"expected shard index {k}, found {idx}")
-    total = np.zeros(L.PFB_ACC_WORDS, dtype=np.int64)
-    for p in seen:
-        total += np.asarray(p.acc if p.acc else acc_of_values([p.sum]), dtype=np.int64)
-    return round_acc(total)
+def partial_nll(sh, pdf, snap, norms=None, block: int = DEFAULT_BLOCK, ctx=None):
+    """Device ``partial_nll`` (P/sharding.py:94-114): the reference
+    ``PartialSum`` with an exact expansion of the shard's sum."""
+    if sh.size == 0:
+        return PartialSum(sh.index, 0, 0.0, ())
+    acc = partial_accumulator(sh, pdf, snap, norms, block, ctx)
+    return PartialSum.from_components(sh.index, sh.size, components_from_acc(acc))
 
 
 def sharded_nll(pdf, ds, snap=None, workers: int = 1, store=None, block: int = DEFAULT_BLOCK) -> float:
-    from . import engine
-
-    store = store if store is not None else engine.NormalizationStore()
-    norms = engine.resolve_norms(pdf, snap, store)
+    """Device ``sharded_nll`` (P/sharding.py:134-146): shard, device partials,
+    the reference's ``reduce_partials``."""
+    store = store if store is not None else ref_engine.NormalizationStore()
+    norms = ref_engine.resolve_norms(pdf, snap, store)
     return reduce_partials([partial_nll(sh, pdf, snap, norms, block) for sh in shard(ds, workers, block)])
 
 
@@ -225,7 +207,7 @@ class ShardedNll:
         b = shard_bounds(self.n, world)
         self.begin, self.end = b[rank], b[rank + 1]
         self.ctx = engine.device_context(device)
-        cols = engine._needed_columns(pdf, ds)
+        cols = ref_engine._needed_columns(pdf, ds)
         self.names = tuple(cols)
         # the shard only: this rank never holds the other ranks' events
         self.arrays = [np.ascontiguousarray(cols[k][self.begin:self.end]) for k in self.names]
@@ -292,7 +274,7 @@ class ShardedNll:
             self.rank, self.world, (err.code, err.index, err.node, err.value), self.group, self.acc.device)
         e = L.PfbErr()
         e.code, e.index, e.node, e.value = code, index, node, value
-        engine.raise_for(e, e.code, self.pdf, "ShardedNll")
+        engine.raise_for(e, e.code, "ShardedNll")
 
 
 def first_error_across_ranks(rank: int, world: int, err: tuple, group=None, device="cpu") -> tuple:

@@ -93,8 +93,7 @@ def main():
             cols = list(mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 3))  # Philox on the GPU
             obs, pdf, _ = models.c3()
         gen_s = time.perf_counter() - t0
-        ds = pf.UnbinnedDataSet(list(obs))
-        ds.extend(cols)
+        ds = pf.DeviceDataSet.from_columns(list(obs), cols, device=None)
         backend = pf.DeviceBackend(lineshape_cache=args.cache if cfg == "c3" else 0)
         for w in warps_list:
             ctx.set_warps_per_block(w)

@@ -1,11 +1,13 @@
-"""Shared model builders for the tests: the same model as a device tree
-(paper_1710_08826_b200 nodes) and as an oracle spec (plain tuples)."""
+"""Shared model builders for the tests: the same model as a reference tree
+(parafit's own builders -- the API the device engine plugs into) and as an
+oracle spec (plain tuples)."""
 
 from __future__ import annotations
 
 import math
 
 import numpy as np
+from paper_1710_08826_b200._reference import parafit as P
 
 D_CHANNEL_T = (1.86484, 0.13957, 0.13957, 0.13498)
 
@@ -19,14 +21,13 @@ C3_TERMS = [
 
 
 def c1(point=(5.0, 0.5, -0.3, 0.3)):
-    import paper_1710_08826_b200 as pf
-
-    x = pf.Variable.observable("x", 0.0, 10.0)
-    mu = pf.Variable("mu", point[0], 0.0, 10.0, step=0.01)
-    sigma = pf.Variable("sigma", point[1], 0.01, 5.0, step=1e-3)
-    alpha = pf.Variable("alpha", point[2], -5.0, 5.0, step=1e-3)
-    f = pf.Variable("f", point[3], 0.0, 1.0, step=1e-3)
-    pdf = pf.add_pdf([pf.gaussian(x, mu, sigma), pf.exponential(x, alpha)], [f])
+    pf = ref()
+    x = P.Variable.observable("x", 0.0, 10.0)
+    mu = P.Variable("mu", point[0], 0.0, 10.0, step=0.01)
+    sigma = P.Variable("sigma", point[1], 0.01, 5.0, step=1e-3)
+    alpha = P.Variable("alpha", point[2], -5.0, 5.0, step=1e-3)
+    f = P.Variable("f", point[3], 0.0, 1.0, step=1e-3)
+    pdf = P.add_pdf([P.gaussian(x, mu, sigma), P.exponential(x, alpha)], [f])
     return x, pdf, (mu, sigma, alpha, f)
 
 
@@ -36,14 +37,13 @@ def c1_spec(point):
 
 
 def c2(point=(5.0, 1.0, -0.4)):
-    import paper_1710_08826_b200 as pf
-
-    x = pf.Variable.observable("x", 0.0, 10.0)
-    y = pf.Variable.observable("y", 0.0, 10.0)
-    mu = pf.Variable("mu", point[0], 0.0, 10.0, step=0.01)
-    sigma = pf.Variable("sigma", point[1], 0.01, 5.0, step=1e-3)
-    alpha = pf.Variable("alpha", point[2], -5.0, 5.0, step=1e-3)
-    pdf = pf.prod_pdf([pf.gaussian(x, mu, sigma), pf.exponential(y, alpha)])
+    pf = ref()
+    x = P.Variable.observable("x", 0.0, 10.0)
+    y = P.Variable.observable("y", 0.0, 10.0)
+    mu = P.Variable("mu", point[0], 0.0, 10.0, step=0.01)
+    sigma = P.Variable("sigma", point[1], 0.01, 5.0, step=1e-3)
+    alpha = P.Variable("alpha", point[2], -5.0, 5.0, step=1e-3)
+    pdf = P.prod_pdf([P.gaussian(x, mu, sigma), P.exponential(y, alpha)])
     return (x, y), pdf, (mu, sigma, alpha)
 
 
@@ -53,22 +53,21 @@ def c2_spec(point):
 
 
 def c3(terms=C3_TERMS, grid=(400, 400)):
-    import paper_1710_08826_b200 as pf
-
-    ch = pf.DecayChannel(*D_CHANNEL_T)
+    pf = ref()
+    ch = P.DecayChannel(*D_CHANNEL_T)
     rts = []
     for k, (pair, m, w, spin, mag, ph) in enumerate(terms):
-        rts.append(pf.ResonanceTerm(
+        rts.append(P.ResonanceTerm(
             pair=pair,
-            mass=pf.Variable(f"t{k}_m", m, fixed=True),
-            width=pf.Variable(f"t{k}_w", w, fixed=True),
+            mass=P.Variable(f"t{k}_m", m, fixed=True),
+            width=P.Variable(f"t{k}_w", w, fixed=True),
             spin=spin,
-            magnitude=pf.Variable(f"t{k}_mag", mag, 0.0, 100.0, step=0.01, fixed=(k == 0)),
-            phase=pf.Variable(f"t{k}_ph", ph, -2 * math.pi, 2 * math.pi, step=0.01, fixed=(k == 0)),
+            magnitude=P.Variable(f"t{k}_mag", mag, 0.0, 100.0, step=0.01, fixed=(k == 0)),
+            phase=P.Variable(f"t{k}_ph", ph, -2 * math.pi, 2 * math.pi, step=0.01, fixed=(k == 0)),
         ))
-    s12 = pf.Variable.observable("s12", *ch.s12_range)
-    s13 = pf.Variable.observable("s13", *ch.s13_range)
-    pdf = pf.dalitz_pdf(rts, ch, s12_obs=s12, s13_obs=s13, grid=grid)
+    s12 = P.Variable.observable("s12", *ch.s12_range)
+    s13 = P.Variable.observable("s13", *ch.s13_range)
+    pdf = P.dalitz_pdf(rts, ch, s12_obs=s12, s13_obs=s13, grid=grid)
     return (s12, s13), pdf, rts
 
 
@@ -77,10 +76,25 @@ def c3_spec(terms=C3_TERMS, grid=(400, 400)):
     return ("dalitz", "s12", "s13", spec_terms, D_CHANNEL_T, grid)
 
 
-def dataset(observables, columns):
-    import paper_1710_08826_b200 as pf
+def ref():
+    """The reference package (parafit) the engine plugs into."""
+    from paper_1710_08826_b200._reference import parafit
 
-    ds = pf.UnbinnedDataSet(list(observables))
+    return parafit
+
+
+def dataset(observables, columns):
+    """A DeviceDataSet (a reference UnbinnedDataSet) over whole columns; the
+    HBM copy is made on the first device NLL."""
+    from paper_1710_08826_b200.datasets import DeviceDataSet
+
+    return DeviceDataSet.from_columns(list(observables), [np.asarray(c, dtype=np.float64) for c in columns],
+                                      device=None)
+
+
+def ref_dataset(observables, columns):
+    """The reference's own list-backed UnbinnedDataSet (small inputs only)."""
+    ds = ref().UnbinnedDataSet(list(observables))
     ds.extend([np.asarray(c, dtype=np.float64) for c in columns])
     return ds
 

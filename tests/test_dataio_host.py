@@ -12,7 +12,7 @@ def dio():
 
 
 def test_npy_length_and_rejects(dio, tmp_path):
-    from paper_1710_08826_b200 import errors as E
+    from paper_1710_08826_b200._reference import errors as E
 
     a = np.arange(12345, dtype="<f8")
     np.save(tmp_path / "a.npy", a)

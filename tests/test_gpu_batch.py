@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -25,20 +26,20 @@ def pf():
 
 def points_eval(pf, pdf, ds, params, pts):
     """(snaps, norms) per point the way the fitter builds them."""
-    store = pf.NormalizationStore()
+    store = P.NormalizationStore()
     snaps, norms = [], []
     for pt in pts:
         for v, val in zip(params, pt):
-            pf.set_value(v, float(val))
-        snap = pf.snapshot(pdf.param_closure())
+            P.set_value(v, float(val))
+        snap = P.snapshot(pdf.param_closure())
         snaps.append(snap)
-        norms.append(pf.resolve_norms(pdf, snap, store))
+        norms.append(P.resolve_norms(pdf, snap, store))
     return snaps, norms
 
 
 def single(pf, pdf, ds, params, pt):
     for v, val in zip(params, pt):
-        pf.set_value(v, float(val))
+        P.set_value(v, float(val))
     try:
         return pf.nll(pdf, ds)
     except Exception as exc:  # the batched call returns the exception in this slot
@@ -93,35 +94,43 @@ def test_batch_equals_single_bitwise(pf, config):
 
 
 def test_batch_error_attributed_to_its_point(pf):
-    x = pf.Variable.observable("x", 0.0, 1.0)
-    c0 = pf.Variable("c0", 0.5, -1.0, 2.0)
-    c1 = pf.Variable("c1", 1.0, -2.0, 2.0)
-    pdf = pf.polynomial(x, [c0, c1])
+    x = P.Variable.observable("x", 0.0, 1.0)
+    c0 = P.Variable("c0", 0.5, -1.0, 2.0)
+    c1 = P.Variable("c1", 1.0, -2.0, 2.0)
+    pdf = P.polynomial(x, [c0, c1])
     vals = np.linspace(0.0, 1.0, 9000)
     ds = models.dataset([x], [vals])
     pts = [(0.5, 1.0), (0.0, 1.0), (0.6, 1.0)]  # point 1: p(0) = 0 -> NonPositiveDensity at index 0
     snaps, norms = points_eval(pf, pdf, ds, [c0, c1], pts)
     got = pf.DeviceBackend().evaluate_batch(pdf, {"x": ds.column("x")}, snaps, norms, 0, ds.n_events)
-    assert isinstance(got[1], pf.errors.NonPositiveDensity) and got[1].index == 0
+    assert isinstance(got[1], P.errors.NonPositiveDensity) and got[1].index == 0
     assert got[0] == single(pf, pdf, ds, [c0, c1], pts[0])
     assert got[2] == single(pf, pdf, ds, [c0, c1], pts[2])
 
 
 def test_batched_fit_equals_unbatched_fit(pf, golden_dir):
+    """DeviceFitManager with batched stencils == the same fit point by point ==
+    the unmodified reference FitManager over DeviceBackend: same n_calls,
+    bitwise values, errors, minimum and norm-cache counters."""
     import os
-
-    from paper_1710_08826_b200.fitting import FcnHandle, FitManager, minimize
 
     g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
     (x, y), pdf, params = models.c2((4.9, 1.1, -0.35))
     ds = models.dataset([x, y], [g["x"], g["y"]])
-    batched = FitManager(pdf, ds).fit()
-    for v, val in zip(params, (4.9, 1.1, -0.35)):
-        pf.set_value(v, val)
-    fm = FitManager(pdf, ds)
-    plain = fm.fcn()
-    unbatched = minimize(FcnHandle(plain._objective), fm.free_parameters(), fm.options)
-    assert batched.n_calls == unbatched.n_calls
-    assert np.array_equal(batched.values, unbatched.values)
-    assert batched.nll_min == unbatched.nll_min
-    np.testing.assert_array_equal(batched.covariance, unbatched.covariance)
+    fits = []
+    for make in (lambda: pf.DeviceFitManager(pdf, ds),
+                 lambda: pf.DeviceFitManager(pdf, ds, batch=False),
+                 lambda: P.FitManager(pdf, ds, backend=pf.DeviceBackend())):
+        for v, val in zip(params, (4.9, 1.1, -0.35)):
+            P.set_value(v, val)
+        fm = make()
+        fits.append((fm.fit(), fm))
+    (batched, fm0), (plain, fm1), (ref, fm2) = fits
+    assert fm0.objective.batches > 0 and fm0.objective.batched_points > 10
+    for other, fm in ((plain, fm1), (ref, fm2)):
+        assert batched.n_calls == other.n_calls
+        assert np.array_equal(batched.values, other.values)
+        assert np.array_equal(batched.errors, other.errors)
+        assert batched.nll_min == other.nll_min
+        assert fm0.store.kernel_evals == fm.store.kernel_evals
+        assert fm0.store.norm_computations == fm.store.norm_computations

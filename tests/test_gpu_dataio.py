@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -44,8 +45,8 @@ def test_load_equals_in_memory_and_shards(pf, golden_dir, tmp_path):
         sh = dataio.load_npy_shard([x, y], files, r, w)
         assert sh.n_events == b[r + 1] - b[r]
         assert np.array_equal(np.asarray(sh.column("y")), g["y"][b[r]:b[r + 1]])
-        snap = pf.snapshot(pdf.param_closure())
-        norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+        snap = P.snapshot(pdf.param_closure())
+        norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
         parts.append(pf.nll_block_sums(pdf, sh.columns(), snap, norms, 0, sh.n_events))
     total = sharding.round_acc(sharding.acc_of_values(np.concatenate(parts)))
     assert total == pf.nll(pdf, mem)
@@ -53,10 +54,10 @@ def test_load_equals_in_memory_and_shards(pf, golden_dir, tmp_path):
 
 def test_range_check_matches_reference_error(pf, tmp_path):
     from paper_1710_08826_b200 import dataio
-    from paper_1710_08826_b200 import errors as E
+    from paper_1710_08826_b200._reference import errors as E
 
-    x = pf.Variable.observable("x", 0.0, 10.0)
-    y = pf.Variable.observable("y", 0.0, 10.0)
+    x = P.Variable.observable("x", 0.0, 10.0)
+    y = P.Variable.observable("y", 0.0, 10.0)
     xs = np.linspace(0.0, 10.0, 50001)
     ys = np.full_like(xs, 5.0)
     ys[31337] = 10.5

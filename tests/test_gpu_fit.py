@@ -35,7 +35,7 @@ def check(result, ref):
 
 def test_c1_fit_matches_reference(fits, golden_dir):
     import paper_1710_08826_b200 as pf
-    from paper_1710_08826_b200.fitting import FitManager
+    from paper_1710_08826_b200.fitting import DeviceFitManager as FitManager
 
     g = np.load(os.path.join(golden_dir, "c1_sumpdf.npz"))
     x, pdf, params = models.c1(tuple(fits["c1"]["start"]))
@@ -44,7 +44,7 @@ def test_c1_fit_matches_reference(fits, golden_dir):
 
 
 def test_c2_fit_matches_reference(fits, golden_dir):
-    from paper_1710_08826_b200.fitting import FitManager
+    from paper_1710_08826_b200.fitting import DeviceFitManager as FitManager
 
     g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
     (x, y), pdf, params = models.c2(tuple(fits["c2"]["start"]))
@@ -53,7 +53,7 @@ def test_c2_fit_matches_reference(fits, golden_dir):
 
 
 def test_c3_dalitz_fit_matches_reference(fits, golden_dir):
-    from paper_1710_08826_b200.fitting import FitManager
+    from paper_1710_08826_b200.fitting import DeviceFitManager as FitManager
 
     g = np.load(os.path.join(golden_dir, "c3_dalitz.npz"))
     ref = fits["c3"]

@@ -23,6 +23,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -39,7 +40,7 @@ def run_fit(ref):
     """Generate the reference's 100M events on the device and fit them;
     returns (result, dataset, timings)."""
     import paper_1710_08826_b200 as pf
-    from paper_1710_08826_b200.fitting import FitManager
+    from paper_1710_08826_b200.fitting import DeviceFitManager as FitManager
     from paper_1710_08826_b200.mcgen import GenSpec, generate_dalitz
 
     start = ref["start"]
@@ -50,7 +51,7 @@ def run_fit(ref):
         t.magnitude.name, t.phase.name = f"{nm}_mag", f"{nm}_ph"
     _, _, truth = models.c3(models.C3_TERMS, grid=tuple(ref["grid"]))
     t0 = time.perf_counter()
-    ds = generate_dalitz(truth, pf.DecayChannel(*models.D_CHANNEL_T), GenSpec(**ref["spec"]),
+    ds = generate_dalitz(truth, P.DecayChannel(*models.D_CHANNEL_T), GenSpec(**ref["spec"]),
                          observables=(s12, s13))
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()

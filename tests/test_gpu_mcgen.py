@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -52,13 +53,15 @@ def test_dalitz_generation_inside_and_fit_truth(mc):
     s12, s13 = mc.device_dalitz(300_000, terms, models.D_CHANNEL_T, seed=11)
     s12b, _ = mc.device_dalitz(300_000, terms, models.D_CHANNEL_T, seed=11)
     assert np.array_equal(s12, s12b)
-    ch = pf.DecayChannel(*models.D_CHANNEL_T)
-    from paper_1710_08826_b200.dalitz import in_boundary_mask
+    ch = P.DecayChannel(*models.D_CHANNEL_T)
+    from paper_1710_08826_b200._reference import dalitz as RD
+
+    in_boundary_mask = RD.in_boundary_mask
 
     assert in_boundary_mask(s12, s13, ch).all()
     # the generating coefficients give a lower NLL than perturbed ones
     (o12, o13), pdf, rts = models.c3()
     ds = models.dataset([o12, o13], [s12, s13])
     truth = pf.nll(pdf, ds)
-    pf.set_value(rts[1].magnitude, 0.9)
+    P.set_value(rts[1].magnitude, 0.9)
     assert pf.nll(pdf, ds) > truth + 10.0

@@ -14,6 +14,7 @@ import pytest
 
 from oracle import parafit_oracle as O
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -23,6 +24,7 @@ RTOL = 1e-10
 @pytest.fixture(scope="module")
 def pf():
     import paper_1710_08826_b200 as pf
+    import paper_1710_08826_b200.dalitz  # noqa: F401
     from paper_1710_08826_b200 import _lib as L
 
     if L.device_count() < 1:
@@ -72,11 +74,11 @@ def test_c1_sumpdf_parity(pf, golden_dir):
     ds = models.dataset([x], [g["x"]])
     for i, pt in enumerate(g["points"]):
         for v, val in zip(params, pt):
-            pf.set_value(v, float(val))
+            P.set_value(v, float(val))
         got = pf.nll(pdf, ds)
         assert rel(got, g["nll"][i]) <= RTOL, (i, got, g["nll"][i])
-        bs = pf.nll_block_sums(pdf, ds.columns(), pf.snapshot(pdf.param_closure()),
-                               pf.resolve_norms(pdf, None, pf.NormalizationStore()), 0, ds.n_events)
+        bs = pf.nll_block_sums(pdf, ds.columns(), P.snapshot(pdf.param_closure()),
+                               P.resolve_norms(pdf, None, P.NormalizationStore()), 0, ds.n_events)
         np.testing.assert_allclose(bs, g[f"bsums_{i}"], rtol=1e-12)
 
 
@@ -86,13 +88,13 @@ def test_c2_prod_parity_and_shards(pf, golden_dir):
     ds = models.dataset([x, y], [g["x"], g["y"]])
     for i, pt in enumerate(g["points"]):
         for v, val in zip(params, pt):
-            pf.set_value(v, float(val))
+            P.set_value(v, float(val))
         assert rel(pf.nll(pdf, ds), g["nll"][i]) <= RTOL
     for v, val in zip(params, g["points"][0]):
-        pf.set_value(v, float(val))
+        P.set_value(v, float(val))
     whole = pf.nll(pdf, ds)
     for w in (2, 3, 4):
-        got = pf.sharded_nll(pdf, ds, pf.snapshot(pdf.param_closure()), workers=w)
+        got = pf.sharded_nll(pdf, ds, P.snapshot(pdf.param_closure()), workers=w)
         assert rel(got, g[f"sharded_{w}"][0]) <= RTOL
         # aligned shards (N >= W*4096) reproduce the unsharded device total bit for bit
         assert got == whole
@@ -104,35 +106,36 @@ def test_c3_dalitz_parity(pf, golden_dir):
     ds = models.dataset([s12, s13], [g["s12"], g["s13"]])
     got = pf.nll(pdf, ds)
     assert rel(got, g["nll"][0]) <= RTOL, (got, g["nll"][0])
-    pf.set_value(terms[1].magnitude, 0.9)
-    pf.set_value(terms[2].phase, 1.1)
+    P.set_value(terms[1].magnitude, 0.9)
+    P.set_value(terms[2].phase, 1.1)
     assert rel(pf.nll(pdf, ds), g["nll_b"][0]) <= RTOL
 
 
 def test_dalitz_grid_mask_and_integrals(pf, golden_dir):
     g = load(golden_dir, "c3_dalitz.npz")
-    ch = pf.DecayChannel(*models.D_CHANNEL_T)
+    ch = P.DecayChannel(*models.D_CHANNEL_T)
     for tag, grid in (("64x64", (64, 64)), ("400x400", (400, 400))):
-        _, _, mask, darea = pf.integration_grid(ch, grid)
+        dg = pf.dalitz.device_grid(ch, grid, owner="mask-test")
+        mask = dg.mask()
         assert np.array_equal(np.packbits(mask), g[f"mask_{tag}"]), tag
-        assert int(mask.sum()) == int(g[f"ninside_{tag}"][0])
-        assert darea == g[f"darea_{tag}"][0]
+        assert int(mask.sum()) == int(g[f"ninside_{tag}"][0]) == dg.n_inside
+        assert dg.area == g[f"darea_{tag}"][0]
         _, pdf, terms = models.c3(grid=grid)
-        cache = pf.compute_integrals(terms, ch, grid)
+        cache = pf.dalitz.compute_integrals(terms, ch, grid)
         np.testing.assert_allclose(cache.matrix, g[f"matrix_{tag}"], rtol=1e-12, atol=0)
-        assert rel(pf.dalitz_norm(terms, cache), g[f"norm_{tag}"][0]) <= 1e-12
+        assert rel(P.dalitz_norm(terms, cache), g[f"norm_{tag}"][0]) <= 1e-12
 
 
 def test_dalitz_integral_cache_reuse(pf):
-    ch = pf.DecayChannel(*models.D_CHANNEL_T)
+    ch = P.DecayChannel(*models.D_CHANNEL_T)
     _, pdf, terms = models.c3(grid=(64, 64))
-    prior = pf.compute_integrals(terms, ch, (64, 64))
-    pf.set_value(terms[1].magnitude, 2.5)
-    assert pf.compute_integrals(terms, ch, (64, 64), prior=prior) is prior
-    m = pf.Variable("mfloat", 0.9, 0.5, 1.3, step=0.001)
+    prior = pf.dalitz.compute_integrals(terms, ch, (64, 64))
+    P.set_value(terms[1].magnitude, 2.5)
+    assert pf.dalitz.compute_integrals(terms, ch, (64, 64), prior=prior) is prior
+    m = P.Variable("mfloat", 0.9, 0.5, 1.3, step=0.001)
     terms[3].mass = m
-    fresh = pf.compute_integrals(terms, ch, (64, 64), prior=prior)
-    scratch = pf.compute_integrals(terms, ch, (64, 64))
+    fresh = pf.dalitz.compute_integrals(terms, ch, (64, 64), prior=prior)
+    scratch = pf.dalitz.compute_integrals(terms, ch, (64, 64))
     assert fresh.matrix[0, 0] == prior.matrix[0, 0]
     np.testing.assert_array_equal(fresh.matrix, scratch.matrix)
     spec_terms = [(t.pair, t.spin, t.mass.value, t.width.value, t.magnitude.value, t.phase.value) for t in terms]
@@ -159,8 +162,8 @@ def test_warps_per_block_and_ranges_bitwise(pf):
     ctx.set_warps_per_block(0)
     assert rel(ref, O.nll(models.c1_spec((5.0, 0.5, -0.3, 0.3)), {"x": xs})) <= RTOL
     # multi-device style split of whole blocks reproduces the bits (host limb sum)
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     bs = pf.nll_block_sums(pdf, ds.columns(), snap, norms, 0, n)
     from paper_1710_08826_b200 import sharding
 
@@ -179,7 +182,7 @@ def test_e2e_host_streaming_equals_device(pf):
     dev = pf.nll(pdf, ds)
     ctx = pf.device_context(0)
     plan = ctx.plan_for(pdf, ("x", "y"))
-    vals, nv = plan.pack(None, pf.resolve_norms(pdf, None, pf.NormalizationStore()))
+    vals, nv = plan.pack(None, P.resolve_norms(pdf, None, P.NormalizationStore()))
     cols = (L._DBL_P * 2)(L.dptr(ds.column("x")), L.dptr(ds.column("y")))
     out = ctypes.c_double()
     err = L.PfbErr()
@@ -200,7 +203,7 @@ def test_lineshape_cache_matches_recompute(pf, golden_dir):
     ctx = pf.device_context(0)
     plan = ctx.plan_for(pdf, ("s12", "s13"))
     before = plan.cache_recomputes()
-    pf.set_value(terms[1].magnitude, 0.8)  # coefficient move: no amplitude rows recomputed
+    P.set_value(terms[1].magnitude, 0.8)  # coefficient move: no amplitude rows recomputed
     pf.nll(pdf, ds, backend=cached_backend)
     assert plan.cache_recomputes() == before
     plan.set_lineshape_cache(0)
@@ -212,48 +215,48 @@ def test_lineshape_cache_matches_recompute(pf, golden_dir):
 def test_error_indices_match_reference(pf, golden_dir):
     with open(os.path.join(golden_dir, "errors.json")) as fh:
         cases = json.load(fh)
-    x = pf.Variable.observable("x", 0.0, 1.0)
+    x = P.Variable.observable("x", 0.0, 1.0)
     vals = np.full(5000, 0.5)
     vals[4321] = 0.0
     ds = models.dataset([x], [vals])
-    with pytest.raises(pf.errors.NonPositiveDensity) as e:
-        pf.nll(pf.polynomial(x, [0.0, 1.0]), ds)
+    with pytest.raises(P.errors.NonPositiveDensity) as e:
+        pf.nll(P.polynomial(x, [0.0, 1.0]), ds)
     assert [type(e.value).__name__, e.value.index, e.value.value] == cases["poly_zero"]
 
     kind, idx, val, c, eps = cases["poly_dip_negative"]
     v3 = np.full(7000, 0.9)
     v3[6001] = c
     v3[6500] = c
-    with pytest.raises(pf.errors.NegativeDensity) as e:
-        pf.nll(pf.polynomial(x, [c * c - eps, -2.0 * c, 1.0]), models.dataset([x], [v3]))
+    with pytest.raises(P.errors.NegativeDensity) as e:
+        pf.nll(P.polynomial(x, [c * c - eps, -2.0 * c, 1.0]), models.dataset([x], [v3]))
     assert e.value.index == idx
     assert rel(e.value.value, val) <= 1e-6
 
-    y = pf.Variable.observable("y", 0.0, 10.0)
-    g_ = pf.gaussian(y, pf.Variable("m", 5.0, fixed=True), pf.Variable("s", 0.05, fixed=True))
-    e_ = pf.exponential(y, pf.Variable("a", -0.2, fixed=True))
-    tree = pf.add_pdf([g_, e_], [pf.Variable("f", 1.0, 0.0, 1.0)])
+    y = P.Variable.observable("y", 0.0, 10.0)
+    g_ = P.gaussian(y, P.Variable("m", 5.0, fixed=True), P.Variable("s", 0.05, fixed=True))
+    e_ = P.exponential(y, P.Variable("a", -0.2, fixed=True))
+    tree = P.add_pdf([g_, e_], [P.Variable("f", 1.0, 0.0, 1.0)])
     v4 = np.full(6000, 5.0)
     v4[5555] = 9.9
-    with pytest.raises(pf.errors.NonPositiveDensity) as e:
+    with pytest.raises(P.errors.NonPositiveDensity) as e:
         pf.nll(tree, models.dataset([y], [v4]))
     assert [type(e.value).__name__, e.value.index, e.value.value] == cases["sum_underflow"]
 
-    z = pf.Variable.observable("z")
+    z = P.Variable.observable("z")
     one = models.dataset([z], [np.array([0.0])])
-    got = pf.nll(pf.gaussian(z, pf.Variable("mu", 0.0, fixed=True), pf.Variable("sg", 1.0, fixed=True)), one)
+    got = pf.nll(P.gaussian(z, P.Variable("mu", 0.0, fixed=True), P.Variable("sg", 1.0, fixed=True)), one)
     assert abs(got - 0.5 * math.log(2 * math.pi)) <= 1e-12
-    with pytest.raises(pf.errors.EmptyDataSet):
-        pf.nll(pf.gaussian(z, 0.0, 1.0), pf.UnbinnedDataSet([z]))
+    with pytest.raises(P.errors.EmptyDataSet):
+        pf.nll(P.gaussian(z, 0.0, 1.0), P.UnbinnedDataSet([z]))
 
 
 def test_worker_error_index_in_third_block(pf):
     # reference tests/test_engine.py:106-114 (global index 9000)
-    x = pf.Variable.observable("x", 0.0, 1.0)
+    x = P.Variable.observable("x", 0.0, 1.0)
     values = np.full(4096 * 3, 0.5)
     values[9000] = 0.0
-    with pytest.raises(pf.errors.NonPositiveDensity) as err:
-        pf.nll(pf.polynomial(x, [0.0, 1.0]), models.dataset([x], [values]))
+    with pytest.raises(P.errors.NonPositiveDensity) as err:
+        pf.nll(P.polynomial(x, [0.0, 1.0]), models.dataset([x], [values]))
     assert err.value.index == 9000
 
 
@@ -266,8 +269,8 @@ def test_backend_protocol_drop_in(pf, golden_dir):
     x, pdf, params = models.c1()
     ds = models.dataset([x], [g["x"]])
     backend = pf.DeviceBackend()
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     columns = {"x": ds.column("x")}
     ranges = backend.chunk_ranges(ds.n_events)
     chunks = backend.map(lambda *a: None, [(pdf, columns, snap, norms, a, b, backend.block) for a, b in ranges])
@@ -288,9 +291,9 @@ def test_c1_uncertified_blocks_take_the_exact_fixup(pf, alpha):
     rng = np.random.default_rng(12)
     n = 9 * 4096 + 99
     xs = np.clip(np.concatenate([rng.normal(5.0, 0.5, n // 2), rng.uniform(0.0, 10.0, n - n // 2)]), 0, 10)
-    x = pf.Variable.observable("x", 0.0, 10.0)
-    pdf = pf.add_pdf([pf.gaussian(x, pf.Variable("mu", 5.0, 0.0, 10.0), pf.Variable("sigma", 0.5, 0.01, 5.0)),
-                      pf.exponential(x, pf.Variable("alpha", alpha, -50.0, 50.0))], [pf.Variable("f", 0.3, 0.0, 1.0)])
+    x = P.Variable.observable("x", 0.0, 10.0)
+    pdf = P.add_pdf([P.gaussian(x, P.Variable("mu", 5.0, 0.0, 10.0), P.Variable("sigma", 0.5, 0.01, 5.0)),
+                      P.exponential(x, P.Variable("alpha", alpha, -50.0, 50.0))], [P.Variable("f", 0.3, 0.0, 1.0)])
     ds = models.dataset([x], [xs])
     ctx = pf.device_context(0)
     before = ctx.launch_count()

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -78,8 +79,8 @@ def test_single_rank_sharded_nll_equals_nll(pf):
     (x, y), pdf, _ = models.c2()
     ds = models.dataset([x, y], [np.clip(rng.normal(5, 1, 50000), 0, 10), np.clip(rng.exponential(2.5, 50000), 0, 10)])
     sn = ShardedNll(pdf, ds, 0, 1, 0, collective="peer")
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     assert sn(snap, norms) == pf.nll(pdf, ds)
     assert sn(snap, norms) == pf.nll(pdf, ds)  # parity flips between calls
 
@@ -149,8 +150,8 @@ def test_fused_single_rank_equals_nll(pf):
     (x, y), pdf, _ = models.c2()
     ds = models.dataset([x, y], [np.clip(rng.normal(5, 1, n), 0, 10), np.clip(rng.exponential(2.5, n), 0, 10)])
     sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     ref = pf.nll(pdf, ds)
     for _ in range(5):  # parity alternates call to call
         assert sn(snap, norms) == ref
@@ -177,8 +178,8 @@ def test_fused_with_preposted_peer(pf):
     ctx = DeviceContext(0)
     try:
         plan = ctx.plan_for(pdf, ("x", "y"))
-        snap = pf.snapshot(pdf.param_closure())
-        norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+        snap = P.snapshot(pdf.param_closure())
+        norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
         vals, nv = plan.pack(snap, norms)
         # rank 1's exact partial over its shard
         st1 = ctx.store_for([np.ascontiguousarray(cx[b[1]:]), np.ascontiguousarray(cy[b[1]:])])
@@ -227,7 +228,7 @@ def test_fused_with_preposted_peer(pf):
 def test_fused_slow_path_reports_the_reference_error(pf):
     """An event with zero density: the fused call flags the slow path and the
     unfused redo raises the reference's NonPositiveDensity (global index)."""
-    from paper_1710_08826_b200 import errors as E
+    from paper_1710_08826_b200._reference import errors as E
     from paper_1710_08826_b200.sharding import ShardedNll
 
     rng = np.random.default_rng(6)
@@ -239,8 +240,8 @@ def test_fused_slow_path_reports_the_reference_error(pf):
     with pytest.raises(E.NonPositiveDensity) as ref:
         pf.nll(pdf, ds)
     sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     with pytest.raises(E.NonPositiveDensity) as got:
         sn(snap, norms)
     assert got.value.index == ref.value.index == 4321
@@ -257,19 +258,19 @@ def test_fused_single_rank_every_kernel_family(pf, cfg, n):
     if cfg == "c1":
         x, pdf, _ = models.c1()
         col = mcgen.device_sumpdf_1d(n, 5.0, 0.5, -0.3, 0.3, 0.0, 10.0, 31)
-        ds = pf.UnbinnedDataSet.from_columns([x], [col], copy=False)
+        ds = pf.DeviceDataSet.from_columns([x], [col], device=None)
     elif cfg == "c2":
         (x, y), pdf, _ = models.c2()
         cx, cy = mcgen.device_prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, 32)
-        ds = pf.UnbinnedDataSet.from_columns([x, y], [cx, cy], copy=False)
+        ds = pf.DeviceDataSet.from_columns([x, y], [cx, cy], device=None)
     else:
         terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
         a, b = mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 33)
         (o12, o13), pdf, _ = models.c3()
-        ds = pf.UnbinnedDataSet.from_columns([o12, o13], [a, b], copy=False)
+        ds = pf.DeviceDataSet.from_columns([o12, o13], [a, b], device=None)
     ref = pf.nll(pdf, ds)
     sn = ShardedNll(pdf, ds, 0, 1, 0, collective="fused")
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     for _ in range(3):
         assert sn(snap, norms) == ref

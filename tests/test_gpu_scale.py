@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -34,8 +35,8 @@ def test_600m_events_whole_equals_pieces(pf):
     L.check(L.lib().pfb_gen_1d(ctx.handle, 1, 5.0, 1.0, -0.4, 0.0, 0.0, 10.0, 77, N, st), "pfb_gen_1d")
     (x, y), pdf, _ = models.c2()
     plan = ctx.plan_for(pdf, ("x", "y"))
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     vals, nv = plan.pack(snap, norms)
     out, err = ctypes.c_double(), L.PfbErr()
     L.check(L.lib().pfb_nll(ctx.handle, plan.handle, st, 0, N, 0, L.dptr(vals), len(vals), L.dptr(nv), len(nv),
@@ -59,18 +60,18 @@ def test_600m_events_whole_equals_pieces(pf):
 def test_error_index_beyond_2_31(pf):
     """NonPositiveDensity at global event 2^31 + 12345 of a 2.3e9-event range
     addressed through an index offset (the shard path)."""
-    from paper_1710_08826_b200 import errors as E
+    from paper_1710_08826_b200._reference import errors as E
 
-    x = pf.Variable.observable("x", 0.0, 1.0)
-    pdf = pf.polynomial(x, [pf.Variable("c0", 0.5, -1.0, 2.0), pf.Variable("c1", 1.0, -2.0, 2.0)])
+    x = P.Variable.observable("x", 0.0, 1.0)
+    pdf = P.polynomial(x, [P.Variable("c0", 0.5, -1.0, 2.0), P.Variable("c1", 1.0, -2.0, 2.0)])
     vals = np.linspace(0.0, 1.0, 100_000)
     ds = models.dataset([x], [vals])
     backend = pf.DeviceBackend()
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
-    pf.set_value(pdf.parameters[0], 0.0)  # p(0) = 0 at local event 0
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
+    P.set_value(pdf.parameters[0], 0.0)  # p(0) = 0 at local event 0
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     off = (1 << 31) + 12345
     with pytest.raises(E.NonPositiveDensity) as ei:
         backend.evaluate(pdf, {"x": ds.column("x")}, snap, norms, 0, ds.n_events, index_offset=off)
@@ -89,14 +90,14 @@ def test_batched_points_at_scale_equal_single(pf):
     L.check(L.lib().pfb_gen_1d(ctx.handle, 1, 5.0, 1.0, -0.4, 0.0, 0.0, 10.0, 78, n, st), "pfb_gen_1d")
     (x, y), pdf, params = models.c2()
     plan = ctx.plan_for(pdf, ("x", "y"))
-    store = pf.NormalizationStore()
+    store = P.NormalizationStore()
     snaps, norms = [], []
     for k in range(4):
-        pf.set_value(params[0], 5.0 + 0.01 * k)
-        pf.set_value(params[1], 1.0 - 0.005 * k)
-        snap = pf.snapshot(pdf.param_closure())
+        P.set_value(params[0], 5.0 + 0.01 * k)
+        P.set_value(params[1], 1.0 - 0.005 * k)
+        snap = P.snapshot(pdf.param_closure())
         snaps.append(snap)
-        norms.append(pf.resolve_norms(pdf, snap, store))
+        norms.append(P.resolve_norms(pdf, snap, store))
     vals, nv = plan.pack_batch(snaps, norms)
     out = np.empty(4)
     errs = (L.PfbErr * 4)()
@@ -120,7 +121,7 @@ def test_dalitz_100m_product_kernel_matches_reference_tree_kernel(pf):
     terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
     s12, s13 = mcgen.device_dalitz(100_000_000, terms, models.D_CHANNEL_T, 4)
     (o12, o13), pdf, _ = models.c3()
-    ds = pf.UnbinnedDataSet.from_columns([o12, o13], [s12, s13], copy=False)
+    ds = pf.DeviceDataSet.from_columns([o12, o13], [s12, s13], device=None)
     ctx = pf.device_context(0)
     fast = pf.nll(pdf, ds)
     L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, 0), "pfb_ctx_set_pipeline")

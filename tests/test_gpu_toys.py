@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -37,7 +38,7 @@ def check_stats(stats, want, keys):
 @pytest.mark.parametrize("tag,spec", [("a", dict(n_events=20000, seed=5)),
                                       ("b", dict(n_events=10001, seed=9, streams=3))])
 def test_generate_1d_equals_reference(pf, g, tag, spec):
-    from paper_1710_08826_b200.mcgen import GenSpec, generate_1d
+    from paper_1710_08826_b200.mcgen import GenSpec, generate_1d  # GenSpec: the reference's
 
     x, pdf, _ = models.c1()
     stats = {}
@@ -47,16 +48,16 @@ def test_generate_1d_equals_reference(pf, g, tag, spec):
 
 
 def test_envelope_rescan_exceeded_and_budget(pf, g):
-    from paper_1710_08826_b200 import errors as E
-    from paper_1710_08826_b200.mcgen import GenSpec, generate_1d
+    from paper_1710_08826_b200._reference import errors as E
+    from paper_1710_08826_b200.mcgen import GenSpec, generate_1d  # GenSpec: the reference's
 
-    xs = pf.Variable.observable("x", 0.0, 10.0)
-    spike = pf.gaussian(xs, pf.Variable("m", 5.00061, 0.0, 10.0), pf.Variable("s", 0.001, 1e-5, 1.0))
+    xs = P.Variable.observable("x", 0.0, 10.0)
+    spike = P.gaussian(xs, P.Variable("m", 5.00061, 0.0, 10.0), P.Variable("s", 0.001, 1e-5, 1.0))
     stats = {}
     ds = generate_1d(spike, xs, GenSpec(300, seed=2, max_attempts_factor=100000), stats)
     assert ds.column("x").tolist() == g["spike_x"].tolist()
     check_stats(stats, g["spike_stats"], ("attempts", "accepted"))
-    narrow = pf.gaussian(xs, pf.Variable("m2", 5.00061, 0.0, 10.0), pf.Variable("s2", 0.0005, 1e-5, 1.0))
+    narrow = P.gaussian(xs, P.Variable("m2", 5.00061, 0.0, 10.0), P.Variable("s2", 0.0005, 1e-5, 1.0))
     assert int(g["narrow_exceeded"][0]) == 1
     with pytest.raises(E.EnvelopeExceeded):
         generate_1d(narrow, xs, GenSpec(300, seed=2, max_attempts_factor=100000))
@@ -72,7 +73,7 @@ def test_generate_dalitz_equals_reference(pf, g, tag, spec):
 
     _, _, terms = models.c3()
     stats = {}
-    ds = generate_dalitz(terms, pf.DecayChannel(*models.D_CHANNEL_T), GenSpec(**spec), stats=stats)
+    ds = generate_dalitz(terms, P.DecayChannel(*models.D_CHANNEL_T), GenSpec(**spec), stats=stats)
     assert ds.column("s12").tolist() == g[f"dal{tag}_s12"].tolist()
     assert ds.column("s13").tolist() == g[f"dal{tag}_s13"].tolist()
     check_stats(stats, g[f"dal{tag}_stats"], ("box_draws", "in_boundary_draws", "accepted"))

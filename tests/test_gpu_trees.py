@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -36,7 +37,7 @@ def test_tree_nll_matches_reference(pf, golden_dir, name, pipeline):
     L.check(L.lib().pfb_ctx_set_pipeline(ctx.handle, pipeline), "pfb_ctx_set_pipeline")
     try:
         for scale, want in zip((0.0, 0.01, -0.02), g[f"{name}__nll"]):
-            root, obs, _ = models.build_tree(pf, models.perturb(spec, scale))
+            root, obs, _ = models.build_tree(P, models.perturb(spec, scale))
             names = sorted(obs)
             ds = models.dataset([obs[c] for c in names], [g[f"{name}__{c}"] for c in names])
             got = pf.nll(root, ds)

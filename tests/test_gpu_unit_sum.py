@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 from tests import models
+from paper_1710_08826_b200._reference import parafit as P
 
 pytestmark = pytest.mark.gpu
 
@@ -39,8 +40,8 @@ def test_simt_and_tma_unit_sums_are_bitwise_equal():
     (x, y), pdf, _ = models.c2((4.97, 1.02, -0.41))
     plan = ctx.plan_for(pdf, ("x", "y"))
     st = ctx.store_for([cx, cy])
-    snap = pf.snapshot(pdf.param_closure())
-    norms = pf.resolve_norms(pdf, snap, pf.NormalizationStore())
+    snap = P.snapshot(pdf.param_closure())
+    norms = P.resolve_norms(pdf, snap, P.NormalizationStore())
     vals, nv = plan.pack(snap, norms)
     whole = block_sums(pf, L, ctx, plan, st, vals, nv, 0, N)
     pieces = np.concatenate([block_sums(pf, L, ctx, plan, st, vals, nv, a, b)
@@ -48,7 +49,7 @@ def test_simt_and_tma_unit_sums_are_bitwise_equal():
     assert whole.shape == pieces.shape
     assert whole.tobytes() == pieces.tobytes()
     # and the NLL of the whole equals the exact sum of the pieces' NLL partials
-    ds = pf.UnbinnedDataSet.from_columns([x, y], [cx, cy], copy=False)
+    ds = pf.DeviceDataSet.from_columns([x, y], [cx, cy], device=None)
     total = pf.nll(pdf, ds)
     from paper_1710_08826_b200 import sharding
 

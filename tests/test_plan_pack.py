@@ -8,7 +8,9 @@ import types
 
 import numpy as np
 
-from paper_1710_08826_b200.core import ParameterSnapshot, Variable
+from paper_1710_08826_b200._reference import core as _core
+
+ParameterSnapshot, Variable = _core.ParameterSnapshot, _core.Variable
 from paper_1710_08826_b200.plan import Plan
 
 

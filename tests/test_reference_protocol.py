@@ -1,5 +1,5 @@
-"""The drop-in boundary against the REAL reference (builder container only:
-skipped where /root/reference is absent, e.g. on the GPU box).
+"""The drop-in boundary against the REAL reference (the unmodified parafit
+installed in baseline/_ref), on CPU.
 
 The reference's own `parafit.engine.nll` (engine.py:214-243) is driven with a
 backend whose protocol methods are DeviceBackend's (`block`, `chunk_ranges`,
@@ -11,7 +11,6 @@ that `math.fsum([total]) == total` hands the device total back unchanged.
 
 import math
 import os
-import sys
 
 import numpy as np
 import pytest
@@ -19,8 +18,6 @@ import pytest
 from oracle import parafit_oracle as O
 from tests import models
 
-REF = "/root/reference/pkg/src"
-pytestmark = pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present (GPU box)")
 
 
 class ProtocolBackend:
@@ -42,13 +39,9 @@ class ProtocolBackend:
 
 
 def _reference():
-    if REF not in sys.path:
-        sys.path.insert(0, REF)
-    import parafit.core as core
-    import parafit.engine as engine
-    import parafit.pdf as rpdf
+    from paper_1710_08826_b200._reference import core, engine, pdf
 
-    return core, engine, rpdf
+    return core, engine, pdf
 
 
 def test_reference_nll_through_the_backend_protocol():
