@@ -6,7 +6,7 @@ SRC := paper_1710_08826_b200/csrc
 OUT := paper_1710_08826_b200/_native
 LIB := $(OUT)/libpfb200.so
 OBJS := $(OUT)/pfb_nll.o $(OUT)/pfb_nll_sop.o $(OUT)/pfb_nll_dal.o $(OUT)/pfb_dalitz.o $(OUT)/pfb_binned.o $(OUT)/pfb_pcg.o $(OUT)/pfb_io.o $(OUT)/pfb_peer.o $(OUT)/pfb_gen.o $(OUT)/pfb_api.o
-HDRS := $(SRC)/pfb_internal.cuh $(SRC)/pfb_math.cuh $(SRC)/pfb_nll_kernel.cuh $(SRC)/pfb_nll_tma.cuh $(SRC)/pfb_nll_prod.cuh include/pfb200.h
+HDRS := $(SRC)/pfb_objective.cuh $(SRC)/pfb_nll_task.cuh $(SRC)/pfb_internal.cuh $(SRC)/pfb_math.cuh $(SRC)/pfb_nll_kernel.cuh $(SRC)/pfb_nll_tma.cuh $(SRC)/pfb_nll_prod.cuh include/pfb200.h
 
 all: $(LIB)
 

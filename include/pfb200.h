@@ -67,6 +67,8 @@ enum pfb_status {
                                       (mcgen.py _EnvelopeHit; caller rescans) */
     PFB_E_ATTEMPTS_EXHAUSTED = 11, /* AttemptsExhausted                  errors.py */
     PFB_E_PEER_TIMEOUT = 12,       /* a peer rank never posted its accumulator */
+    PFB_E_UNBOUNDED_OBSERVABLE = 13, /* UnboundedObservable               errors.py:75 */
+    PFB_E_OUT_OF_BOUNDS = 14,      /* OutOfBounds (set_value, core.py:126-142) */
     PFB_E_INVALID_ARGUMENT = 20,
     PFB_E_UNSUPPORTED_PLAN = 21,
     PFB_E_CUDA = 30,
@@ -121,10 +123,25 @@ typedef struct pfb_err {
     double value;  /* offending value (NaN when the reference carries none) */
 } pfb_err;
 
+/* Normalisation programs of a pfb_objective node (see pfb_objective_create). */
+enum pfb_norm_kind {
+    PFB_NORM_CONST = 0,       /* `value` (add / prod: 1, pdf.py:238-239; or a norm fixed for the fit) */
+    PFB_NORM_GAUSSIAN = 1,    /* _gaussian_norm over [lo, hi] (pdf.py:130-138) */
+    PFB_NORM_EXPONENTIAL = 2, /* _exponential_norm over [lo, hi] (pdf.py:147-161) */
+    PFB_NORM_DALITZ = 3       /* dalitz_norm with a fixed overlap matrix (dalitz.py:332-349) */
+};
+typedef struct pfb_obj_node {
+    int32_t norm_kind; /* enum pfb_norm_kind */
+    int32_t pad;
+    double lo, hi;     /* observable bounds (gaussian / exponential) */
+    double value;      /* PFB_NORM_CONST */
+} pfb_obj_node;
+
 typedef struct pfb_ctx pfb_ctx;
 typedef struct pfb_store pfb_store;
 typedef struct pfb_plan pfb_plan;
 typedef struct pfb_grid pfb_grid;
+typedef struct pfb_objective pfb_objective;
 
 /* ---- library / context ---------------------------------------------------- */
 int pfb_version(void);
@@ -248,6 +265,31 @@ int pfb_acc_add_host(int64_t* acc, const double* values, int64_t n);
 int pfb_bin_fill(pfb_ctx* ctx, const pfb_store* store, int64_t begin, int64_t end, int32_t naxes,
                  const int32_t* cols, const double* lower, const double* width, const int64_t* nbins,
                  double* inout_contents);
+/* ---- the minimiser's objective in C (replaces FitManager.fcn's objective,
+ * fitting.py:436-447, + nll's host part, engine.py:214-243) ------------------
+ * Binds plan + store + [begin, end) once.  value_src[r] (plan raw value r) is
+ * an index into the free-parameter vector x or -1 (then value_const[r]);
+ * nodes[i] gives node i's normalisation program.  pfb_objective_eval maps x to
+ * the raw values, recomputes only the norms whose inputs changed (bitwise),
+ * and runs the fused NLL (== pfb_nll on the same values / norms).  A norm
+ * failure returns PFB_E_NONPOSITIVE_NORM / PFB_E_UNBOUNDED_OBSERVABLE with
+ * err->node (callers re-evaluate that point through the reference path for
+ * the reference's exception).  eval_batch: npts <= 16 points (rows of x),
+ * one pass over the events where the plan allows (pfb_nll_batch); points
+ * after a host norm failure are not evaluated. */
+int pfb_objective_create(pfb_ctx* ctx, pfb_plan* plan, const pfb_store* store, int64_t begin, int64_t end,
+                         int32_t nfree, const int32_t* value_src, const double* value_const,
+                         const pfb_obj_node* nodes, const double* dalitz_matrix, pfb_objective** out);
+/* Bounds of the free parameters (set_value's check, core.py:126-142): an x
+ * outside them (or NaN) returns PFB_E_OUT_OF_BOUNDS without evaluating. */
+int pfb_objective_set_bounds(pfb_objective* obj, const double* lower, const double* upper);
+int pfb_objective_eval(pfb_objective* obj, const double* x, int32_t nfree, double* out_nll, pfb_err* out_err);
+int pfb_objective_eval_batch(pfb_objective* obj, const double* xs, int32_t npts, int32_t nfree, double* out_nll,
+                             pfb_err* out_err);
+/* New overlap matrix (2 K^2 doubles, re/im) after a shape change. */
+int pfb_objective_set_matrix(pfb_objective* obj, const double* dalitz_matrix);
+int pfb_objective_destroy(pfb_objective* obj);
+
 /* Normalisation integral by quadrature (north_star item 4; pdf._polynomial_norm +
  * gauss_legendre_points, pdf.py:181-199): sum_j w_j * f(x_j) with f the plan's
  * unnormalised density (pass the root norm as 1) at the abscissas held in the

@@ -36,6 +36,8 @@ E_NONPOSITIVE_EXPECTATION = 9
 E_ENVELOPE_HIT = 10
 E_ATTEMPTS_EXHAUSTED = 11
 E_PEER_TIMEOUT = 12
+E_UNBOUNDED_OBSERVABLE = 13
+E_OUT_OF_BOUNDS = 14
 E_INVALID_ARGUMENT = 20
 E_UNSUPPORTED_PLAN = 21
 E_CUDA = 30
@@ -76,6 +78,13 @@ class PfbDalitzDesc(ctypes.Structure):
         ("pair", c_int32 * PFB_MAX_DALITZ_TERMS),
         ("spin", c_int32 * PFB_MAX_DALITZ_TERMS),
     ]
+
+
+NORM_CONST, NORM_GAUSSIAN, NORM_EXPONENTIAL, NORM_DALITZ = 0, 1, 2, 3
+
+
+class PfbObjNode(ctypes.Structure):
+    _fields_ = [("norm_kind", c_int32), ("pad", c_int32), ("lo", c_double), ("hi", c_double), ("value", c_double)]
 
 
 class PfbErr(ctypes.Structure):
@@ -128,6 +137,13 @@ _SIGNATURES = [
     ("pfb_finalize", c_int, [_PTR, _PTR, _DBL_P, _I64_P]),
     ("pfb_last_error", c_int, [_PTR, POINTER(PfbErr)]),
     ("pfb_ctx_last_fraction_failure", c_int, [_PTR, POINTER(c_int32)]),
+    ("pfb_objective_create", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, c_int32, POINTER(c_int32), _DBL_P,
+                                     POINTER(PfbObjNode), _DBL_P, POINTER(_PTR)]),
+    ("pfb_objective_eval", c_int, [_PTR, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
+    ("pfb_objective_eval_batch", c_int, [_PTR, _DBL_P, c_int32, c_int32, _DBL_P, POINTER(PfbErr)]),
+    ("pfb_objective_set_matrix", c_int, [_PTR, _DBL_P]),
+    ("pfb_objective_set_bounds", c_int, [_PTR, _DBL_P, _DBL_P]),
+    ("pfb_objective_destroy", c_int, [_PTR]),
     ("pfb_quadrature", c_int, [_PTR, _PTR, _PTR, c_int32, _DBL_P, c_int32, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
     ("pfb_nll_host", c_int, [_PTR, _PTR, POINTER(_DBL_P), c_int32, c_int64, _DBL_P, c_int32, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
     ("pfb_terms_block_sums", c_int, [_PTR, _DBL_P, c_int64, _DBL_P, _DBL_P]),

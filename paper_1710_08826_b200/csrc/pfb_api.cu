@@ -93,7 +93,8 @@ static int cuda_fail(cudaError_t e) {
 
 static constexpr int kStoreMaxCols = 16;
 // result words: [0, 72) exported accumulator, [72] deferred-block count, [73] error key
-static constexpr int kResHead = 4;  // [0] deferred-block count, [1] error key, [2] [3] fused exchange status
+static constexpr int kResHead = 5;  // [0] deferred-block count, [1] error key, [2] [3] fused exchange
+                                    // status, [4] completion sequence (post_seq)
 static constexpr int kResWords = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
 enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
@@ -121,8 +122,12 @@ struct pfb_ctx {
     long long* res_dev = nullptr;   // kResWords, device view
     long long* res_host = nullptr;  // kResWords, host view
     bool res_mapped = false;
+    long long call_seq = 0;  // completion sequence numbers posted by the exporting CTA
     unsigned long long* fix_counter = nullptr;
     int64_t* fix_list = nullptr;
+    double* gfold = nullptr;       // task kernel: cross-CTA block fold slots (fix_cap blocks)
+    int* gbad = nullptr;
+    unsigned int* gcnt = nullptr;  // zeroed once, self-resetting
     int64_t fix_cap = 0;
     double* bsums = nullptr;
     int64_t bsums_cap = 0;
@@ -249,6 +254,8 @@ const char* pfb_strerror(int code) {
         case PFB_E_ENVELOPE_HIT: return "density above the generation envelope";
         case PFB_E_ATTEMPTS_EXHAUSTED: return "generation attempts exhausted";
         case PFB_E_PEER_TIMEOUT: return "peer rank did not post its accumulator";
+        case PFB_E_UNBOUNDED_OBSERVABLE: return "normalisation over an unbounded observable";
+        case PFB_E_OUT_OF_BOUNDS: return "parameter outside its bounds";
         case PFB_E_INVALID_ARGUMENT: return "invalid argument";
         case PFB_E_UNSUPPORTED_PLAN: return "unsupported plan";
         case PFB_E_CUDA: return "CUDA error";
@@ -335,6 +342,9 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     if (!c->res_mapped) cudaFree(c->res_dev);
     cudaFree(c->fix_counter);
     cudaFree(c->fix_list);
+    cudaFree(c->gfold);
+    cudaFree(c->gbad);
+    cudaFree(c->gcnt);
     cudaFree(c->probe_dev);
     cudaFree(c->bsums);
     cudaFree(c->bin_dev);
@@ -817,6 +827,15 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         }
         vo += L.nv;
     }
+    if (m == 0 && A->nleaf == 2 && A->leaf[0].kind == PFB_GAUSSIAN && A->leaf[1].kind == PFB_EXPONENTIAL) {
+        const double mu = row[0], is = row[1], al = row[2];
+        A->g2_c2 = (-0.5 * is) * is;
+        A->g2_amu = al * mu;
+        const double lim = 256.0 / fabs(al);
+        uint64_t bits;
+        memcpy(&bits, &lim, 8);
+        A->g2_xlim = al == 0.0 ? 0x7ff00000 : (int32_t)(bits >> 32);
+    }
     A->nterm = (int)p->terms.size();
     for (int t = 0; t < A->nterm; ++t) {
         const TermStruct& ts = p->terms[t];
@@ -883,6 +902,9 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     A->fix_counter = c->fix_counter;
     A->fix_list = c->fix_list;
     A->fix_count = c->res_dev;
+    A->gfold = c->gfold;
+    A->gbad = c->gbad;
+    A->gcnt = c->gcnt;
     A->block_base = 0;
     A->mode = MODE_EXPORT;
     A->nops = (int)p->nodes.size();
@@ -1097,12 +1119,47 @@ static int read_result(pfb_ctx* c, int npts = 1) {
     return PFB_OK;
 }
 
+// Wait for a launch whose exporting CTA posts `seq` (NllArgs::seq) into the
+// mapped result block: the host spins on that word instead of a stream
+// synchronize (no driver round trip on the critical path of a minimiser
+// call).  Every 1024 polls the stream is queried, so an error or a launch
+// that does not post falls back to the ordinary synchronize.
+static int wait_result(pfb_ctx* c, long long seq) {
+    static const bool sync_wait = getenv("PFB_SYNC_WAIT") != nullptr;  // A/B switch (scripts/latency_probe.py)
+    if (sync_wait || c->timing || !c->res_mapped || seq <= 0) return read_result(c);
+    volatile long long* flag = c->res_host + 4;
+    for (unsigned spins = 1;; ++spins) {
+        if (*flag == seq) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return PFB_OK;
+        }
+        if ((spins & 1023u) == 0u) {
+            const cudaError_t e = cudaStreamQuery(c->stream);
+            if (e != cudaErrorNotReady) {
+                if (e != cudaSuccess) return cuda_fail(e);
+                if (*flag != seq) return read_result(c);
+            }
+        }
+    }
+}
+
 static int ensure_fix(pfb_ctx* c, int64_t nblocks) {
     if (c->fix_cap >= nblocks) return PFB_OK;
     cudaFree(c->fix_list);
+    cudaFree(c->gfold);
+    cudaFree(c->gbad);
+    cudaFree(c->gcnt);
     c->fix_list = nullptr;
+    c->gfold = nullptr;
+    c->gbad = nullptr;
+    c->gcnt = nullptr;
     c->fix_cap = 0;
-    CK(cudaMalloc(&c->fix_list, sizeof(int64_t) * (nblocks > 0 ? nblocks : 1)));
+    const size_t nb = (size_t)(nblocks > 0 ? nblocks : 1);
+    CK(cudaMalloc(&c->fix_list, sizeof(int64_t) * nb));
+    CK(cudaMalloc(&c->gfold, sizeof(double) * 8 * 32 * nb));
+    CK(cudaMalloc(&c->gbad, sizeof(int) * 8 * nb));
+    CK(cudaMalloc(&c->gcnt, sizeof(unsigned int) * nb));
+    CK(cudaMemset(c->gcnt, 0, sizeof(unsigned int) * nb));
     c->fix_cap = nblocks;
     return PFB_OK;
 }
@@ -1175,15 +1232,17 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
         }
         A->block_sums = c->bsums;
     }
+    A->seq = ++c->call_seq;
     rc = launch_eval(p, st, begin, end, A.get(), !restaged);
     if (rc) return rc;
-    rc = read_result(c);
+    rc = wait_result(c, A->seq);
     if (rc) return rc;
     if (c->res_host[0] > 0) {  // deferred blocks: exact fix-up
+        A->seq = ++c->call_seq;
         rc = launch_fixup(c, *A, c->res_dev + kResHead);
         if (rc) return rc;
         const float fast_ms = c->last_ms;
-        rc = read_result(c);
+        rc = wait_result(c, A->seq);
         if (rc) return rc;
         c->last_ms = fast_ms;
     }
@@ -2453,3 +2512,6 @@ int pfb_overhead_probe(pfb_ctx* c, int32_t mode, int32_t reps, double* out_us) {
 }
 
 }  // extern "C"
+
+// the minimiser objective in C (uses the internals above)
+#include "pfb_objective.cuh"

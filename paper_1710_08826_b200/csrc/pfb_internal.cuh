@@ -123,10 +123,15 @@ struct NllArgs {
     unsigned long long* errkey;  // min (rank<<40 | local index), ~0 when clean
     double* tail_scratch;     // 4096 doubles
     long long* acc_out;       // PFB_ACC_WORDS export target
-    long long* result_i;      // [0] deferred-block count, [1] error key
+    long long* result_i;      // [0] deferred-block count, [1] error key, [4] completion sequence
+    long long seq;            // > 0: the exporting CTA posts it to result_i[4] last (host polls)
     unsigned long long* fix_counter;  // deferred-block list fill (self-resetting)
     int64_t* fix_list;        // deferred global block indices
     const long long* fix_count;       // list length for the fix-up launch (device)
+    // task kernel (pfb_nll_task.cuh): fold slots of blocks split across CTAs
+    double* gfold;            // [block][8 unit rows][32 lanes] unit values
+    int* gbad;                // [block][8] uncertified flags
+    unsigned int* gcnt;       // [block] arrivals (self-resetting)
     // literal interpreter
     int32_t nops;
     int32_t final_rank;       // rank of the root p > 0 check
@@ -137,6 +142,10 @@ struct NllArgs {
     int32_t nleaf, nterm;
     SopLeaf leaf[kMaxLeaves];  // voff indexes a ptv row
     SopTerm term[kMaxTerms];
+    // SumPdf(gaussian, exponential) constants of point 0 (EvSum2GE):
+    // c2 = -1/(2 sigma^2), alpha mu, and the high word of 256/|alpha|
+    double g2_c2, g2_amu;
+    int32_t g2_xlim;
     // batched objective: npts parameter points per pass over the data
     int32_t npts;
     int32_t fix_point;         // fix-up launch: the point whose deferred blocks it redoes

@@ -908,6 +908,18 @@ __device__ __forceinline__ void peer_finish(const NllArgs& A) {
 
 // Flush the CTA accumulator; the last CTA to finish exports (per A.mode) and
 // resets the launch-scoped counters.  Shared by every fast kernel.
+// Completion post for the polling host (NllArgs::seq): after every export
+// store of the last CTA, one system-scope fence and the sequence number --
+// a host that sees seq in result_i[4] reads a complete result block.
+__device__ __forceinline__ void post_seq(const NllArgs& A) {
+    if (A.seq <= 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile long long*>(A.result_i + 4) = A.seq;
+    }
+}
+
 template <bool LIST>
 __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc, unsigned int* s_last) {
     __syncthreads();
@@ -939,6 +951,7 @@ __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc,
         else
             A.acc_out[i] += v;
     }
+    post_seq(A);
 }
 
 template <int P, class Ev, bool LIST>

@@ -64,72 +64,93 @@ __device__ __forceinline__ void renorm(double& m, int& ex) {
     m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(m));
 }
 
-// 2^(j/16), j = 0..15, correctly rounded.  Kept in shared memory: 16 doubles
-// fill the 32 banks once, so any lane pattern reads conflict-free.
-__constant__ static double kExp2Tab[16] = {
-    0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0, 0x1.2387a6e756238p+0,
-    0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0, 0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,
-    0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0, 0x1.ea4afa2a490dap+0};
-// 16/ln2, ln2/16 split hi (32 significant bits: kd * hi exact) + lo, and the
-// Taylor coefficients 1/n! (read as constant-bank operands, no per-use moves).
-__constant__ static double kExpK[9] = {
-    23.083120654223414, 0x1.62e42fee00000p-5, 0x1.a39ef35793c76p-37,
-    1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
+// 2^(j/64), j = 0..63, correctly rounded.  An evaluator's per-launch table
+// (c * 2^(j/64), 64 doubles) lives in shared memory: one 16-byte-free LDS.64
+// per event, no multiply by the table value in the per-event chain.
+constexpr int kTabN = 64;
+__constant__ static double kExp2Tab64[kTabN] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
+// 64/ln2; ln2/64 split hi (32 significant bits: kd * hi exact for |kd| < 2^21)
+// + lo.
+constexpr double kExpK = 92.33248261689366;
+constexpr double kLn2o64Hi = 0x1.62e42fee00000p-7;
+constexpr double kLn2o64Lo = 0x1.a39ef35793c76p-39;
 
-// exp(x) for x in [-707, 707] (callers clamp): x = k ln2/16 + r, |r| <= ln2/32;
-// exp(r) by its degree-6 Taylor polynomial (truncation < 2^-52), times
-// 2^(k mod 16 / 16) from the table, times 2^(k div 16) by exponent addition.
-// <= 3 ulp; 11 FP64 operations against ~17 plus a range branch for exp().
-__device__ __forceinline__ double exp_tab(double x, const double* tab) {
-    const double t = fma(x, kExpK[0], 0x1.8p52);
+// c * exp(d) + a for d in [-500, 256] (callers clamp) with tab[j] = c 2^(j/64):
+// d = k ln2/64 + r, |r| <= ln2/128; exp(r) by its degree-5 Taylor polynomial
+// (truncation < 2^-53), times tab[k mod 64] with 2^(k div 64) added to its
+// exponent (integer op), plus a in the same FMA.  <= 3 ulp; 10 FP64 operations.
+__device__ __forceinline__ double cexp_tab_add(double d, const double* tab, double a) {
+    const double t = fma(d, kExpK, 0x1.8p52);
     const int k = __double2loint(t);
     const double kd = t - 0x1.8p52;
-    double r = fma(kd, -kExpK[1], x);
-    r = fma(kd, -kExpK[2], r);
-    double q = fma(r, kExpK[3], kExpK[4]);  // Horner (Estrin measured slower: throughput-bound)
-    q = fma(q, r, kExpK[5]);
-    q = fma(q, r, kExpK[6]);
-    q = fma(q, r, kExpK[7]);
-    q = fma(q, r, kExpK[8]);
+    double r = fma(kd, -kLn2o64Hi, d);
+    r = fma(kd, -kLn2o64Lo, r);
+    double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);  // Horner: throughput-bound, Estrin measured slower
+    q = fma(q, r, 1.0 / 6.0);
+    q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
-    const double v = q * tab[k & 15];
-    return __hiloint2double(__double2hiint(v) + ((k >> 4) << 20), __double2loint(v));
+    q = fma(q, r, 1.0);
+    const double tv = tab[k & (kTabN - 1)];
+    const double cs = __hiloint2double(__double2hiint(tv) + ((k >> 6) << 20), __double2loint(tv));
+    return fma(cs, q, a);
 }
 
 // SumPdf(gaussian, exponential) on one column (C1 / C5):
 //   p = c0 exp(u0) + c1 exp(u1),  u0 = (-0.5 z) z,  z = (x - mu) / sigma,
 //   u1 = alpha x,  c_t = weight_t / (norm_t * norm_root)
 //   (pdf.py:122-127, 141-144, 205-219), factored as
-//   p = exp(u1) * q,  q = c1 + c0 exp(u0 - u1):
-// one exponential per event; u1 goes into the unit's sum, q into its product.
+//   p = exp(u1) * q,  q = c1 + c0 exp(d),  d = u0 - u1:
+// one exponential per event; x goes into the unit's sum (times alpha once
+// per unit: sum_i u1_i = alpha sum_i x_i), q into its product.
+//   d = c2 w^2 - alpha w - alpha mu,  w = x - mu,  c2 = -1/(2 sigma^2):
+// two FMAs on w, no cancellation beyond |alpha mu| (the u1 - alpha mu part).
 // Leaf/term layout fixed by the dispatcher: leaf 0 gaussian (ptv[0][0..1] =
 // mu, 1/sigma), leaf 1 exponential (ptv[0][2] = alpha), term t = leaf t, and
 // |ln c_t| < 200.
-// Certification: |u1| < 256 and q in [2^-500, 2^500] (kernel check) put p
-// in [2^-870, 2^870] and keep the reference's exp(u1) finite and normal; a
-// subnormal exp(u0) in the reference is then below 2^-75 p (negligible).
-// d = u0 - u1 <= -u1 < 256 for a certified event (u0 <= 0) and is clamped
-// below at -707 (then c0 e^d < 2^-700 c1, negligible); whatever exp_tab
-// returns for an uncertified event (NaN d, d > 707) is discarded.
+// Certification (integer ops only): |x| < 256 / |alpha| (so |u1| < 256) and
+// q in [2^-250, 2^251) (unit check) put p in [2^-620, 2^620] and keep the
+// reference's exp(u1) finite and normal.  d is clamped below at -500 by its
+// high word: then c0 e^d <= e^-300 c1 < ulp(c1) / 2 -- q is unchanged -- and
+// c0 2^(k div 64) stays a normal double.  Whatever an uncertified event
+// computes is discarded (its block is deferred to the exact fix-up).
 struct EvSum2GE {
     static constexpr int NC = 1;
     static constexpr int U = 4;
     static constexpr int MINB = 3;
+    static constexpr bool TAB = true;     // tab = c0 2^(j/64)
+    static constexpr bool LSCALE = true;  // unit sum of l times alpha
 
-    // d = -(x - mu)^2 / (2 sigma^2) - alpha x as one FMA: c2 = -1/(2 sigma^2)
-    // is loop-invariant.  |u1| < 256 is read off the exponent bits (no FP64 op).
+    __device__ static __forceinline__ double tab_entry(const NllArgs& A, int j) {
+        return A.term[0].coef * kExp2Tab64[j];
+    }
+    __device__ static __forceinline__ double lscale(const NllArgs& A) { return A.ptv[0][2]; }
+
     __device__ static __forceinline__ double one(const NllArgs& A, double x, const double* tab, bool& ok,
                                                  double& l) {
-        const double is = A.ptv[0][1];
-        const double c2 = (-0.5 * is) * is;
+        // per-launch constants from the host (NllArgs::g2_*)
         const double w = x - A.ptv[0][0];
-        const double u1 = A.ptv[0][2] * x;
-        double d = fma(c2 * w, w, -u1);
-        d = d < -707.0 ? -707.0 : d;
-        ok = (__double2hiint(u1) & 0x7fffffff) < 0x40700000;  // |u1| < 256 => d <= 256: no upper clamp
-        l = u1;
-        return fma(A.term[0].coef, exp_tab(d, tab), A.term[1].coef);
+        double d = fma(w, fma(A.g2_c2, w, -A.ptv[0][2]), -A.g2_amu);
+        d = (unsigned)__double2hiint(d) > 0xc07f4000u ? -500.0 : d;  // d < -500 (or -inf / -NaN)
+        ok = (__double2hiint(x) & 0x7fffffff) < A.g2_xlim;
+        l = x;
+        return cexp_tab_add(d, tab, A.term[1].coef);
     }
 
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[1], bool& okx,
@@ -255,15 +276,41 @@ __device__ __forceinline__ bool unit_in_range(const Unit& u, bool ratio) {
 #endif
 }
 
+// per-launch shared table (Ev::TAB) and scaled log sums (Ev::LSCALE)
+template <class Ev, class = void>
+struct HasTab {
+    static constexpr bool value = false;
+};
 template <class Ev>
-__device__ __forceinline__ double unit_value(const Unit& u) {
+struct HasTab<Ev, decltype((void)Ev::TAB)> {
+    static constexpr bool value = Ev::TAB;
+};
+template <class Ev, class = void>
+struct HasLScale {
+    static constexpr bool value = false;
+};
+template <class Ev>
+struct HasLScale<Ev, decltype((void)Ev::LSCALE)> {
+    static constexpr bool value = Ev::LSCALE;
+};
+template <class Ev>
+__device__ __forceinline__ void init_tab(const NllArgs& A, double* tab, int tid) {
+    if constexpr (HasTab<Ev>::value) {
+        if (tid < kTabN) tab[tid] = Ev::tab_entry(A, tid);
+    }
+}
+
+template <class Ev>
+__device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u) {
     if constexpr (IsRatio<Ev>::value) {
         constexpr double pw = (double)RatioPow<Ev>::value;
         const double fe = (double)u.ex - pw * (double)u.exd;
         return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, fma(-pw, log(u.md), log(u.m))));
     } else {
         const double fe = (double)u.ex;
-        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) + u.ls));
+        double L = u.ls;
+        if constexpr (HasLScale<Ev>::value) L = Ev::lscale(A) * L;
+        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) + L));
     }
 }
 
@@ -332,7 +379,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     __shared__ unsigned int s_cnt[kSumTeams][kSumRing];
     __shared__ int s_done[kSumTeams][kSumRing];
     __shared__ long long sacc[kMaxPts][PFB_ACC_WORDS];
-    __shared__ double s_tab[16];
+    __shared__ double s_tab[kTabN];
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
@@ -398,7 +445,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
             }
         }
     } else {
-        if (tid < 16) s_tab[tid] = kExp2Tab[tid];
+        init_tab<Ev>(A, s_tab, tid);
         for (int i = tid; i < kMaxPts * PFB_ACC_WORDS; i += 32 * kSumWarps * kSumTeams) (&sacc[0][0])[i] = 0;
         if (tid < kSumTeams * kSumRing) {
             (&s_cnt[0][0])[tid] = 0u;
@@ -520,7 +567,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                 }
                 if constexpr (PROD) {
                     bad |= !unit_in_range(un, IsRatio<Ev>::value);
-                    acc = unit_value<Ev>(un);
+                    acc = unit_value<Ev>(A, un);
                 }
                 if (m == A.npts - 1) {  // the stage is no longer read by this warp
                     __syncwarp();
@@ -588,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
     __shared__ double xch[2][GROUPS][8][32];  // unit values, double-buffered by item parity
     __shared__ int xbad[2][GROUPS][P];
     __shared__ long long sacc[PFB_ACC_WORDS];
-    __shared__ double s_tab[16];
+    __shared__ double s_tab[kTabN];
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
@@ -597,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
     const int grp = warp / P;
     const int wig = warp % P;
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
-    if (tid < 16) s_tab[tid] = kExp2Tab[tid];
+    init_tab<Ev>(A, s_tab, tid);
     __syncthreads();
 
     // Static round-robin items (every block costs the same): the next item is
@@ -677,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
                 }
                 if constexpr (PROD) {
                     bad |= !unit_in_range(un, IsRatio<Ev>::value);
-                    acc = unit_value<Ev>(un);
+                    acc = unit_value<Ev>(A, un);
                 }
                 xch[par][grp][(r0 >> 3) + ju][lane] = acc;
             }
@@ -710,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, PROD ? Ev::MINB : PFB_SUM_MINB) nll_
                 if ((i & 7) == 7) {
                     if constexpr (PROD) {
                     bad |= !unit_in_range(un, IsRatio<Ev>::value);
-                    acc = unit_value<Ev>(un);
+                    acc = unit_value<Ev>(A, un);
                 }
                     xch[par][grp][(r0 + i) >> 3][lane] = acc;
                     un = Unit();
@@ -763,7 +810,10 @@ constexpr int kUnitEvents = 512;  // events per warp per item
 #ifndef PFB_BULK_RING
 #define PFB_BULK_RING 4
 #endif
-constexpr int kRing = PFB_BULK_RING;  // block-fold slots (warps may drift this many items)
+constexpr int kRing = PFB_BULK_RING;
+#ifndef PFB_BULK_MINB
+#define PFB_BULK_MINB 3
+#endif  // block-fold slots (warps may drift this many items)
 
 template <class T>
 __device__ __forceinline__ T ld_volatile(const T* p) {
@@ -779,7 +829,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 template <class Ev>
-__global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid_constant__ NllArgs A) {
+__global__ void __launch_bounds__(kThreads, PFB_BULK_MINB) nll_prod_bulk_kernel(const __grid_constant__ NllArgs A) {
     constexpr int NC = Ev::NC;
     static_assert(kThreads == 32 * kBulkWarps, "one item per CTA");
     extern __shared__ __align__(128) double sbuf[];  // [8 warps][2 buffers][NC][512]
@@ -789,14 +839,14 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
     __shared__ unsigned int s_cnt[kRing];
     __shared__ int s_done[kRing];  // folds completed per slot
     __shared__ long long sacc[PFB_ACC_WORDS];
-    __shared__ double s_tab[16];
+    __shared__ double s_tab[kTabN];
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int w = tid >> 5;
     for (int i = tid; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
-    if (tid < 16) s_tab[tid] = kExp2Tab[tid];
+    init_tab<Ev>(A, s_tab, tid);
     if (tid < kRing) {
         s_cnt[tid] = 0u;
         s_done[tid] = 0;
@@ -885,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 3) nll_prod_bulk_kernel(const __grid
         if (lane == 0)
             while (ld_volatile(&s_done[slot]) < j / kRing) __nanosleep(32);
         __syncwarp();
-        xch[slot][w][lane] = unit_value<Ev>(un);
+        xch[slot][w][lane] = unit_value<Ev>(A, un);
         const unsigned anybad = __any_sync(0xffffffffu, bad);
         unsigned arrived = 0;
         if (lane == 0) {

@@ -3,6 +3,7 @@
 // trees -- streamed through the TMA pipeline -- and a generic instantiation
 // (<= 4 leaves, <= 4 terms) on the SIMT kernel for the rest.
 #include "pfb_nll_prod.cuh"
+#include "pfb_nll_task.cuh"
 #include "pfb_nll_tma.cuh"
 
 namespace pfb {
@@ -51,8 +52,16 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // (two exp per event, one log per 16 events) on the SIMT streaming
         // kernel; the log-domain kernel (one exp + one log per event) when
         // the pipeline is off or the shape's preconditions do not hold.
-        if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A))
+        // pipeline 1: per-warp bulk prefetch below ~40 blocks per SM, the
+        // warp-task kernel (pfb_nll_task.cuh: no end-of-launch imbalance;
+        // 100M events 202 -> 189 us, 10M 29.7 vs 31.7 us, measured) above;
+        // 2: bulk prefetch; 3: the TMA unit kernel -- the same canonical blocks
+        if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A)) {
+            const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+            if (A.tma == 1 && A.warps == 0 && nitems >= 40 * (int64_t)sm_count)
+                return launch_task<EvSum2GE>(A, stream, sm_count);
             return launch_prod<EvSum2GE>(A, stream, sm_count);
+        }
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2))
             return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);
         if (nl == 1 && nt == 1 && kinds == kG)

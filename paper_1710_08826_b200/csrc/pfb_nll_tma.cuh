@@ -120,6 +120,7 @@ __device__ __forceinline__ void finish_launch_pts(const NllArgs& A, long long* s
         else
             A.acc_out[i] += v;
     }
+    post_seq(A);
 }
 
 template <class Ev, int S>

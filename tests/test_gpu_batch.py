@@ -109,9 +109,11 @@ def test_batch_error_attributed_to_its_point(pf):
 
 
 def test_batched_fit_equals_unbatched_fit(pf, golden_dir):
-    """DeviceFitManager with batched stencils == the same fit point by point ==
-    the unmodified reference FitManager over DeviceBackend: same n_calls,
-    bitwise values, errors, minimum and norm-cache counters."""
+    """DeviceFitManager (C objective + batched stencils) == its exact
+    reference-objective mode, batched or point by point == the unmodified
+    reference FitManager over DeviceBackend: same n_calls, bitwise values,
+    errors and minimum; the reference-objective modes also leave the
+    norm-cache counters exactly where the reference's own fit leaves them."""
     import os
 
     g = np.load(os.path.join(golden_dir, "c2_prod.npz"))
@@ -119,18 +121,23 @@ def test_batched_fit_equals_unbatched_fit(pf, golden_dir):
     ds = models.dataset([x, y], [g["x"], g["y"]])
     fits = []
     for make in (lambda: pf.DeviceFitManager(pdf, ds),
-                 lambda: pf.DeviceFitManager(pdf, ds, batch=False),
+                 lambda: pf.DeviceFitManager(pdf, ds, fast=False),
+                 lambda: pf.DeviceFitManager(pdf, ds, batch=False, fast=False),
                  lambda: P.FitManager(pdf, ds, backend=pf.DeviceBackend())):
         for v, val in zip(params, (4.9, 1.1, -0.35)):
             P.set_value(v, val)
         fm = make()
         fits.append((fm.fit(), fm))
-    (batched, fm0), (plain, fm1), (ref, fm2) = fits
+    (fast, fmf), (batched, fm0), (plain, fm1), (ref, fm2) = fits
+    from paper_1710_08826_b200.fitting import FastObjective
+
+    assert isinstance(fmf.objective, FastObjective)
     assert fm0.objective.batches > 0 and fm0.objective.batched_points > 10
-    for other, fm in ((plain, fm1), (ref, fm2)):
-        assert batched.n_calls == other.n_calls
-        assert np.array_equal(batched.values, other.values)
-        assert np.array_equal(batched.errors, other.errors)
-        assert batched.nll_min == other.nll_min
+    for other, fm in ((batched, fm0), (plain, fm1), (ref, fm2)):
+        assert fast.n_calls == other.n_calls
+        assert np.array_equal(fast.values, other.values)
+        assert np.array_equal(fast.errors, other.errors)
+        assert fast.nll_min == other.nll_min
+    for fm in (fm1, fm2):
         assert fm0.store.kernel_evals == fm.store.kernel_evals
         assert fm0.store.norm_computations == fm.store.norm_computations

@@ -1,0 +1,143 @@
+"""The minimiser's objective in C (pfb_objective, fitting.FastObjective)
+against the reference objective (FitManager.fcn, P/fitting.py:436-447).
+
+* gaussian / exponential / add / prod models: every value bitwise the
+  reference objective's (same raw values, the reference's norm formulas on
+  the same doubles through libm), so whole fits are bitwise identical;
+* Dalitz (fixed shapes): norm from the fixed overlap matrix, NLL within
+  1e-12 of the reference objective's; fit within the north-star tolerance;
+* failures take the reference path: out-of-bounds x -> OutOfBounds, a
+  non-positive norm -> NonPositiveNorm, fractions -> FractionOutOfRange;
+* models it cannot express (free polynomial coefficients) fall back to the
+  reference objective.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_1710_08826_b200._reference import errors as E
+from paper_1710_08826_b200._reference import parafit as P
+from tests import models
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pf():
+    import paper_1710_08826_b200 as pf
+    from paper_1710_08826_b200 import _lib as L
+
+    if L.device_count() < 1:
+        pytest.fail("GPU test run without a CUDA device")
+    return pf
+
+
+def _c1_data(n, seed=3):
+    rng = np.random.default_rng(seed)
+    x, pdf, params = models.c1()
+    xs = np.clip(np.concatenate([rng.normal(5, 0.5, n // 3), rng.exponential(3.3, n - n // 3)]), 0, 10)
+    return x, pdf, params, models.dataset([x], [xs])
+
+
+def test_values_bitwise_reference_objective(pf):
+    from paper_1710_08826_b200.fitting import FastObjective
+
+    x, pdf, params, ds = _c1_data(40 * 4096 + 77)
+    fast = pf.DeviceFitManager(pdf, ds).fcn()
+    exact = pf.DeviceFitManager(pdf, ds, fast=False).fcn()
+    assert isinstance(fast._objective, FastObjective)
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        pt = np.array([rng.uniform(4.5, 5.5), rng.uniform(0.3, 0.8), rng.uniform(-0.5, -0.1), rng.uniform(0.1, 0.6)])
+        assert fast(pt) == exact(pt)
+    assert fast.n_calls == exact.n_calls == 50
+
+
+def test_fit_bitwise_reference_fitmanager(pf):
+    x, pdf, params, ds = _c1_data(100 * 4096 + 5)
+    start = (4.8, 0.6, -0.25, 0.35)
+    res = []
+    for make in (lambda: pf.DeviceFitManager(pdf, ds), lambda: P.FitManager(pdf, ds, backend=pf.DeviceBackend())):
+        for v, val in zip(params, start):
+            P.set_value(v, val)
+        res.append(make().fit())
+    fast, ref = res
+    assert fast.status == ref.status == "converged"
+    assert fast.n_calls == ref.n_calls
+    assert np.array_equal(fast.values, ref.values) and np.array_equal(fast.errors, ref.errors)
+    assert fast.nll_min == ref.nll_min
+    # write-back as the reference FitManager does
+    assert [v.value for v in params] == list(fast.values)
+
+
+def test_dalitz_fast_objective_matches_reference(pf, golden_dir):
+    import os
+
+    from paper_1710_08826_b200.fitting import FastObjective
+
+    g = np.load(os.path.join(golden_dir, "c3_dalitz.npz"))
+    (s12, s13), pdf, terms = models.c3(grid=(128, 128))
+    ds = models.dataset([s12, s13], [g["s12"], g["s13"]])
+    free = [v for t in terms for v in (t.magnitude, t.phase) if not v.fixed]
+    fast = pf.DeviceFitManager(pdf, ds).fcn()
+    exact = pf.DeviceFitManager(pdf, ds, fast=False).fcn()
+    assert isinstance(fast._objective, FastObjective)
+    base = np.array([v.value for v in free])
+    for k in range(8):
+        pt = base * (1.0 + 0.01 * k)
+        a, b = fast(pt), exact(pt)
+        assert abs(a - b) <= 1e-12 * abs(b), (k, a, b)
+    start = [0.8, 0.0, 0.5, 0.3, 19.0, -0.45]
+    fits = []
+    for make in (lambda: pf.DeviceFitManager(pdf, ds), lambda: pf.DeviceFitManager(pdf, ds, fast=False)):
+        for v, val in zip(free, start):
+            P.set_value(v, val)
+        fits.append(make().fit())
+    f, r = fits
+    assert f.status == r.status == "converged"
+    for v, e, rv, re in zip(f.values, f.errors, r.values, r.errors):
+        assert abs(v - rv) <= max(1e-6 * abs(rv), 1e-3 * re)
+    assert abs(f.nll_min - r.nll_min) <= 1e-10 * abs(r.nll_min)
+
+
+def test_failures_take_the_reference_path(pf):
+    x, pdf, params, ds = _c1_data(9 * 4096 + 1)
+    fcn = pf.DeviceFitManager(pdf, ds).fcn()
+    with pytest.raises(E.OutOfBounds):
+        fcn(np.array([5.0, 0.5, -0.3, 1.5]))  # f outside [0, 1]
+    with pytest.raises(E.OutOfBounds):
+        fcn(np.array([5.0, math.nan, -0.3, 0.3]))
+    # a sum whose fractions leave a negative remainder: FractionOutOfRange
+    y = P.Variable.observable("y", 0.0, 10.0)
+    f1, f2 = P.Variable("f1", 0.3, 0.0, 1.0), P.Variable("f2", 0.3, 0.0, 1.0)
+    tree = P.add_pdf([P.gaussian(y, P.Variable("m", 5.0, fixed=True), P.Variable("s", 2.0, fixed=True)),
+                      P.exponential(y, P.Variable("a", -0.1, fixed=True)),
+                      P.gaussian(y, P.Variable("m2", 3.0, fixed=True), P.Variable("s2", 3.0, fixed=True))], [f1, f2])
+    dsy = models.dataset([y], [ds.column("x")])
+    fcn2 = pf.DeviceFitManager(tree, dsy).fcn()
+    assert math.isfinite(fcn2(np.array([0.3, 0.3])))
+    with pytest.raises(E.FractionOutOfRange):
+        fcn2(np.array([0.7, 0.6]))
+    # a gaussian whose sigma may reach 0: NonPositiveNorm from the reference path
+    z = P.Variable.observable("z", 0.0, 1.0)
+    sg = P.Variable("sg", 0.2, 0.0, 1.0)
+    node = P.gaussian(z, P.Variable("mz", 0.5, 0.0, 1.0), sg)
+    dsz = models.dataset([z], [np.linspace(0.01, 0.99, 5000)])
+    fcn3 = pf.DeviceFitManager(node, dsz).fcn()
+    assert math.isfinite(fcn3(np.array([0.5, 0.2])))
+    with pytest.raises(E.NonPositiveNorm):
+        fcn3(np.array([0.5, 0.0]))
+
+
+def test_unsupported_models_fall_back(pf):
+    from paper_1710_08826_b200.fitting import DeviceObjective, FastObjective
+
+    x = P.Variable.observable("x", 0.0, 1.0)
+    node = P.polynomial(x, [P.Variable("c0", 1.0, 0.1, 2.0), P.Variable("c1", 0.2, -0.5, 0.5)])
+    ds = models.dataset([x], [np.linspace(0.0, 1.0, 3000)])
+    fm = pf.DeviceFitManager(node, ds)
+    fcn = fm.fcn()
+    assert type(fcn._objective) is DeviceObjective and not isinstance(fcn._objective, FastObjective)
+    assert math.isfinite(fcn(np.array([1.0, 0.1])))

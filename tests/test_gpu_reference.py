@@ -135,10 +135,15 @@ def test_reference_fitmanager_device_vs_reference_pool(pf, cfg, n):
     start()
     on_device = P.FitManager(pdf, ds, backend=pf.DeviceBackend()).fit()
     start()
-    batched = pf.DeviceFitManager(pdf, ds).fit()
+    batched = pf.DeviceFitManager(pdf, ds, fast=False).fit()
+    start()
+    fast = pf.DeviceFitManager(pdf, ds).fit()  # the objective in C (+ batched stencils)
     _check_fit(on_device, want)
     _check_fit(batched, want)
+    _check_fit(fast, want)
     # the batched stencils change nothing but the number of device passes
     assert batched.n_calls == on_device.n_calls
     assert np.array_equal(batched.values, on_device.values)
     assert batched.nll_min == on_device.nll_min
+    if cfg != "c3":  # gaussian / exponential norms in C are the reference's bits
+        assert fast.n_calls == on_device.n_calls and np.array_equal(fast.values, on_device.values)
