@@ -286,6 +286,22 @@ int pfb_objective_set_bounds(pfb_objective* obj, const double* lower, const doub
 int pfb_objective_eval(pfb_objective* obj, const double* x, int32_t nfree, double* out_nll, pfb_err* out_err);
 int pfb_objective_eval_batch(pfb_objective* obj, const double* xs, int32_t npts, int32_t nfree, double* out_nll,
                              pfb_err* out_err);
+/* Persistent evaluation (on != 0): calls go through a kernel that stays
+ * resident between calls -- the call's arguments are written into a mapped
+ * pinned mailbox and a doorbell word, the kernel (one CTA per SM, polling)
+ * runs the pass and posts the result into mapped memory: no launch and no
+ * stream synchronisation per call.  Same canonical blocks, so the same bits
+ * as the one-shot kernels.  Shapes without a persistent kernel, deferred
+ * blocks (the exact fix-up) and any other device work on the context fall
+ * back to / stop it (it restarts on the next call); it also leaves by itself
+ * after 20 ms without a call.  off: stop it now. */
+int pfb_objective_set_persistent(pfb_objective* obj, int32_t on);
+/* Stop the context's resident kernel, if any. */
+int pfb_ctx_persist_stop(pfb_ctx* ctx);
+/* Diagnostics (PFB_PERSIST_TRACE set when the kernel starts): %globaltimer ns
+ * of the last call -- doorbell seen, CTAs released, last CTA starts / ends its
+ * pass, result posted. */
+int pfb_ctx_persist_trace(pfb_ctx* ctx, uint64_t* out5);
 /* New overlap matrix (2 K^2 doubles, re/im) after a shape change. */
 int pfb_objective_set_matrix(pfb_objective* obj, const double* dalitz_matrix);
 int pfb_objective_destroy(pfb_objective* obj);

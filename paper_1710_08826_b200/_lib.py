@@ -144,6 +144,9 @@ _SIGNATURES = [
     ("pfb_objective_set_matrix", c_int, [_PTR, _DBL_P]),
     ("pfb_objective_set_bounds", c_int, [_PTR, _DBL_P, _DBL_P]),
     ("pfb_objective_destroy", c_int, [_PTR]),
+    ("pfb_objective_set_persistent", c_int, [_PTR, c_int32]),
+    ("pfb_ctx_persist_stop", c_int, [_PTR]),
+    ("pfb_ctx_persist_trace", c_int, [_PTR, POINTER(ctypes.c_uint64)]),
     ("pfb_quadrature", c_int, [_PTR, _PTR, _PTR, c_int32, _DBL_P, c_int32, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
     ("pfb_nll_host", c_int, [_PTR, _PTR, POINTER(_DBL_P), c_int32, c_int64, _DBL_P, c_int32, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
     ("pfb_terms_block_sums", c_int, [_PTR, _DBL_P, c_int64, _DBL_P, _DBL_P]),

@@ -19,6 +19,8 @@
 namespace pfb {
 cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int nc);
 cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count);
+int persist_kind(const NllArgs& A, int nc);
+cudaError_t launch_persist_kind(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count);
 bool sop_batched_in_kernel(const NllArgs& A, int nc);
 cudaError_t launch_export(unsigned long long* acc, long long* out, long long* result_i,
                           unsigned long long* fix_counter, unsigned long long* errkey,
@@ -157,6 +159,21 @@ struct pfb_ctx {
     // parallel download lanes (pfb_store_download to pageable memory)
     double* dl_pinned[kDlLanes][2] = {};
     cudaStream_t dl_stream[kDlLanes] = {};
+    // persistent NLL kernel (pfb_nll_task.cuh): doorbell + mailbox in mapped
+    // pinned memory, their device copies, the kernel's own stream
+    int persist_kind = 0;                  // kind of the resident kernel (0: none)
+    cudaStream_t persist_stream = nullptr;
+    unsigned long long* persist_ctl = nullptr;      // host view [seq, op]
+    unsigned long long* persist_ctl_dev = nullptr;  // device view of the same
+    PersistBox* persist_box = nullptr;              // host view of the mailbox
+    PersistBox* persist_box_dev = nullptr;
+    NllArgs* persist_args = nullptr;                // device copy (kMaxArgChunks x 128 B)
+    unsigned int* persist_chunks = nullptr;         // device: count + changed chunk indices
+    std::unique_ptr<unsigned char[]> persist_shadow;  // the NllArgs bytes the kernel holds
+    bool persist_shadow_valid = false;
+    unsigned long long* persist_go = nullptr;       // device [seq, op]
+    unsigned long long* persist_trace = nullptr;    // mapped %globaltimer stamps of the last call (host view)
+    unsigned long long* persist_trace_dev = nullptr;
     // binned data scratch
     void* bin_dev = nullptr;  // bin counts / contents
     int64_t bin_cap = 0;      // bytes
@@ -233,6 +250,26 @@ struct pfb_grid {
     double2* amps = nullptr;
     int amps_rows = 0;
 };
+
+// The persistent kernel owns every SM while it is resident: any other device
+// work first stops it (it is restarted by the next persistent call).
+static int persist_stop(pfb_ctx* c) {
+    if (!c->persist_kind) return PFB_OK;
+    c->persist_kind = 0;
+    c->persist_ctl[1] = 1;  // op: stop
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    reinterpret_cast<volatile unsigned long long*>(c->persist_ctl)[0] = (unsigned long long)(++c->call_seq);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    CK(cudaStreamSynchronize(c->persist_stream));
+    return PFB_OK;
+}
+#define PFB_QUIESCE(c)                              \
+    do {                                            \
+        if ((c)->persist_kind) {                    \
+            const int q_ = persist_stop(c);         \
+            if (q_) return q_;                      \
+        }                                           \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -333,6 +370,16 @@ int pfb_ctx_create(int device, pfb_ctx** out) {
 int pfb_ctx_destroy(pfb_ctx* c) {
     if (!c) return PFB_OK;
     cudaSetDevice(c->device);
+    persist_stop(c);
+    if (c->persist_stream) {
+        cudaStreamDestroy(c->persist_stream);
+        cudaFreeHost(c->persist_ctl);
+        cudaFreeHost(c->persist_box);
+        cudaFree(c->persist_args);
+        cudaFree(c->persist_go);
+        cudaFree(c->persist_chunks);
+        cudaFreeHost(c->persist_trace);
+    }
     cudaStreamSynchronize(c->stream);
     cudaFree(c->acc);
     cudaFree(c->ticket);
@@ -385,6 +432,7 @@ void* pfb_ctx_stream(pfb_ctx* c) { return c ? (void*)c->stream : nullptr; }
 int pfb_ctx_synchronize(pfb_ctx* c) {
     if (!c) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     CK(cudaStreamSynchronize(c->stream));
     return PFB_OK;
 }
@@ -424,6 +472,7 @@ int pfb_ctx_last_kernel_ms(pfb_ctx* c, float* out) {
 int pfb_store_create(pfb_ctx* c, int32_t ncols, int64_t n, pfb_store** out) {
     if (!c || !out || ncols < 1 || ncols > kStoreMaxCols || n < 0) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto* s = new pfb_store();
     s->ctx = c;
     s->ncols = ncols;
@@ -458,6 +507,7 @@ int pfb_store_upload(pfb_store* s, int32_t col, const double* host, int64_t offs
     // a single pageable copy: the source pages are already resident, and the
     // driver's own staging (~10 GB/s measured) beats host_copy's lanes here
     CK(cudaSetDevice(s->ctx->device));
+    PFB_QUIESCE(s->ctx);
     store_touched(s);
     CK(cudaMemcpyAsync(s->cols[col] + offset, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                        s->ctx->stream));
@@ -1208,6 +1258,7 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
         return PFB_E_EMPTY_DATASET;
     }
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     pfb_store staged;
     const bool restaged = !range_aligned(p, st, begin);
     if (restaged) {
@@ -1290,6 +1341,7 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
         return PFB_E_EMPTY_DATASET;
     }
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     pfb_store staged;
     if (!range_aligned(p, st, begin)) {
         const int rs = restage(c, p, st, begin, end, &staged);
@@ -1367,6 +1419,7 @@ int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, i
     if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
     if (begin < 0 || end < begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     pfb_store staged;
     const bool restaged = end > begin && !range_aligned(p, st, begin);
     if (restaged) {
@@ -1399,6 +1452,7 @@ int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, i
 int pfb_finalize(pfb_ctx* c, const int64_t* dev_acc, double* out_nll, int64_t* out_fails) {
     if (!c || !dev_acc) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     long long h[PFB_ACC_WORDS];
     CK(cudaMemcpyAsync(h, dev_acc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1420,6 +1474,7 @@ int pfb_ctx_last_fraction_failure(pfb_ctx* c, int32_t* out) {
 int pfb_last_error(pfb_ctx* c, pfb_err* out_err) {
     if (!c || !out_err || !c->last_args) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     int rc = read_result(c);
     if (rc) return rc;
     const unsigned long long key = (unsigned long long)c->res_host[1];
@@ -1443,6 +1498,7 @@ int pfb_nll_host(pfb_ctx* c, const pfb_plan* pc, const double* const* host_cols,
         return PFB_E_EMPTY_DATASET;
     }
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     if (c->e2e_cap < n) {
         for (auto& ptr : c->e2e_dev) {
             cudaFree(ptr);
@@ -1518,6 +1574,7 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
         return PFB_OK;
     }
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     pfb_store* st = nullptr;
     int rc = pfb_store_create(c, 1, n, &st);
     if (rc) return rc;
@@ -1605,6 +1662,7 @@ int pfb_grid_create(pfb_ctx* c, const pfb_dalitz_desc* d, int32_t nx, int32_t ny
     *out = nullptr;
     if (nx < 32 || ny < 32) return PFB_E_DEGENERATE_GRID;  // dalitz.py:253-254
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto g = std::make_unique<pfb_grid>();
     g->ctx = c;
     g->desc = *d;
@@ -1675,6 +1733,7 @@ int pfb_grid_integrals(pfb_ctx* c, pfb_grid* g, int32_t K, const int32_t* pair,
         !inout)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     const int64_t n = g->n_inside;
     if (g->amps_rows < K) {
         double2* na = nullptr;
@@ -1802,6 +1861,7 @@ int pfb_gen_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term_valu
         d->nterms < 1 || d->nterms > kMaxDal)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     GenDalitz G;
     memset(&G, 0, sizeof(G));
     fill_daldesc(*d, term_values, &G.D);
@@ -1832,6 +1892,7 @@ int pfb_gen_1d(pfb_ctx* c, int32_t kind, double mu, double sigma, double alpha, 
         !(sigma > 0.0) || !(hi > lo))
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     Gen1D G;
     G.kind = kind;
     G.mu = mu;
@@ -1862,6 +1923,7 @@ int pfb_gen_1d(pfb_ctx* c, int32_t kind, double mu, double sigma, double alpha, 
 // straight through cudaMemcpyAsync.
 static int download_to_host(pfb_ctx* c, const double* dev, double* host, int64_t count) {
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     cudaPointerAttributes pa;
     const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered;
     cudaGetLastError();
@@ -1928,6 +1990,7 @@ int pfb_store_download(pfb_store* st, int32_t col, double* host, int64_t offset,
 int pfb_fp64_peak(pfb_ctx* c, double* out) {
     if (!c || !out) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     const int blocks = c->sm_count * 8, threads = 256, iters = 2048;
     CK(launch_fp64_peak(c->probe_dev, blocks, threads, 16, c->stream));  // warm-up
     CK(cudaEventRecord(c->ev0, c->stream));
@@ -1963,6 +2026,7 @@ extern "C" {
 int pfb_ctx_spin(pfb_ctx* c, int64_t cycles, const double* flush_buf, int64_t flush_bytes) {
     if (!c || cycles < 0 || flush_bytes < 0 || (flush_bytes && !flush_buf)) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     CK(launch_spin_flush(cycles, flush_buf, flush_bytes, c->probe_dev, c->sm_count, c->stream));
     return PFB_OK;
 }
@@ -1987,6 +2051,7 @@ int pfb_bin_fill(pfb_ctx* c, const pfb_store* st, int64_t begin, int64_t end, in
     }
     if (end == begin) return PFB_OK;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     int rc = ensure_bin(c, (int64_t)sizeof(unsigned long long) * total_bins);
     if (rc) return rc;
     auto* counts = static_cast<unsigned long long*>(c->bin_dev);
@@ -2024,6 +2089,7 @@ int pfb_quadrature(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int32_t 
         if (p->slot_col[s] >= st->ncols || p->slot_col[s] == weight_col) return PFB_E_INVALID_ARGUMENT;
     clear_err(out_err);
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     const int frac = pack_args(p, st, 0, st->n, values, norms, A.get());
     if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
@@ -2058,6 +2124,7 @@ int pfb_binned_nll(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, const do
         return PFB_E_EMPTY_DATASET;
     }
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     int rc = ensure_bin(c, (int64_t)sizeof(double) * nbins);
     if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
@@ -2154,6 +2221,7 @@ int pfb_pcg_scan_1d(pfb_ctx* c, const pfb_plan* p, const double* values, int32_t
                     int32_t nnorms, double lo, double hi, int64_t points, double* out_max) {
     if (!c || !p || !values || !norms || !out_max || points < 1) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     int rc = pack_density_args(c, p, values, nvalues, norms, nnorms, A.get());
     if (rc) return rc;
@@ -2169,6 +2237,7 @@ int pfb_pcg_scan_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* term
     if (!c || !d || !term_values || !out_max || n < 1 || d->nterms < 1 || d->nterms > kMaxDal)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     memset(A.get(), 0, sizeof(NllArgs));
     fill_daldesc(*d, term_values, &A->dal);
@@ -2187,6 +2256,7 @@ int pfb_pcg_generate_1d(pfb_ctx* c, const pfb_plan* p, const double* values, int
         out_offset < 0 || out_offset + n_wanted > out->n || out->ncols < 1)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     int rc = pack_density_args(c, p, values, nvalues, norms, nnorms, A.get());
     if (rc) return rc;
@@ -2207,6 +2277,7 @@ int pfb_pcg_generate_dalitz(pfb_ctx* c, const pfb_dalitz_desc* d, const double* 
         d->nterms > kMaxDal)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     memset(A.get(), 0, sizeof(NllArgs));
     fill_daldesc(*d, term_values, &A->dal);
@@ -2258,6 +2329,7 @@ int pfb_store_load_npy(pfb_store* st, int32_t col, const char* path, int64_t src
     if (npy_parse(fd, &n, &off) || src_offset + count > n) return PFB_E_INVALID_ARGUMENT;
     if (count == 0) return PFB_OK;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     for (int b = 0; b < 2; ++b) {
         if (!c->io_pinned[b]) CK(cudaHostAlloc(&c->io_pinned[b], sizeof(double) * kIoChunk, cudaHostAllocDefault));
         if (!c->io_event[b]) CK(cudaEventCreateWithFlags(&c->io_event[b], cudaEventDisableTiming));
@@ -2293,6 +2365,7 @@ int pfb_store_check_range(pfb_store* st, int32_t col, int64_t begin, int64_t end
     *first_bad = -1;
     if (end == begin) return PFB_OK;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     int rc = ensure_bin(c, 0);
     if (rc) return rc;
     CK(cudaMemsetAsync(c->bin_key, 0xff, sizeof(unsigned long long), c->stream));
@@ -2319,6 +2392,7 @@ int pfb_read_bw(pfb_ctx* c, const double* buf, int64_t bytes, int32_t mode, int3
     if (!c || !buf || bytes <= 0 || !out_gbps || mode < 0 || mode > 2 || reps < 1 || chunk_kb < 1)
         return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     int rc = ensure_bin(c, 0);
     if (rc) return rc;
     cudaEvent_t a, b;
@@ -2348,6 +2422,7 @@ int pfb_read_bw(pfb_ctx* c, const double* buf, int64_t bytes, int32_t mode, int3
 int pfb_peer_create(pfb_ctx* c, int32_t rank, int32_t world, uint8_t* out_handle) {
     if (!c || world < 1 || world > peer_max() || rank < 0 || rank >= world) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     if (c->peer_world) {  // already a member: the same group again is a no-op
         if (c->peer_world != world || c->peer_rank != rank) return PFB_E_INVALID_ARGUMENT;
         if (out_handle) {
@@ -2378,6 +2453,7 @@ int pfb_peer_create(pfb_ctx* c, int32_t rank, int32_t world, uint8_t* out_handle
 int pfb_peer_open(pfb_ctx* c, const uint8_t* handles) {
     if (!c || !handles || !c->peer_world) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     for (int q = 0; q < c->peer_world; ++q) {
         if (q == c->peer_rank || c->peer_ptr[q]) continue;
         cudaIpcMemHandle_t h;
@@ -2417,6 +2493,7 @@ int pfb_nll_peer(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t be
     (void)index_offset;  // errors take the unfused path, which reports them with their offsets
     *out_slow = 0;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     pfb_store staged;
     const bool restaged = !range_aligned(p, st, begin);
     if (restaged) {
@@ -2460,6 +2537,7 @@ int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {
     for (int q = 0; q < c->peer_world; ++q)
         if (!c->peer_ptr[q]) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     const int khz = c->clock_khz;  // a per-call attribute query would stall the queue
     const long long cycles = (long long)(timeout_s * (double)khz * 1e3);
     const unsigned long long seq = ++c->peer_seq;
@@ -2479,6 +2557,7 @@ int pfb_peer_allreduce(pfb_ctx* c, int64_t* dev_acc, double timeout_s) {
 int pfb_overhead_probe(pfb_ctx* c, int32_t mode, int32_t reps, double* out_us) {
     if (!c || !out_us || reps < 1 || mode < 0 || mode > 3) return PFB_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
     memset(A.get(), 0, sizeof(NllArgs));
     A->acc = c->acc;

@@ -125,6 +125,7 @@ struct NllArgs {
     long long* acc_out;       // PFB_ACC_WORDS export target
     long long* result_i;      // [0] deferred-block count, [1] error key, [4] completion sequence
     long long seq;            // > 0: the exporting CTA posts it to result_i[4] last (host polls)
+
     unsigned long long* fix_counter;  // deferred-block list fill (self-resetting)
     int64_t* fix_list;        // deferred global block indices
     const long long* fix_count;       // list length for the fix-up launch (device)
@@ -161,6 +162,31 @@ struct NllArgs {
     int32_t peer_rank;
     unsigned long long peer_seq;
     long long peer_timeout;   // clock64 cycles of the bounded wait
+};
+
+// Persistent NLL kernel control (pfb_nll_task.cuh nll_persist_kernel): the
+// doorbell [seq, op] and the call's NllArgs in mapped pinned host memory,
+// their device copy and the CTA-release word [seq, op] in device memory.
+// Mailbox of one call: the 128-byte chunks of the call's NllArgs that differ
+// from the previous call (chunk indices, then their payloads).
+constexpr int kArgChunk = 128;
+constexpr int kMaxArgChunks = 64;  // >= ceil(sizeof(NllArgs) / 128)
+struct PersistBox {
+    unsigned long long nchunks;
+    unsigned int idx[kMaxArgChunks];
+    unsigned long long pad[7];
+    unsigned char payload[kMaxArgChunks][kArgChunk];
+};
+struct NllArgs;
+struct PersistCtl {
+    const unsigned long long* host_seq;  // mapped: [0] sequence, [1] op (0 run, 1 stop)
+    const PersistBox* host_args;         // mapped mailbox (changed chunks)
+    unsigned int* dev_chunks;            // device: [0] count, [1..] changed chunk indices
+    NllArgs* dev_args;                   // device copy of the mailbox
+    unsigned long long* go;              // device: [0] released sequence, [1] op, [2] idle exit
+    unsigned long long start_seq;        // the doorbell value at launch (== go[0])
+    unsigned long long idle_ns;          // leave after this long without a call
+    unsigned long long* trace;           // optional (mapped): %globaltimer stamps of the last call
 };
 
 // Peer mailbox layout (64-bit words): data [2][kMaxPeers][kPeerSlotWords],

@@ -65,6 +65,29 @@ cudaError_t launch_nll(const NllArgs& A, cudaStream_t stream, int sm_count, int 
     }
 }
 
+int persist_kind_sop(const NllArgs& A, int nc);
+int persist_kind_dal(const NllArgs& A);
+cudaError_t launch_persist_sop(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count);
+cudaError_t launch_persist_dal(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count);
+
+// The persistent-kernel kind of a call (0: none) and its launch.
+int persist_kind(const NllArgs& A, int nc) {
+    switch (A.evaluator) {
+        case EV_SOP:
+            return persist_kind_sop(A, nc);
+        case EV_DALITZ:
+            return persist_kind_dal(A);
+        default:
+            return 0;
+    }
+}
+
+cudaError_t launch_persist_kind(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count) {
+    if (kind == 1 || kind == 2) return launch_persist_sop(kind, P, stream, sm_count);
+    if (kind == 3) return launch_persist_dal(kind, P, stream, sm_count);
+    return cudaErrorInvalidValue;
+}
+
 // Exact recomputation of the deferred blocks listed by a fast launch.
 cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count) {
     NllArgs F = A;

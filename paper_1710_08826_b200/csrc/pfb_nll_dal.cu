@@ -3,6 +3,7 @@
 // structure (pair, spin per term) fixed at compile time; the generic /
 // lineshape-cache path for everything else.
 #include "pfb_nll_prod.cuh"
+#include "pfb_nll_task.cuh"
 
 namespace pfb {
 
@@ -51,6 +52,17 @@ cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
         default:  // any K: per-term reciprocals, no cache rows
             return launch_p<EvDalitzCached>(A, stream, sm_count);
     }
+}
+
+// Persistent kernel for the D0 -> pi+ pi- pi0 ratio form (C3 / C4): kind 3.
+int persist_kind_dal(const NllArgs& A) {
+    if (!A.tma || A.warps || A.npts != 1 || A.evaluator != EV_DALITZ) return 0;
+    return A.dal.K == 4 && signature_of(A.dal) == kSigD0 ? 3 : 0;
+}
+
+cudaError_t launch_persist_dal(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count) {
+    if (kind == 3) return launch_persist<EvDalitzR<4, kSigD0>, true>(P, stream, sm_count);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace pfb

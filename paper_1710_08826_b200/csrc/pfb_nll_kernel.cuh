@@ -825,17 +825,17 @@ __device__ __forceinline__ unsigned int ticket_acq_rel(unsigned int* t) {
 // peer timeout.  Parity alternation: a rank can be at most one call ahead
 // (it cannot pass call s+1's wait before every rank has posted s+1, i.e.
 // finished reading call s), so it never overwrites a slot still being read.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #ifdef PFB_TRACE
 // Per-CTA timeline of the TMA unit kernel (debug builds only): %globaltimer ns
 // at [0] entry, [1] first copy issued, [2] first stage ready (team 0),
 // [3] team 0 done, [4] team 1 done, [5] finish entry, [6] ticket taken,
 // [7] export done (last CTA only).
 __device__ unsigned long long g_trace[1024][16];  // [8..9] ns waited for data per team, [10..11] blocks per team, [12..15] fused-exchange phases (last CTA)
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 #define PFB_T(slot) g_trace[blockIdx.x][slot] = gtimer()
 #else
 #define PFB_T(slot) ((void)0)

@@ -308,9 +308,14 @@ __device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u) {
         return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, fma(-pw, log(u.md), log(u.m))));
     } else {
         const double fe = (double)u.ex;
-        double L = u.ls;
-        if constexpr (HasLScale<Ev>::value) L = Ev::lscale(A) * L;
-        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, log(u.m) + L));
+        // explicit fma / add: no contraction choice left to the compiler, so
+        // every kernel shell (bulk, task, TMA, SIMT, persistent) gives the same bits
+        double s;
+        if constexpr (HasLScale<Ev>::value)
+            s = fma(Ev::lscale(A), u.ls, log(u.m));
+        else
+            s = __dadd_rn(log(u.m), u.ls);
+        return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, s));
     }
 }
 

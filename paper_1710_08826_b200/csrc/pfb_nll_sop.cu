@@ -45,6 +45,24 @@ static cudaError_t launch_stream(const NllArgs& A, cudaStream_t stream, int sm_c
     return launch_p<Ev>(A, stream, sm_count);
 }
 
+// Persistent kernels (pfb_nll_task.cuh) for the shapes the minimiser calls
+// most: 1 = SumPdf(gaussian, exponential) product mode (C1 / C5), 2 =
+// ProdPdf(gaussian(x), exponential(y)) unit sums (C2).  0: none (one-shot
+// launches).  The kind is re-derived from every call's arguments.
+int persist_kind_sop(const NllArgs& A, int nc) {
+    if (!A.tma || A.warps || A.npts != 1 || A.evaluator != EV_SOP) return 0;
+    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
+    if (nc == 1 && nl == 2 && nt == 2 && kinds == (kG | kE << 2) && sum2ge_ok(A)) return 1;
+    if (nc == 2 && nl == 2 && nt == 1 && kinds == (kG | kE << 2)) return 2;
+    return 0;
+}
+
+cudaError_t launch_persist_sop(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count) {
+    if (kind == 1) return launch_persist<EvSum2GE, true>(P, stream, sm_count);
+    if (kind == 2) return launch_persist<EvSop<2, 2, 1, true, kG | kE << 2>, false>(P, stream, sm_count);
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int nc) {
     const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
     if (nc == 1) {

@@ -32,6 +32,8 @@ struct pfb_objective {
     std::vector<pfb_obj_node> node;  // per plan node
     std::vector<double> mat;         // dalitz overlap matrix, K x K (re, im)
     std::vector<double> lower, upper;  // free-parameter bounds (empty: unchecked)
+    int persistent = 0;              // pfb_objective_set_persistent
+    NllArgs args;                    // the persistent path's packed arguments
     // caches: last inputs and norms per node
     std::vector<double> values, norms;
     std::vector<std::vector<double>> last_in;
@@ -143,6 +145,143 @@ static int obj_fill(pfb_objective* o, const double* x, pfb_err* err) {
     return PFB_OK;
 }
 
+// ---- the persistent kernel (pfb_nll_task.cuh nll_persist_kernel) -----------------
+
+static constexpr unsigned long long kPersistIdleNs = 20ull * 1000 * 1000;  // 20 ms without a call: leave
+
+// Make the resident kernel the one of `kind` (stop / start as needed).  The
+// kernel's doorbell starts at c->persist_ctl[0], which the device release word
+// go[0] is set to on the persistent stream before the launch.
+static int persist_start(pfb_ctx* c, int kind) {
+    if (c->persist_kind == kind) return PFB_OK;
+    if (c->persist_kind) {
+        const int r = persist_stop(c);
+        if (r) return r;
+    }
+    if (!c->persist_stream) {
+        CK(cudaStreamCreateWithFlags(&c->persist_stream, cudaStreamNonBlocking));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->persist_ctl), 64, cudaHostAllocMapped));
+        memset(c->persist_ctl, 0, 64);
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->persist_ctl_dev), c->persist_ctl, 0));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->persist_box), sizeof(PersistBox), cudaHostAllocMapped));
+        memset(c->persist_box, 0, sizeof(PersistBox));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->persist_box_dev), c->persist_box, 0));
+        CK(cudaMalloc(&c->persist_args, (size_t)kMaxArgChunks * kArgChunk));
+        CK(cudaMalloc(&c->persist_chunks, sizeof(unsigned int) * (1 + kMaxArgChunks)));
+        CK(cudaMalloc(&c->persist_go, 4 * sizeof(unsigned long long)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->persist_trace), 8 * sizeof(unsigned long long),
+                         cudaHostAllocMapped));
+        memset(c->persist_trace, 0, 8 * sizeof(unsigned long long));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->persist_trace_dev), c->persist_trace, 0));
+        c->persist_shadow.reset(new unsigned char[(size_t)kMaxArgChunks * kArgChunk]());
+    }
+    // work queued on the context stream finishes before the kernel takes the SMs
+    CK(cudaStreamSynchronize(c->stream));
+    unsigned long long go[4] = {c->persist_ctl[0], 0ull, 0ull, 0ull};
+    CK(cudaMemcpyAsync(c->persist_go, go, sizeof(go), cudaMemcpyHostToDevice, c->persist_stream));
+    PersistCtl P;
+    P.host_seq = c->persist_ctl_dev;
+    P.host_args = c->persist_box_dev;
+    P.dev_chunks = c->persist_chunks;
+    P.dev_args = c->persist_args;
+    P.go = c->persist_go;
+    P.start_seq = c->persist_ctl[0];
+    P.idle_ns = kPersistIdleNs;
+    P.trace = getenv("PFB_PERSIST_TRACE") ? c->persist_trace_dev : nullptr;
+    CK(launch_persist_kind(kind, P, c->persist_stream, c->sm_count));
+    ++c->launches;
+    c->persist_kind = kind;
+    c->persist_shadow_valid = false;  // a new kernel holds no arguments yet
+    return PFB_OK;
+}
+
+// Mailbox for `A`: the 128-byte chunks that differ from what the kernel holds.
+static void persist_post_args(pfb_ctx* c, const NllArgs& A) {
+    const unsigned char* a = reinterpret_cast<const unsigned char*>(&A);
+    unsigned char* sh = c->persist_shadow.get();
+    PersistBox* box = c->persist_box;
+    constexpr int kChunks = (int)((sizeof(NllArgs) + kArgChunk - 1) / kArgChunk);
+    unsigned int n = 0;
+    for (int k = 0; k < kChunks; ++k) {
+        const size_t off = (size_t)k * kArgChunk;
+        const size_t len = std::min((size_t)kArgChunk, sizeof(NllArgs) - off);
+        if (c->persist_shadow_valid && memcmp(sh + off, a + off, len) == 0) continue;
+        memcpy(sh + off, a + off, len);
+        memcpy(box->payload[n], a + off, len);
+        box->idx[n] = (unsigned int)k;
+        ++n;
+    }
+    box->nchunks = n;
+    c->persist_shadow_valid = true;
+}
+
+// One call through the resident kernel.  Returns 1 (nothing done) when the
+// call cannot take this path: the caller then runs the ordinary launch.
+static int objective_eval_persistent(pfb_objective* o, double* out_nll, pfb_err* out_err) {
+    pfb_ctx* c = o->ctx;
+    pfb_plan* p = o->plan;
+    const pfb_store* st = o->store;
+    if (c->timing || !c->res_mapped || !range_aligned(p, st, o->begin)) return 1;
+    const int64_t nb = (o->end - o->begin + kBlock - 1) / kBlock;
+    if (c->fix_cap < nb) {  // (re)allocation synchronises the device: not under the resident kernel
+        int rc = persist_stop(c);
+        if (rc) return rc;
+        rc = ensure_fix(c, nb);
+        if (rc) return rc;
+    }
+    NllArgs& A = o->args;
+    const int frac = pack_args(p, st, o->begin, o->end, o->values.data(), o->norms.data(), &A);
+    const int kind = persist_kind(A, sop_ncols(p));
+    if (!kind) return 1;
+    if (c->persist_kind != kind) {
+        const int rc = persist_start(c, kind);
+        if (rc) return rc;
+    }
+    const long long seq = ++c->call_seq;
+    A.seq = seq;
+    persist_post_args(c, A);
+    c->persist_ctl[1] = 0;  // op: run
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    reinterpret_cast<volatile unsigned long long*>(c->persist_ctl)[0] = (unsigned long long)seq;
+    // wait for the posted result (post_seq); a kernel that left (idle exit) is restarted
+    volatile long long* flag = c->res_host + 4;
+    for (unsigned spins = 1;; ++spins) {
+        if (*flag == seq) break;
+        if ((spins & 4095u) == 0u) {
+            const cudaError_t e = cudaStreamQuery(c->persist_stream);
+            if (e == cudaErrorNotReady) continue;
+            if (e != cudaSuccess) return cuda_fail(e);
+            if (*flag == seq) break;
+            // the kernel is gone without this call's result: start again from
+            // the previous doorbell value, so the pending one is served
+            c->persist_kind = 0;
+            c->persist_ctl[0] = (unsigned long long)(seq - 1);
+            int rc = persist_start(c, kind);
+            if (rc) return rc;
+            persist_post_args(c, A);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            reinterpret_cast<volatile unsigned long long*>(c->persist_ctl)[0] = (unsigned long long)seq;
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (c->res_host[0] > 0) {  // deferred blocks: stop, exact fix-up on the context stream
+        int rc = persist_stop(c);
+        if (rc) return rc;
+        NllArgs F = A;
+        F.seq = ++c->call_seq;
+        rc = launch_fixup(c, F, c->res_dev + kResHead);
+        if (rc) return rc;
+        rc = wait_result(c, F.seq);
+        if (rc) return rc;
+    }
+    const unsigned long long key = (unsigned long long)c->res_host[1];
+    const int code = decode_error(c, p, A, key, frac, 0, out_err);
+    if (code) return code;
+    const int st_round = round_result(c, out_nll);
+    if (st_round && out_err) out_err->code = st_round;
+    return st_round;
+}
+
 extern "C" {
 
 int pfb_objective_create(pfb_ctx* c, pfb_plan* p, const pfb_store* st, int64_t begin, int64_t end, int32_t nfree,
@@ -206,6 +345,10 @@ int pfb_objective_eval(pfb_objective* o, const double* x, int32_t nfree, double*
     clear_err(out_err);
     const int st = obj_fill(o, x, out_err);
     if (st) return st;
+    if (o->persistent) {
+        const int r = objective_eval_persistent(o, out_nll, out_err);
+        if (r != 1) return r;
+    }
     return nll_common(o->ctx, o->plan, o->store, o->begin, o->end, 0, o->values.data(), o->plan->nraw,
                       o->norms.data(), (int32_t)o->norms.size(), nullptr, 0, out_nll, out_err);
 }
@@ -235,7 +378,26 @@ int pfb_objective_eval_batch(pfb_objective* o, const double* xs, int32_t npts, i
     return PFB_OK;
 }
 
+int pfb_objective_set_persistent(pfb_objective* o, int32_t on) {
+    if (!o) return PFB_E_INVALID_ARGUMENT;
+    o->persistent = on ? 1 : 0;
+    if (!on) return persist_stop(o->ctx);
+    return PFB_OK;
+}
+
+int pfb_ctx_persist_trace(pfb_ctx* c, uint64_t* out5) {
+    if (!c || !out5) return PFB_E_INVALID_ARGUMENT;
+    for (int i = 0; i < 5; ++i) out5[i] = c->persist_trace ? c->persist_trace[i] : 0;
+    return PFB_OK;
+}
+
+int pfb_ctx_persist_stop(pfb_ctx* c) {
+    if (!c) return PFB_E_INVALID_ARGUMENT;
+    return persist_stop(c);
+}
+
 int pfb_objective_destroy(pfb_objective* o) {
+    if (o && o->persistent) persist_stop(o->ctx);
     delete o;
     return PFB_OK;
 }

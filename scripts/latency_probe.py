@@ -10,6 +10,7 @@ Per config and size, median over `calls` calls after 20 warm-up calls:
 * ``fast_objective``: ``DeviceFitManager(...).fcn()`` -- the objective in C
   (pfb_objective) through the reference ``FcnHandle``, one parameter moved
   per call;
+* ``persistent``: the same with the resident kernel (pfb_objective_set_persistent);
 * ``kernel``: CUDA-event time of the fused launch (pfb_ctx timing).
 One JSON line per (config, size).
 """
@@ -71,7 +72,8 @@ def main():
                 P.set_value(v0, base + 1e-7 * flip[0])
                 P.nll(pdf, ds, P.snapshot(pdf.param_closure()), backend, store)
 
-            handle = pf.DeviceFitManager(pdf, ds).fcn()
+            handle = pf.DeviceFitManager(pdf, ds, persistent=False).fcn()
+            phandle = pf.DeviceFitManager(pdf, ds, persistent=True).fcn()
             x0 = np.array([v.value for v in free])
             x1 = x0.copy()
             x1[0] += 1e-7
@@ -80,8 +82,13 @@ def main():
                 flip[0] ^= 1
                 handle(x1 if flip[0] else x0)
 
+            def persistent_call():
+                flip[0] ^= 1
+                phandle(x1 if flip[0] else x0)
+
             res = {"config": cfg, "n": n, "objective": type(handle._objective).__name__}
-            for tag, fn in (("raw_us", raw), ("reference_nll_us", ref_call), ("fast_objective_us", fast_call)):
+            for tag, fn in (("raw_us", raw), ("reference_nll_us", ref_call), ("fast_objective_us", fast_call),
+                            ("persistent_us", persistent_call)):
                 for _ in range(20):
                     fn()
                 t = []
@@ -91,6 +98,7 @@ def main():
                     t.append(time.perf_counter() - t0)
                 res[tag] = 1e6 * float(np.median(t))
             P.set_value(v0, base)
+            phandle._objective.release()
             ctx.enable_timing(True)
             km = []
             for _ in range(50):
