@@ -228,6 +228,16 @@ int pfb_nll_batch(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64
 int pfb_nll_partial_async(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin,
                           int64_t end, int64_t index_offset, const double* values,
                           int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc);
+/* Enqueue one fused NLL launch (no host synchronisation, no fix-up launch):
+ * the finishing CTA writes the exact accumulator to dev_acc (PFB_ACC_WORDS
+ * int64, device memory) and [deferred-block count, error key] to
+ * dev_status[0..1].  For back-to-back throughput measurement (bench.py): a
+ * step is valid when its deferred count is 0 and its key ~0; its NLL is
+ * pfb_acc_round(dev_acc), bitwise pfb_nll's.  Fractions out of range return
+ * PFB_E_FRACTION_OUT_OF_RANGE without a launch. */
+int pfb_nll_enqueue(pfb_ctx* ctx, const pfb_plan* plan, const pfb_store* st, int64_t begin, int64_t end,
+                    const double* values, int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc,
+                    int64_t* dev_status);
 /* Round a (reduced) device accumulator; synchronises the context stream.
  * out_fails = failed events/blocks summed over the ranks, + 1 when this
  * context's last partial had fractions out of range (pdf._fractions,

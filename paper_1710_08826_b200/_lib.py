@@ -134,6 +134,7 @@ _SIGNATURES = [
     ("pfb_nll_block_sums", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, c_int64, _DBL_P, c_int32, _DBL_P, c_int32, _DBL_P, c_int64, POINTER(PfbErr)]),
     ("pfb_nll_batch", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, c_int64, _DBL_P, c_int32, c_int32, _DBL_P, c_int32, _DBL_P, POINTER(PfbErr)]),
     ("pfb_nll_partial_async", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, c_int64, _DBL_P, c_int32, _DBL_P, c_int32, _PTR]),
+    ("pfb_nll_enqueue", c_int, [_PTR, _PTR, _PTR, c_int64, c_int64, _DBL_P, c_int32, _DBL_P, c_int32, _PTR, _PTR]),
     ("pfb_finalize", c_int, [_PTR, _PTR, _DBL_P, _I64_P]),
     ("pfb_last_error", c_int, [_PTR, POINTER(PfbErr)]),
     ("pfb_ctx_last_fraction_failure", c_int, [_PTR, POINTER(c_int32)]),

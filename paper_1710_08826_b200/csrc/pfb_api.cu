@@ -131,6 +131,7 @@ struct pfb_ctx {
     int* gbad = nullptr;
     unsigned int* gcnt = nullptr;  // zeroed once, self-resetting
     int64_t fix_cap = 0;
+    int64_t fold_cap = 0;
     double* bsums = nullptr;
     int64_t bsums_cap = 0;
     double* probe_dev = nullptr;
@@ -140,6 +141,7 @@ struct pfb_ctx {
     float last_ms = 0.f;
     // last partial launch, for error decoding
     std::unique_ptr<NllArgs> last_args;
+    std::unique_ptr<NllArgs> enqueue_args;  // pfb_nll_enqueue's packing buffer
     const pfb_plan* last_plan = nullptr;
     int64_t last_index_offset = 0;
     int last_frac_rank = -1;
@@ -1174,9 +1176,16 @@ static int read_result(pfb_ctx* c, int npts = 1) {
 // synchronize (no driver round trip on the critical path of a minimiser
 // call).  Every 1024 polls the stream is queried, so an error or a launch
 // that does not post falls back to the ordinary synchronize.
+static bool poll_results() {
+    // opt-in: measured no faster than a stream synchronize for one-shot
+    // launches, and the post costs the exporting CTA a system fence
+    // (profiles/r2_persistent.md); the persistent kernel always posts
+    static const bool on = getenv("PFB_POLL") != nullptr;
+    return on;
+}
+
 static int wait_result(pfb_ctx* c, long long seq) {
-    static const bool sync_wait = getenv("PFB_SYNC_WAIT") != nullptr;  // A/B switch (scripts/latency_probe.py)
-    if (sync_wait || c->timing || !c->res_mapped || seq <= 0) return read_result(c);
+    if (c->timing || !c->res_mapped || seq <= 0) return read_result(c);
     volatile long long* flag = c->res_host + 4;
     for (unsigned spins = 1;; ++spins) {
         if (*flag == seq) {
@@ -1193,24 +1202,32 @@ static int wait_result(pfb_ctx* c, long long seq) {
     }
 }
 
-static int ensure_fix(pfb_ctx* c, int64_t nblocks) {
-    if (c->fix_cap >= nblocks) return PFB_OK;
-    cudaFree(c->fix_list);
-    cudaFree(c->gfold);
-    cudaFree(c->gbad);
-    cudaFree(c->gcnt);
-    c->fix_list = nullptr;
-    c->gfold = nullptr;
-    c->gbad = nullptr;
-    c->gcnt = nullptr;
-    c->fix_cap = 0;
-    const size_t nb = (size_t)(nblocks > 0 ? nblocks : 1);
-    CK(cudaMalloc(&c->fix_list, sizeof(int64_t) * nb));
-    CK(cudaMalloc(&c->gfold, sizeof(double) * 8 * 32 * nb));
-    CK(cudaMalloc(&c->gbad, sizeof(int) * 8 * nb));
-    CK(cudaMalloc(&c->gcnt, sizeof(unsigned int) * nb));
-    CK(cudaMemset(c->gcnt, 0, sizeof(unsigned int) * nb));
-    c->fix_cap = nblocks;
+// Deferred-block list for up to `nentries` (block, point) pairs, and the task
+// kernel's cross-CTA fold slots for `nblocks` blocks (one parameter point).
+static int ensure_fix(pfb_ctx* c, int64_t nentries, int64_t nblocks = -1) {
+    if (nblocks < 0) nblocks = nentries;
+    if (c->fix_cap < nentries) {
+        cudaFree(c->fix_list);
+        c->fix_list = nullptr;
+        c->fix_cap = 0;
+        CK(cudaMalloc(&c->fix_list, sizeof(int64_t) * (size_t)(nentries > 0 ? nentries : 1)));
+        c->fix_cap = nentries;
+    }
+    if (c->fold_cap < nblocks) {
+        cudaFree(c->gfold);
+        cudaFree(c->gbad);
+        cudaFree(c->gcnt);
+        c->gfold = nullptr;
+        c->gbad = nullptr;
+        c->gcnt = nullptr;
+        c->fold_cap = 0;
+        const size_t nb = (size_t)(nblocks > 0 ? nblocks : 1);
+        CK(cudaMalloc(&c->gfold, sizeof(double) * 8 * 32 * nb));
+        CK(cudaMalloc(&c->gbad, sizeof(int) * 8 * nb));
+        CK(cudaMalloc(&c->gcnt, sizeof(unsigned int) * nb));
+        CK(cudaMemset(c->gcnt, 0, sizeof(unsigned int) * nb));
+        c->fold_cap = nblocks;
+    }
     return PFB_OK;
 }
 
@@ -1283,13 +1300,13 @@ static int nll_common(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64
         }
         A->block_sums = c->bsums;
     }
-    A->seq = ++c->call_seq;
+    A->seq = poll_results() ? ++c->call_seq : 0;
     rc = launch_eval(p, st, begin, end, A.get(), !restaged);
     if (rc) return rc;
     rc = wait_result(c, A->seq);
     if (rc) return rc;
     if (c->res_host[0] > 0) {  // deferred blocks: exact fix-up
-        A->seq = ++c->call_seq;
+        A->seq = poll_results() ? ++c->call_seq : 0;
         rc = launch_fixup(c, *A, c->res_dev + kResHead);
         if (rc) return rc;
         const float fast_ms = c->last_ms;
@@ -1351,7 +1368,7 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
         begin = 0;
     }
     // the batched kernels list one deferred entry per (block, point) pair
-    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock * npts);
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock * npts, (end - begin + kBlock - 1) / kBlock);
     if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
     int frac0 = pack_args(p, st, begin, end, values, norms, A.get());
@@ -1408,6 +1425,31 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
         if (code && !first) first = code;
     }
     return first;
+}
+
+int pfb_nll_enqueue(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin, int64_t end,
+                    const double* values, int32_t nvalues, const double* norms, int32_t nnorms, int64_t* dev_acc,
+                    int64_t* dev_status) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!c || !p || !st || !values || !norms || !dev_acc || !dev_status || p->ctx != c || st->ctx != c)
+        return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+    if (begin < 0 || end <= begin || end > st->n) return PFB_E_INVALID_ARGUMENT;
+    if (!range_aligned(p, st, begin)) return PFB_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(c->device));
+    PFB_QUIESCE(c);
+    int rc = ensure_fix(c, (end - begin + kBlock - 1) / kBlock);
+    if (rc) return rc;
+    NllArgs* A = c->enqueue_args.get();
+    if (!A) {
+        c->enqueue_args.reset(new NllArgs());
+        A = c->enqueue_args.get();
+    }
+    if (pack_args(p, st, begin, end, values, norms, A) >= 0) return PFB_E_FRACTION_OUT_OF_RANGE;
+    A->acc_out = (long long*)dev_acc;
+    A->result_i = (long long*)dev_status;
+    A->seq = 0;
+    return launch_eval(p, st, begin, end, A, true);
 }
 
 int pfb_nll_partial_async(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t begin,

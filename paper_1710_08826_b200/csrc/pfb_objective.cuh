@@ -223,7 +223,7 @@ static int objective_eval_persistent(pfb_objective* o, double* out_nll, pfb_err*
     const pfb_store* st = o->store;
     if (c->timing || !c->res_mapped || !range_aligned(p, st, o->begin)) return 1;
     const int64_t nb = (o->end - o->begin + kBlock - 1) / kBlock;
-    if (c->fix_cap < nb) {  // (re)allocation synchronises the device: not under the resident kernel
+    if (c->fix_cap < nb || c->fold_cap < nb) {  // (re)allocation synchronises the device: not under the resident kernel
         int rc = persist_stop(c);
         if (rc) return rc;
         rc = ensure_fix(c, nb);
@@ -268,7 +268,7 @@ static int objective_eval_persistent(pfb_objective* o, double* out_nll, pfb_err*
         int rc = persist_stop(c);
         if (rc) return rc;
         NllArgs F = A;
-        F.seq = ++c->call_seq;
+        F.seq = 0;
         rc = launch_fixup(c, F, c->res_dev + kResHead);
         if (rc) return rc;
         rc = wait_result(c, F.seq);

@@ -102,8 +102,14 @@ class DeviceContext:
         L.check(L.lib().pfb_ctx_launch_count(self.handle, ctypes.byref(out)), "pfb_ctx_launch_count")
         return out.value
 
+    CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
     def set_stream(self, stream_ptr: int | None) -> None:
-        L.check(L.lib().pfb_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)), "pfb_ctx_set_stream")
+        """Run the engine on `stream_ptr` (e.g. ``torch.cuda.current_stream().cuda_stream``).
+        0 -- torch's default stream -- is the legacy default stream, so the
+        engine stays ordered with torch's work; None: the context's own stream."""
+        ptr = self.CUDA_STREAM_LEGACY if stream_ptr == 0 else stream_ptr
+        L.check(L.lib().pfb_ctx_set_stream(self.handle, ctypes.c_void_p(ptr)), "pfb_ctx_set_stream")
 
     def enable_timing(self, on: bool = True) -> None:
         L.check(L.lib().pfb_ctx_enable_timing(self.handle, 1 if on else 0), "pfb_ctx_enable_timing")

@@ -32,6 +32,13 @@ __global__ void empty_k(int* sink) {
 __global__ void big_k(const __grid_constant__ Big b, double* sink) {
     if (threadIdx.x == 0 && blockIdx.x == 0 && b.v[799] == 12345.0) sink[0] = b.v[3];
 }
+extern __shared__ double dyn_smem[];
+__global__ void big_smem_k(const __grid_constant__ Big b, double* sink) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && b.v[799] == 12345.0) sink[0] = dyn_smem[threadIdx.x];
+}
+__global__ void small_smem_k(double* sink) {
+    if (threadIdx.x == 100000) sink[0] = dyn_smem[threadIdx.x];
+}
 __global__ void mapped_k(volatile long long* host_res, int words) {
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < words) host_res[threadIdx.x] = threadIdx.x + 1;
 }
@@ -77,6 +84,8 @@ int main() {
     CK(cudaHostGetDevicePointer((void**)&dres, hres, 0));
     Big big;
     for (int i = 0; i < 800; ++i) big.v[i] = i;
+    CK(cudaFuncSetAttribute(big_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608));
+    CK(cudaFuncSetAttribute(small_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608));
     const int reps = 200;
 
     auto ev_time = [&](auto launch, bool spin_before) -> double {
@@ -115,6 +124,10 @@ int main() {
         {"empty 592x256", [&] { empty_k<<<592, 256, 0, s>>>(sink); }},
         {"6.4KB param 148x256", [&] { big_k<<<148, 256, 0, s>>>(big, (double*)sink); }},
         {"mapped result 148x256", [&] { mapped_k<<<148, 256, 0, s>>>(dres, 80); }},
+        // the C2 TMA unit kernel's launch shape: 148 CTAs x 544 threads, 196 KB dynamic shared memory
+        {"148x544 + 196KB smem + 6.4KB param", [&] { big_smem_k<<<148, 544, 196608, s>>>(big, (double*)sink); }},
+        {"148x544 + 196KB smem", [&] { small_smem_k<<<148, 544, 196608, s>>>((double*)sink); }},
+        {"148x544, no smem", [&] { small_smem_k<<<148, 544, 0, s>>>((double*)sink); }},
     };
     for (auto& c : cases) {
         printf("{\"case\": \"%s\", \"event_us\": %.2f, \"event_us_after_spin\": %.2f, \"host_roundtrip_us\": %.2f}\n",
