@@ -335,6 +335,7 @@ class Measure:
         self.ev_a = torch.cuda.Event(enable_timing=True)
         self.ev_b = torch.cuda.Event(enable_timing=True)
         self.c_move = 0
+        self.c2p_fcn = None
 
     def pack(self):
         snap = self.P.snapshot(self.pdf.param_closure())
@@ -345,19 +346,20 @@ class Measure:
         """One NLL over this rank's events; returns (device ms, value)."""
         L, pf = self.L, self.pf
         if self.model == "c2p":
-            # a finite-difference-like move of a polynomial coefficient: the
-            # device GL normalisation kernel runs inside the timed step
+            # a finite-difference-like move of a polynomial coefficient through
+            # the minimiser's objective in C: the device GL normalisation
+            # kernel and the NLL kernel both run inside the timed step
             self.c_move += 1
-            c1 = self.free[3]
-            self.P.set_value(c1, 0.3 + 1e-6 * (self.c_move % 2))
+            if self.c2p_fcn is None:
+                self.c2p_fcn = self.pf.DeviceFitManager(self.pdf, self.ds).fcn()
+                self.c2p_x = np.array([v.value for v in self.free])
+            x = self.c2p_x.copy()
+            x[3] += 1e-6 * (self.c_move % 2)
             self.ev_a.record()
-            vals, nv = self.pack()
-            code = L.lib().pfb_nll(self.ctx.handle, self.plan.handle, self.store, 0, self.n, 0, L.dptr(vals),
-                                   len(vals), L.dptr(nv), len(nv), ctypes.byref(self.out), ctypes.byref(self.err))
+            value = self.c2p_fcn(x)
             self.ev_b.record()
-            L.check(code, "pfb_nll")
             self.ev_b.synchronize()
-            return self.ev_a.elapsed_time(self.ev_b), self.out.value
+            return self.ev_a.elapsed_time(self.ev_b), value
         vals, nv = self.vals, self.nv
         if self.world == 1:
             code = L.lib().pfb_nll(self.ctx.handle, self.plan.handle, self.store, 0, self.n, 0, L.dptr(vals),
@@ -534,8 +536,8 @@ class Measure:
                "roofline": self.roofline(t["ms_per_step"]), "e2e": e2e, "clocks": t["clocks"],
                "wall_s": t["wall_s"], "generate_s": self.gen_s}
         if self.model == "c2p":
-            rec["step"] = ("set_value(c1) -> reference resolve_norms (device GL quadrature kernel) -> fused NLL "
-                           "kernel; CUDA events around both launches (host norm work included)")
+            rec["step"] = ("the C objective (DeviceFitManager.fcn) with c1 moved: device GL quadrature kernel "
+                           "(the polynomial's norm) + fused NLL kernel; CUDA events around the call")
         if self.rank == 0 and self.world == 1:
             rec["parity"], rec["cpu_baseline"] = self.parity_and_cpu(t["nll"], cpu_budget_s)
             if with_fit:

@@ -123,25 +123,30 @@ typedef struct pfb_err {
     double value;  /* offending value (NaN when the reference carries none) */
 } pfb_err;
 
-/* Normalisation programs of a pfb_objective node (see pfb_objective_create). */
-enum pfb_norm_kind {
-    PFB_NORM_CONST = 0,       /* `value` (add / prod: 1, pdf.py:238-239; or a norm fixed for the fit) */
-    PFB_NORM_GAUSSIAN = 1,    /* _gaussian_norm over [lo, hi] (pdf.py:130-138) */
-    PFB_NORM_EXPONENTIAL = 2, /* _exponential_norm over [lo, hi] (pdf.py:147-161) */
-    PFB_NORM_DALITZ = 3       /* dalitz_norm with a fixed overlap matrix (dalitz.py:332-349) */
-};
-typedef struct pfb_obj_node {
-    int32_t norm_kind; /* enum pfb_norm_kind */
-    int32_t pad;
-    double lo, hi;     /* observable bounds (gaussian / exponential) */
-    double value;      /* PFB_NORM_CONST */
-} pfb_obj_node;
-
 typedef struct pfb_ctx pfb_ctx;
 typedef struct pfb_store pfb_store;
 typedef struct pfb_plan pfb_plan;
 typedef struct pfb_grid pfb_grid;
 typedef struct pfb_objective pfb_objective;
+
+/* Normalisation programs of a pfb_objective node (see pfb_objective_create). */
+enum pfb_norm_kind {
+    PFB_NORM_CONST = 0,       /* `value` (add / prod: 1, pdf.py:238-239; or a norm fixed for the fit) */
+    PFB_NORM_GAUSSIAN = 1,    /* _gaussian_norm over [lo, hi] (pdf.py:130-138) */
+    PFB_NORM_EXPONENTIAL = 2, /* _exponential_norm over [lo, hi] (pdf.py:147-161) */
+    PFB_NORM_DALITZ = 3,      /* dalitz_norm with a fixed overlap matrix (dalitz.py:332-349) */
+    PFB_NORM_QUADRATURE = 4   /* pfb_quadrature of the node's own plan over a rule store
+                                 (_polynomial_norm, pdf.py:192-199) */
+};
+typedef struct pfb_obj_node {
+    int32_t norm_kind;  /* enum pfb_norm_kind */
+    int32_t weight_col; /* PFB_NORM_QUADRATURE: the rule store's weight column */
+    double lo, hi;      /* observable bounds (gaussian / exponential) */
+    double value;       /* PFB_NORM_CONST */
+    pfb_plan* quad_plan;        /* PFB_NORM_QUADRATURE: plan of the node alone (root norm 1) */
+    const pfb_store* quad_rule; /* PFB_NORM_QUADRATURE: abscissas + weights */
+} pfb_obj_node;
+
 
 /* ---- library / context ---------------------------------------------------- */
 int pfb_version(void);

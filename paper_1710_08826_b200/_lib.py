@@ -80,11 +80,12 @@ class PfbDalitzDesc(ctypes.Structure):
     ]
 
 
-NORM_CONST, NORM_GAUSSIAN, NORM_EXPONENTIAL, NORM_DALITZ = 0, 1, 2, 3
+NORM_CONST, NORM_GAUSSIAN, NORM_EXPONENTIAL, NORM_DALITZ, NORM_QUADRATURE = 0, 1, 2, 3, 4
 
 
 class PfbObjNode(ctypes.Structure):
-    _fields_ = [("norm_kind", c_int32), ("pad", c_int32), ("lo", c_double), ("hi", c_double), ("value", c_double)]
+    _fields_ = [("norm_kind", c_int32), ("weight_col", c_int32), ("lo", c_double), ("hi", c_double),
+                ("value", c_double), ("quad_plan", c_void_p), ("quad_rule", c_void_p)]
 
 
 class PfbErr(ctypes.Structure):

@@ -8,7 +8,7 @@
 
 namespace pfb {
 
-static constexpr int kG = PFB_GAUSSIAN, kE = PFB_EXPONENTIAL;
+static constexpr int kG = PFB_GAUSSIAN, kE = PFB_EXPONENTIAL, kP = PFB_POLYNOMIAL;
 
 static int kinds_of(const NllArgs& A) {
     int k = 0;
@@ -92,6 +92,10 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // ProdPdf(gaussian(x), exponential(y)): C2
         if (nl == 2 && nt == 1 && kinds == (kG | kE << 2))
             return launch_stream<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
+        // ProdPdf(gaussian(x), polynomial(y)): C2p (the generic SIMT
+        // instantiation took 290 us at 10M events, measured)
+        if (nl == 2 && nt == 1 && kinds == (kG | kP << 2))
+            return launch_stream<EvSop<2, 2, 1, true, kG | kP << 2>>(A, stream, sm_count);
         return launch_p<EvSop<2>>(A, stream, sm_count);
     }
     // the kernels stream exactly the plan's columns (NC of them)

@@ -17,6 +17,8 @@
 //   add / prod 1 (P/pdf.py:238-239), or a constant supplied at creation
 //   dalitz     Re(c I c^H), c_k = mag_k e^{i phase_k}, I the overlap matrix supplied at
 //              creation (P/dalitz.py:332-349; shapes must be fixed)
+//   polynomial the device Gauss-Legendre integral of the node alone (pfb_quadrature,
+//              P/pdf.py:181-199), launched only when a coefficient moved
 // Any norm failure returns PFB_E_NONPOSITIVE_NORM / PFB_E_UNBOUNDED_OBSERVABLE
 // with err->node set: the caller re-evaluates that point through the
 // reference path, which raises the reference's exception.
@@ -96,6 +98,15 @@ static int obj_norm(const pfb_objective* o, int i, const double* raw, double* ou
             if (fabs(tim) > 1e-10 * scale) return PFB_E_NONPOSITIVE_NORM;
             if (!(tre > 0.0)) return PFB_E_NONPOSITIVE_NORM;
             v = tre;
+            break;
+        }
+        case PFB_NORM_QUADRATURE: {
+            // the node's own plan (one node: its raw values, root norm 1) over the rule
+            const double one = 1.0;
+            pfb_err e;
+            const int st = pfb_quadrature(o->ctx, nd.quad_plan, nd.quad_rule, nd.weight_col, raw,
+                                          nd.quad_plan->nraw, &one, 1, &v, &e);
+            if (st) return st;
             break;
         }
         default:
@@ -316,7 +327,13 @@ int pfb_objective_create(pfb_ctx* c, pfb_plan* p, const pfb_store* st, int64_t b
             o->node[i].value = K;
             o->mat.assign(dalitz_matrix, dalitz_matrix + 2 * K * K);
         }
-        if (k < PFB_NORM_CONST || k > PFB_NORM_DALITZ) return PFB_E_INVALID_ARGUMENT;
+        if (k == PFB_NORM_QUADRATURE) {
+            const pfb_plan* qp = o->node[i].quad_plan;
+            if (!qp || !o->node[i].quad_rule || qp->ctx != c || qp->nodes.size() != 1 ||
+                qp->nraw != p->nodes[i].nparam)
+                return PFB_E_INVALID_ARGUMENT;
+        }
+        if (k < PFB_NORM_CONST || k > PFB_NORM_QUADRATURE) return PFB_E_INVALID_ARGUMENT;
     }
     o->values.assign(p->nraw, 0.0);
     o->norms.assign(nn, 1.0);

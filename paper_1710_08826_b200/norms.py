@@ -94,6 +94,21 @@ def _rule(ctx, axes) -> _Rule:
     return r
 
 
+def quadrature_handles(node, nodes: int = GL_NODES, panels: int = GL_PANELS, ctx=None):
+    """(plan, rule) of the device quadrature of `node` alone -- what the C
+    objective launches when the node's parameters move (PFB_NORM_QUADRATURE)."""
+    from .engine import device_context
+
+    ctx = ctx or device_context(0)
+    obs = node.observables
+    for o in obs:
+        if math.isinf(o.lower) or math.isinf(o.upper):
+            raise ref_errors.UnboundedObservable(f"{node.kind} normalization needs finite bounds")
+    rule = _rule(ctx, [(o.lower, o.upper, int(nodes), int(panels)) for o in obs])
+    plan = ctx.plan_for(node, tuple(o.name for o in obs) + ("__weights__",))
+    return plan, rule
+
+
 def quadrature(node, snap=None, child_norms=None, nodes: int = GL_NODES, panels: int = GL_PANELS, ctx=None) -> float:
     """Integral of `node`'s unnormalised density over its observables' box by
     the composite Gauss-Legendre rule (tensor product over the axes), on the

@@ -131,13 +131,37 @@ def test_failures_take_the_reference_path(pf):
         fcn3(np.array([0.5, 0.0]))
 
 
-def test_unsupported_models_fall_back(pf):
+def test_polynomial_norm_in_c_and_fallback(pf):
+    """Free polynomial coefficients: the device GL integral launched from C
+    (PFB_NORM_QUADRATURE) -- the same kernel the reference-path hook runs, so
+    the values are bitwise; a model with a custom norm hook (grid-mode
+    gaussian) falls back to the reference objective."""
     from paper_1710_08826_b200.fitting import DeviceObjective, FastObjective
 
     x = P.Variable.observable("x", 0.0, 1.0)
-    node = P.polynomial(x, [P.Variable("c0", 1.0, 0.1, 2.0), P.Variable("c1", 0.2, -0.5, 0.5)])
-    ds = models.dataset([x], [np.linspace(0.0, 1.0, 3000)])
-    fm = pf.DeviceFitManager(node, ds)
-    fcn = fm.fcn()
-    assert type(fcn._objective) is DeviceObjective and not isinstance(fcn._objective, FastObjective)
-    assert math.isfinite(fcn(np.array([1.0, 0.1])))
+    node = P.polynomial(x, [P.Variable("c0", 1.0, 0.1, 2.0), P.Variable("c1", 0.2, -0.5, 0.5),
+                            P.Variable("c2", 0.1, 0.0, 1.0)])
+    ds = models.dataset([x], [np.linspace(0.0, 1.0, 30001)])
+    fast = pf.DeviceFitManager(node, ds).fcn()
+    exact = pf.DeviceFitManager(node, ds, fast=False).fcn()
+    assert isinstance(fast._objective, FastObjective)
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        pt = np.array([rng.uniform(0.5, 1.5), rng.uniform(-0.3, 0.3), rng.uniform(0.0, 0.5)])
+        assert fast(pt) == exact(pt)
+    # a coefficient move that makes the density dip negative inside the box:
+    # NegativeDensity from the GL abscissas (the reference path), or from the events
+    with pytest.raises((E.NegativeDensity, E.NonPositiveDensity)):
+        fast(np.array([0.1, -0.5, 0.0]))
+    start = (1.0, 0.2, 0.1)
+    fits = []
+    for make in (lambda: pf.DeviceFitManager(node, ds), lambda: pf.DeviceFitManager(node, ds, fast=False)):
+        for v, val in zip(node.parameters, start):
+            P.set_value(v, val)
+        fits.append(make().fit())
+    assert fits[0].n_calls == fits[1].n_calls and np.array_equal(fits[0].values, fits[1].values)
+    with pf.device_norms(grid_kinds=("gaussian",)):
+        g = P.gaussian(x, P.Variable("gm", 0.5, 0.0, 1.0), P.Variable("gs", 0.3, 0.05, 1.0))
+        fcn = pf.DeviceFitManager(g, ds).fcn()
+        assert type(fcn._objective) is DeviceObjective and not isinstance(fcn._objective, FastObjective)
+        assert math.isfinite(fcn(np.array([0.5, 0.3])))
