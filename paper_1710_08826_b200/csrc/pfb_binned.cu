@@ -46,23 +46,32 @@ __global__ void __launch_bounds__(kThreads) binned_nll_kernel(const __grid_const
     __shared__ unsigned int s_last;
     for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
     __syncthreads();
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbins;
-         b += (int64_t)gridDim.x * blockDim.x) {
-        int rank = -1;
-        double val = 0.0;
-        const double p = literal_density(A, A.begin + b, &rank, &val);
-        if (rank >= 0) {
-            record_failure(A, rank, b, sacc);
-            continue;
+    // warp-uniform trip count (acc_add_warp needs the whole warp)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b0 = blockIdx.x * (int64_t)blockDim.x; b0 < nbins; b0 += stride) {
+        const int64_t b = b0 + threadIdx.x;
+        bool act = b < nbins;
+        double term = 0.0;
+        if (act) {
+            int rank = -1;
+            double val = 0.0;
+            const double p = literal_density(A, A.begin + b, &rank, &val);
+            if (rank >= 0) {
+                record_failure(A, rank, b, sacc);
+                act = false;
+            } else {
+                const double nu = Mul(Mul(total, p), volume);
+                const double c = contents[b];
+                const bool observed = c > 0.0;
+                if (observed && !(nu > 0.0)) {
+                    atomicMin(expkey, (unsigned long long)b);
+                    act = false;
+                } else {
+                    term = observed ? Sub(nu, Mul(c, log(nu))) : nu;
+                }
+            }
         }
-        const double nu = Mul(Mul(total, p), volume);
-        const double c = contents[b];
-        const bool observed = c > 0.0;
-        if (observed && !(nu > 0.0)) {
-            atomicMin(expkey, (unsigned long long)b);
-            continue;
-        }
-        acc_add_shared(sacc, observed ? Sub(nu, Mul(c, log(nu))) : nu);
+        acc_add_warp(sacc, term, act);
     }
     finish_launch<false>(A, sacc, &s_last);
 }
@@ -80,15 +89,23 @@ __global__ void __launch_bounds__(kThreads) quadrature_kernel(const __grid_const
     __shared__ unsigned int s_last;
     for (int i = threadIdx.x; i < PFB_ACC_WORDS; i += blockDim.x) sacc[i] = 0;
     __syncthreads();
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        int rank = -1;
-        double val = 0.0;
-        const double f = literal_density(A, A.begin + j, &rank, &val);
-        if (rank >= 0) {
-            record_failure(A, rank, j, sacc);
-            continue;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < n; j0 += stride) {
+        const int64_t j = j0 + threadIdx.x;
+        bool act = j < n;
+        double term = 0.0;
+        if (act) {
+            int rank = -1;
+            double val = 0.0;
+            const double f = literal_density(A, A.begin + j, &rank, &val);
+            if (rank >= 0) {
+                record_failure(A, rank, j, sacc);
+                act = false;
+            } else {
+                term = Mul(weights[j], f);
+            }
         }
-        acc_add_shared(sacc, Mul(weights[j], f));
+        acc_add_warp(sacc, term, act);
     }
     finish_launch<false>(A, sacc, &s_last);
 }

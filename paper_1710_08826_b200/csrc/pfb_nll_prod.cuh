@@ -162,6 +162,59 @@ struct EvSum2GE {
     }
 };
 
+// ProdPdf(gaussian(x), polynomial(y)) on two columns (C2p):
+//   p = c exp(u) q,  u = (-0.5 z) z,  z = (x - mu) / sigma,  q = polyval(y),
+//   c = 1 / (norm_gauss norm_poly norm_root)  (pdf.py:122-127, 160-167, 205-219).
+// The log sum takes l = ln c + u, the unit product q: one logarithm per 16
+// events where the log-domain EvSop pays one per event (and its I2F / MUFU
+// on the XU pipe: 108 us at 10M events, XU 74% busy -- ncu, round 2).
+// Leaf/term layout fixed by the dispatcher (gp_ok): leaf 0 gaussian
+// (ptv[0][0..1] = mu, 1/sigma), leaf 1 polynomial (ptv[0][2..] = coefficients,
+// lowest order first), one term with emask {0}, vmask {1}, finite ln c.
+// Certification: u >= -600 (the reference's exp(u) is a normal double), q
+// positive within 2^+-250 (unit check), and the EvSop budget
+// |u| + |log2 q| ln2 + 1 <= thr (thr = 690 - |ln c|: the reference's linear
+// product stays normal).  Explicit _rn operations: every shell that runs
+// this evaluator (bulk, TMA unit, SIMT) gives the same bits.  NV > 0: the
+// coefficient count at compile time (unrolled Horner); 0: A.leaf[1].nv.
+template <int NV = 0>
+struct EvGaussPoly {
+    static constexpr int NC = 2;
+    static constexpr int U = 2;
+    static constexpr int MINB = 3;
+
+    __device__ static __forceinline__ double one(const NllArgs& A, double xg, double y, bool& ok, double& l) {
+        const double* v = A.ptv[0];
+        const double z = __dmul_rn(__dsub_rn(xg, v[0]), v[1]);
+        const double u = __dmul_rn(__dmul_rn(-0.5, z), z);
+        const int nv = NV > 0 ? NV : A.leaf[1].nv;
+        double q = v[1 + nv];
+        if constexpr (NV > 0) {
+#pragma unroll
+            for (int i = NV - 1; i >= 1; --i) q = fma(q, y, v[1 + i]);
+        } else {
+#pragma unroll 1
+            for (int i = nv - 1; i >= 1; --i) q = fma(q, y, v[1 + i]);
+        }
+        l = __dadd_rn(v[kPtLeafWords], u);
+        // |binary exponent of q| as a double without I2F (magic-number add)
+        const int e = ((__double2hiint(q) >> 20) & 0x7ff) - 1023;
+        const double ae = __dsub_rn(__hiloint2double(0x43300000, e < 0 ? -e : e), 0x1p52);
+        const double budget = fma(ae, 0.6931471805599453, __dsub_rn(1.0, u));
+        ok = (u >= -600.0) && (budget <= v[kPtLeafWords + 1]);
+        return q;
+    }
+
+    __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[2], bool& okx,
+                                                    bool& oky, const double*, double2& l) {
+        const bool g1 = A.leaf[0].col != 0;
+        double2 q;
+        q.x = one(A, g1 ? x[1].x : x[0].x, g1 ? x[0].x : x[1].x, okx, l.x);
+        q.y = one(A, g1 ? x[1].y : x[0].y, g1 ? x[0].y : x[1].y, oky, l.y);
+        return q;
+    }
+};
+
 // Running state of one 16-event unit: the product m * 2^ex of the q factors,
 // for ratio evaluators (Ev::RATIO, p = q / r) the product md * 2^exd of the
 // r factors, and the sum ls of the log factors l.

@@ -36,6 +36,14 @@ static bool sum2ge_ok(const NllArgs& A) {
     return true;
 }
 
+// EvGaussPoly's fixed layout: leaf 0 gaussian, leaf 1 polynomial, one term
+// multiplying both (gaussian in the log sum, polynomial as a value).
+static bool gp_ok(const NllArgs& A) {
+    if (A.leaf[0].voff != 0 || A.leaf[1].voff != 2 || A.leaf[1].nv < 1) return false;
+    if (A.term[0].emask != 1u || A.term[0].vmask != 2u) return false;
+    return fabs(A.term[0].logcoef) < 600.0;
+}
+
 // pipeline 1: the unit-sum TMA kernel; 2: the reference-tree TMA kernel;
 // 0: the SIMT streaming kernel
 template <class Ev>
@@ -92,8 +100,18 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // ProdPdf(gaussian(x), exponential(y)): C2
         if (nl == 2 && nt == 1 && kinds == (kG | kE << 2))
             return launch_stream<EvSop<2, 2, 1, true, kG | kE << 2>>(A, stream, sm_count);
-        // ProdPdf(gaussian(x), polynomial(y)): C2p (the generic SIMT
-        // instantiation took 290 us at 10M events, measured)
+        // ProdPdf(gaussian(x), polynomial(y)): C2p -- product mode (one log
+        // per 16 events) with the pipeline on; the log-domain EvSop (108 us at
+        // 10M, XU-bound) without; the generic SIMT instantiation took 290 us
+        if (nl == 2 && nt == 1 && kinds == (kG | kP << 2) && A.tma && gp_ok(A)) {
+            switch (A.leaf[1].nv) {
+                case 1: return launch_prod<EvGaussPoly<1>>(A, stream, sm_count);
+                case 2: return launch_prod<EvGaussPoly<2>>(A, stream, sm_count);
+                case 3: return launch_prod<EvGaussPoly<3>>(A, stream, sm_count);
+                case 4: return launch_prod<EvGaussPoly<4>>(A, stream, sm_count);
+                default: return launch_prod<EvGaussPoly<>>(A, stream, sm_count);
+            }
+        }
         if (nl == 2 && nt == 1 && kinds == (kG | kP << 2))
             return launch_stream<EvSop<2, 2, 1, true, kG | kP << 2>>(A, stream, sm_count);
         return launch_p<EvSop<2>>(A, stream, sm_count);
