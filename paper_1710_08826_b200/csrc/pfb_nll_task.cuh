@@ -173,7 +173,7 @@ __device__ __forceinline__ void task_loop(const NllArgs& A, TaskShared& S, doubl
         }
         double uval = acc;
         if constexpr (PROD) {
-            bad |= !unit_in_range(un, IsRatio<Ev>::value);
+            bad |= !unit_ok<Ev>(A, un);
             uval = unit_value<Ev>(A, un);
         }
         const unsigned anybad = __any_sync(0xffffffffu, bad);
