@@ -8,6 +8,10 @@
 
 namespace pfb {
 
+#ifndef PFB_TASK_ITEMS_PER_SM
+#define PFB_TASK_ITEMS_PER_SM 40  // C1 / C5: the warp-task kernel from ~24M events
+#endif
+
 static constexpr int kG = PFB_GAUSSIAN, kE = PFB_EXPONENTIAL, kP = PFB_POLYNOMIAL;
 
 static int kinds_of(const NllArgs& A) {
@@ -84,7 +88,7 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // 2: bulk prefetch; 3: the TMA unit kernel -- the same canonical blocks
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A)) {
             const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
-            if (A.tma == 1 && A.warps == 0 && nitems >= 40 * (int64_t)sm_count)
+            if (A.tma == 1 && A.warps == 0 && nitems >= PFB_TASK_ITEMS_PER_SM * (int64_t)sm_count)
                 return launch_task<EvSum2GE>(A, stream, sm_count);
             return launch_prod<EvSum2GE>(A, stream, sm_count);
         }
