@@ -539,7 +539,10 @@ class Measure:
             rec["step"] = ("the C objective (DeviceFitManager.fcn) with c1 moved: device GL quadrature kernel "
                            "(the polynomial's norm) + fused NLL kernel; CUDA events around the call")
         if self.rank == 0 and self.world == 1:
-            rec["parity"], rec["cpu_baseline"] = self.parity_and_cpu(t["nll"], cpu_budget_s)
+            dev_nll = t["nll"]
+            if self.model == "c2p":  # the timed steps alternate c1; parity at the Variables' own point
+                dev_nll = float(self.c2p_fcn(self.c2p_x.copy()))
+            rec["parity"], rec["cpu_baseline"] = self.parity_and_cpu(dev_nll, cpu_budget_s)
             if with_fit:
                 rec["fit"] = self.fits()
         return rec

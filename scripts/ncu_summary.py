@@ -1,8 +1,11 @@
 """Summarise ncu reports (.ncu-rep) into the tracked profiles/ directory.
 
     python scripts/ncu_summary.py gpurun_out/prof_c2.ncu-rep [...] > profiles/r1_<name>.md
+    python scripts/ncu_summary.py gpurun_out/prof_r2c_c2 [...]   # exported pages (gpu_round_profile.sh)
 
-Reads the `details` and `raw` pages with `ncu -i` (no GPU needed) and prints a
+Reads the `details` and `raw` pages with `ncu -i` (no GPU needed) -- or the
+pages gpu_round_profile.sh exported (<prefix>_details.txt, <prefix>_raw.csv)
+when the report itself did not travel back -- and prints a
 markdown table of the numbers DESIGN.md cites: duration, DRAM bytes and
 throughput, FP64-pipe activity, occupancy, issue statistics, top stall reasons.
 """
@@ -10,6 +13,8 @@ throughput, FP64-pipe activity, occupancy, issue statistics, top stall reasons.
 from __future__ import annotations
 
 import csv
+import os
+import re
 import subprocess
 import sys
 
@@ -27,10 +32,29 @@ def ncu_csv(path: str, page: str):
     return list(csv.reader(out.splitlines()))
 
 
+def exported(prefix: str):
+    """(kernel, details values, raw rows) from the exported text/CSV pages."""
+    vals, kernel = {}, None
+    for line in open(prefix + "_details.txt"):
+        m = re.match(r"^\s{4}(\S.*?)\s{2,}(\S+(?: \S+)?)?\s+([-\d.,]+)\s*$", line)
+        if m and m.group(1).strip() in DETAILS:
+            vals[m.group(1).strip()] = f"{m.group(3)} {m.group(2) or ''}".strip()
+        elif kernel is None and line.strip() and not line.startswith(" ") and "(" in line:
+            kernel = line.strip()
+    with open(prefix + "_raw.csv") as f:
+        raw = list(csv.reader(f))
+    return kernel, vals, raw
+
+
 def summarize(path: str) -> list[str]:
+    lines = [f"### `{path.split('/')[-1]}`", ""]
+    if not path.endswith(".ncu-rep") and os.path.exists(path + "_raw.csv"):
+        kernel, vals, raw = exported(path)
+        if len(raw) >= 3 and "Kernel Name" in raw[0]:
+            kernel = raw[2][raw[0].index("Kernel Name")]
+        return finish(lines, kernel, vals, raw)
     rows = ncu_csv(path, "details")
     hdr = rows[0]
-    lines = [f"### `{path.split('/')[-1]}`", ""]
     kernel = None
     vals = {}
     for row in rows[1:]:
@@ -38,6 +62,10 @@ def summarize(path: str) -> list[str]:
         kernel = kernel or d.get("Kernel Name")
         if d.get("Metric Name") in DETAILS:
             vals[d["Metric Name"]] = f"{d['Metric Value']} {d.get('Metric Unit', '')}".strip()
+    return finish(lines, kernel, vals, ncu_csv(path, "raw"))
+
+
+def finish(lines, kernel, vals, raw) -> list[str]:
     lines.append(f"kernel: `{(kernel or '')[:160]}`")
     lines.append("")
     lines.append("| metric | value |")
@@ -45,7 +73,6 @@ def summarize(path: str) -> list[str]:
     for k in DETAILS:
         if k in vals:
             lines.append(f"| {k} | {vals[k]} |")
-    raw = ncu_csv(path, "raw")
     if len(raw) >= 3:
         h, units, v = raw[0], raw[1], raw[2]
         for k in RAW:
