@@ -354,6 +354,10 @@ typedef struct {
     int64_t in_boundary;  /* stats["in_boundary_draws"] (Dalitz) */
     int64_t produced;     /* events written */
     double observed;      /* PFB_E_ENVELOPE_HIT: the chunk's maximum density */
+    int64_t ambiguous;    /* candidates of the consumed chunks whose accept decision (or the chunk's
+                             envelope check) lies within 2^-47 relative of the density: 0 means the
+                             sample is the reference's bit for bit (device densities follow the
+                             reference's operation order; libm may differ from numpy by ulps) */
 } pfb_gen_stats;
 
 /* mcgen._scan_max (mcgen.py:52-54): max of the plan's unnormalised root

@@ -99,7 +99,7 @@ class PfbPcg64(ctypes.Structure):
 
 class PfbGenStats(ctypes.Structure):
     _fields_ = [("attempts", c_int64), ("accepted", c_int64), ("in_boundary", c_int64), ("produced", c_int64),
-                ("observed", c_double)]
+                ("observed", c_double), ("ambiguous", c_int64)]
 
 
 _PTR = c_void_p

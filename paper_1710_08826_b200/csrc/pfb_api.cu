@@ -53,6 +53,7 @@ struct PcgHostResult {
     int status;
     int64_t attempts, accepted, in_boundary, produced;
     double observed;
+    int64_t ambiguous;
 };
 cudaError_t pcg_generate_entry(const NllArgs& A, int dalitz, const double* box, double envelope,
                                const GridConsts* g, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
@@ -2248,6 +2249,7 @@ static int gen_status(const PcgHostResult& R, pfb_gen_stats* stats) {
         stats->in_boundary = R.in_boundary;
         stats->produced = R.produced;
         stats->observed = R.observed;
+        stats->ambiguous = R.ambiguous;
     }
     switch (R.status) {
         case 0: return PFB_OK;

@@ -282,6 +282,8 @@ def _run_streams(spec, budget, gen_one, stats, dalitz: bool):
         if not dalitz:
             stats["attempts"] = stats.get("attempts", 0) + gs.attempts
         stats["accepted"] = stats.get("accepted", 0) + gs.accepted
+        # decisions within 2^-47 of the density (0: the reference's sample bit for bit)
+        stats["ambiguous"] = stats.get("ambiguous", 0) + gs.ambiguous
         offset += cnt
 
 

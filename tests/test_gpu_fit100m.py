@@ -51,8 +51,9 @@ def run_fit(ref):
         t.magnitude.name, t.phase.name = f"{nm}_mag", f"{nm}_ph"
     _, _, truth = models.c3(models.C3_TERMS, grid=tuple(ref["grid"]))
     t0 = time.perf_counter()
+    gen_stats = {}
     ds = generate_dalitz(truth, P.DecayChannel(*models.D_CHANNEL_T), GenSpec(**ref["spec"]),
-                         observables=(s12, s13))
+                         observables=(s12, s13), stats=gen_stats)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     nll_start = pf.nll(pdf, ds)
@@ -60,7 +61,8 @@ def run_fit(ref):
     t0 = time.perf_counter()
     result = FitManager(pdf, ds).fit()
     t_fit = time.perf_counter() - t0
-    return result, ds, {"generate_s": t_gen, "first_nll_s": t_first, "nll_start": nll_start, "fit_s": t_fit}
+    return result, ds, {"generate_s": t_gen, "first_nll_s": t_first, "nll_start": nll_start, "fit_s": t_fit,
+                        "ambiguous": gen_stats["ambiguous"]}
 
 
 @pytest.fixture(scope="module")
@@ -72,6 +74,7 @@ def ref(golden_dir):
 
 def test_100m_dalitz_fit_matches_reference(ref):
     result, ds, tm = run_fit(ref)
+    assert tm["ambiguous"] == 0  # every accept decision clear of its density by > 2^-47
     cols = ref["columns"]
     for name in ("s12", "s13"):
         a = _host(ds.column(name))
