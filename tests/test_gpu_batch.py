@@ -93,6 +93,35 @@ def test_batch_equals_single_bitwise(pf, config):
     assert any(w[0] == "ok" for w in want)
 
 
+def test_sixteen_points_all_blocks_deferred(pf):
+    """16 points (the batch maximum) over 2000 blocks where every block holds
+    an event whose gaussian exponent lies in (-746, -600) at every point: all
+    16 x 2000 (block, point) pairs go to the exact fix-up list at once (its
+    capacity is points x blocks), and each value is still bitwise
+    its own single-point NLL."""
+    rng = np.random.default_rng(11)
+    nb = 2000
+    n = nb * 4096
+    (x, y), pdf, params = models.c2()
+    xs = np.clip(rng.normal(5, 0.5, n), 3, 7)  # z <= 17 elsewhere
+    # z ~ 37.5 at sigma ~ 0.12: u ~ -704, past the fast path's exponent budget
+    # (690 - |ln c|) yet a positive normal density in the reference
+    xs[::4096] = 5.0 + 37.55 * 0.12
+    ds = models.dataset([x, y], [xs, np.clip(rng.exponential(2.5, n), 0, 10)])
+    pts = [np.array([5.0, 0.12 * (1.0 + 0.0002 * k), -0.4]) for k in range(16)]
+    ctx = pf.device_context(0)
+    want = []
+    for p in pts:
+        before = ctx.launch_count()
+        want.append(outcome(single(pf, pdf, ds, params, p)))
+        assert ctx.launch_count() - before == 2  # the pass + the fix-up of every block
+    assert all(w[0] == "ok" for w in want)
+    snaps, norms = points_eval(pf, pdf, ds, params, pts)
+    got = pf.DeviceBackend().evaluate_batch(pdf, {"x": ds.column("x"), "y": ds.column("y")}, snaps, norms, 0,
+                                            ds.n_events)
+    assert [outcome(r) for r in got] == want
+
+
 def test_batch_error_attributed_to_its_point(pf):
     x = P.Variable.observable("x", 0.0, 1.0)
     c0 = P.Variable("c0", 0.5, -1.0, 2.0)
