@@ -154,6 +154,43 @@ int main() {
                "\"host_roundtrip_us\": %.2f}\n",
                ev_time(f2, false), ev_time(f2, true), host_time(f2));
     }
+    // one kernel of the C2 launch shape as a single-node graph vs a stream launch
+    {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        big_smem_k<<<148, 544, 196608, s>>>(big, (double*)sink);
+        CK(cudaStreamEndCapture(s, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        auto f = [&] { cudaGraphLaunch(ge, s); };
+        printf("{\"case\": \"graph(148x544 + 196KB smem + 6.4KB param)\", \"event_us\": %.2f, "
+               "\"event_us_after_spin\": %.2f, \"host_roundtrip_us\": %.2f}\n",
+               ev_time(f, false), ev_time(f, true), host_time(f));
+        // the same graph with the kernel's 6.4 KB parameter block replaced before
+        // every launch (what a per-call NLL launch through a cached graph does)
+        cudaGraphNode_t nodes[4];
+        size_t nn = 4;
+        CK(cudaGraphGetNodes(g, nodes, &nn));
+        cudaKernelNodeParams kp;
+        CK(cudaGraphKernelNodeGetParams(nodes[0], &kp));
+        Big big2 = big;
+        double* sinkd = (double*)sink;
+        void* args[2] = {&big2, &sinkd};
+        kp.kernelParams = args;
+        int flip = 0;
+        auto fset = [&] {
+            big2.v[0] = (double)(++flip);
+            cudaGraphExecKernelNodeSetParams(ge, nodes[0], &kp);
+            cudaGraphLaunch(ge, s);
+        };
+        printf("{\"case\": \"graph + SetParams each call (148x544 + 196KB smem + 6.4KB param)\", \"event_us\": %.2f, "
+               "\"event_us_after_spin\": %.2f, \"host_roundtrip_us\": %.2f}\n",
+               ev_time(fset, false), ev_time(fset, true), host_time(fset));
+        // events inside the graph's stream order but around nothing: the event pair's own floor
+        auto nothing = [&] {};
+        printf("{\"case\": \"event pair around nothing\", \"event_us\": %.2f, \"event_us_after_spin\": %.2f}\n",
+               ev_time(nothing, false), ev_time(nothing, true));
+    }
     // persistent doorbell round trip (host write -> device poll -> mapped result -> host poll)
     {
         unsigned* hbell;
