@@ -884,10 +884,14 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         const double mu = row[0], is = row[1], al = row[2];
         A->g2_c2 = (-0.5 * is) * is;
         A->g2_amu = al * mu;
-        const double lim = 256.0 / fabs(al);
+        // certified |w| = |x - mu| < min(256 / |alpha| - |mu|, 1000 sigma): |alpha x| < 256
+        // (the reference's exp(alpha x) stays normal) and d >= -5e5 - 512 (the
+        // exponential's scale index cannot wrap)
+        double lim = fmin(256.0 / fabs(al) - fabs(mu), 1000.0 / is);
+        if (!(lim > 0.0)) lim = 0.0;
         uint64_t bits;
         memcpy(&bits, &lim, 8);
-        A->g2_xlim = al == 0.0 ? 0x7ff00000 : (int32_t)(bits >> 32);
+        A->g2_wlim = (int32_t)(bits >> 32);
     }
     A->nterm = (int)p->terms.size();
     for (int t = 0; t < A->nterm; ++t) {
@@ -919,6 +923,18 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         T.thr = 690.0 - budget;
         row[kPtLeafWords + 2 * t] = T.logcoef;
         row[kPtLeafWords + 2 * t + 1] = T.thr;
+    }
+    A->g2_qcert = 0;
+    if (m == 0 && A->nleaf == 2 && A->nterm == 2 && A->leaf[0].kind == PFB_GAUSSIAN &&
+        A->leaf[1].kind == PFB_EXPONENTIAL) {
+        // EvSum2GE: q = c1 + c0 e^d with d = u0 - u1 <= alpha^2 sigma^2 / 2 - alpha mu
+        // for every x, and q >= c1: when that range sits inside the unit check's
+        // [2^-250, 2^251) no event can leave it and the kernel drops the
+        // per-event range tracking (EvSum2GE<true>)
+        const double mu = row[0], sg = 1.0 / row[1], al = row[2];
+        const double c0 = A->term[0].coef, c1 = A->term[1].coef;
+        const double qmax = c1 + c0 * exp(0.5 * (al * al) * (sg * sg) - al * mu);
+        A->g2_qcert = (c1 >= 0x1p-249 && c0 >= 0.0 && qmax * (1.0 + 1e-6) <= 0x1p249) ? 1 : 0;
     }
     return true;
 }

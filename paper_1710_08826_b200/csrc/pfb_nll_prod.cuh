@@ -141,14 +141,16 @@ constexpr double kExpK = 369.3299304675746;
 constexpr double kLn2o256Hi = 0x1.62e42fee00000p-9;
 constexpr double kLn2o256Lo = 0x1.a39ef35793c76p-41;
 
-// c * exp(d) + a for d <= 256 with tab[j] = c 2^(j/256):
+// c * exp(d) + a for d in [-5.2e5, 256] with tab[j] = c 2^(j/256):
 // d = k ln2/256 + r, |r| <= ln2/512; exp(r) by its degree-4 Taylor polynomial
 // (truncation |r|^5/120 < 2^-54), times tab[k mod 256] with 2^(k div 256) added
 // to its exponent (integer op), plus a in the same FMA.  <= 3 ulp; 9 FP64
-// operations.  Below d = -500 the scale is held at 2^-722 (one integer max
-// on k): the term is then < e^-300 |c| whatever r is, so callers whose
-// |a| >= e^-200 |c| get a exactly, and c 2^(k div 256) stays a normal double
-// (no clamp on d; NaN / -inf d come from non-finite x, which callers reject).
+// operations (kd * hi is exact for d > -5600; below, r stays small and the
+// term negligible).  Below d = -500 the scale is held at 2^-722 (one integer
+// max on k): the term is then < e^-300 |c| whatever r is, so callers whose
+// |a| >= e^-200 |c| get a exactly, and c 2^(k div 256) stays a normal double.
+// Callers bound d below (k, the low word of the magic-number sum, must not
+// wrap: EvSum2GE certifies |x - mu| < 1000 sigma, d > -5.1e5).
 constexpr int kKMin = -184665;  // floor(-500 * 256 / ln2)
 __device__ __forceinline__ double cexp_tab_add(double d, const double* tab, double a) {
     const double t = fma(d, kExpK, 0x1.8p52);
@@ -161,7 +163,7 @@ __device__ __forceinline__ double cexp_tab_add(double d, const double* tab, doub
     q = fma(q, r, 1.0);
     q = fma(q, r, 1.0);
     const double tv = tab[k & (kTabN - 1)];
-    const double cs = __hiloint2double(__double2hiint(tv) + ((k >> 8) << 20), __double2loint(tv));
+    const double cs = __hiloint2double(__double2hiint(tv) + (int)((unsigned)(k >> 8) << 20), __double2loint(tv));
     return fma(cs, q, a);
 }
 
@@ -177,10 +179,12 @@ __device__ __forceinline__ double cexp_tab_add(double d, const double* tab, doub
 // Leaf/term layout fixed by the dispatcher: leaf 0 gaussian (ptv[0][0..1] =
 // mu, 1/sigma), leaf 1 exponential (ptv[0][2] = alpha), term t = leaf t, and
 // |ln c_t| < 200.
-// Certification (unit-level, integer ops): max |x| < 256 / |alpha| over the
-// unit (so |u1| < 256; the high words' maximum, Ev::XMAX) and q in
-// [2^-250, 2^251) put p in [2^-620, 2^620] and keep the reference's exp(u1)
-// finite and normal.  Below d = -500 cexp_tab_add holds the scale (integer
+// Certification (unit-level, integer ops): max |x - mu| over the unit below
+// min(256 / |alpha| - |mu|, 1000 sigma) (the high words' maximum, Ev::XMAX;
+// so |u1| < 256 and d >= -5e5 - 512) and q in [2^-250, 2^251) -- proven on
+// the host from the parameters alone when possible (q >= c1, d <= alpha^2
+// sigma^2 / 2 - alpha mu: EvSum2GE<true>, no per-event tracking) -- put p in
+// [2^-620, 2^620] and keep the reference's exp(u1) finite and normal.  Below d = -500 cexp_tab_add holds the scale (integer
 // max): c0 e^d <= e^-300 c1 < ulp(c1) / 2 -- q is c1 exactly -- and
 // c0 2^(k div 256) stays a normal double.  Whatever an uncertified event
 // computes is discarded (its block is deferred to the exact fix-up).
@@ -190,13 +194,17 @@ __device__ __forceinline__ double cexp_tab_add(double d, const double* tab, doub
 #ifndef PFB_SUM2GE_MINB
 #define PFB_SUM2GE_MINB 3
 #endif
+template <bool QC = false>
 struct EvSum2GE {
     static constexpr int NC = 1;
     static constexpr int U = PFB_SUM2GE_U;
     static constexpr int MINB = PFB_SUM2GE_MINB;
     static constexpr bool TAB = true;     // tab = c0 2^(j/256)
     static constexpr bool LSCALE = true;  // unit sum of l times alpha
-    static constexpr bool XMAX = true;    // unit check max |x| < 256 / |alpha|
+    static constexpr bool XMAX = true;    // unit check max |x - mu| < the host bound (g2_wlim)
+    static constexpr bool QCERT = QC;     // q range certified on the host (g2_qcert): no per-event tracking
+
+    __device__ static __forceinline__ double cert_value(const NllArgs& A, double x) { return x - A.ptv[0][0]; }
 
     __device__ static __forceinline__ double tab_entry(const NllArgs& A, int j) {
         return A.term[0].coef * kExp2Tab256[j];
@@ -312,6 +320,14 @@ template <class Ev>
 struct HasXMax<Ev, decltype((void)Ev::XMAX)> {
     static constexpr bool value = Ev::XMAX;
 };
+template <class Ev, class = void>
+struct HasQCert {
+    static constexpr bool value = false;
+};
+template <class Ev>
+struct HasQCert<Ev, decltype((void)Ev::QCERT)> {
+    static constexpr bool value = Ev::QCERT;
+};
 // p = q / r^POW for ratio evaluators
 template <class Ev, class = void>
 struct RatioPow {
@@ -351,13 +367,13 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
         }
     }
     if constexpr (HasXMax<Ev>::value) {
-        const int a = (TAIL && e >= n) ? 0 : (__double2hiint(x[0].x) & 0x7fffffff);
-        const int b = (TAIL && e + 1 >= n) ? 0 : (__double2hiint(x[0].y) & 0x7fffffff);
+        const int a = (TAIL && e >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].x)) & 0x7fffffff);
+        const int b = (TAIL && e + 1 >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].y)) & 0x7fffffff);
         u.xhi = max(u.xhi, max(a, b));
     }
 #if PFB_UNIT_MINMAX
     bad |= !(okx && oky);
-    {
+    if constexpr (!HasQCert<Ev>::value) {  // (certified: the initial qlo / qhi pass the unit check)
         const int a = __double2hiint(q.x), b = __double2hiint(q.y);
         u.qlo = min(u.qlo, min(a, b));
         u.qhi = max(u.qhi, max(a, b));
@@ -412,7 +428,7 @@ __device__ __forceinline__ bool unit_in_range(const Unit& u, bool ratio) {
 template <class Ev>
 __device__ __forceinline__ bool unit_ok(const NllArgs& A, const Unit& u) {
     bool ok = unit_in_range(u, IsRatio<Ev>::value);
-    if constexpr (HasXMax<Ev>::value) ok = ok && u.xhi < A.g2_xlim;
+    if constexpr (HasXMax<Ev>::value) ok = ok && u.xhi < A.g2_wlim;
     return ok;
 }
 

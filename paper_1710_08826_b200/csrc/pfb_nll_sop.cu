@@ -70,7 +70,7 @@ int persist_kind_sop(const NllArgs& A, int nc) {
 }
 
 cudaError_t launch_persist_sop(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count) {
-    if (kind == 1) return launch_persist<EvSum2GE, true>(P, stream, sm_count);
+    if (kind == 1) return launch_persist<EvSum2GE<>, true>(P, stream, sm_count);
     if (kind == 2) return launch_persist<EvSop<2, 2, 1, true, kG | kE << 2>, false>(P, stream, sm_count);
     return cudaErrorInvalidValue;
 }
@@ -89,8 +89,10 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A)) {
             const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
             if (A.tma == 1 && A.warps == 0 && nitems >= PFB_TASK_ITEMS_PER_SM * (int64_t)sm_count)
-                return launch_task<EvSum2GE>(A, stream, sm_count);
-            return launch_prod<EvSum2GE>(A, stream, sm_count);
+                return A.g2_qcert ? launch_task<EvSum2GE<true>>(A, stream, sm_count)
+                                  : launch_task<EvSum2GE<>>(A, stream, sm_count);
+            return A.g2_qcert ? launch_prod<EvSum2GE<true>>(A, stream, sm_count)
+                              : launch_prod<EvSum2GE<>>(A, stream, sm_count);
         }
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2))
             return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);

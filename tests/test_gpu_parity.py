@@ -82,6 +82,38 @@ def test_c1_sumpdf_parity(pf, golden_dir):
         np.testing.assert_allclose(bs, g[f"bsums_{i}"], rtol=1e-12)
 
 
+def test_c1_random_points_and_far_outliers(pf, golden_dir):
+    """The C1 product-mode evaluator (EvSum2GE) against the reference's own
+    nll on the same events at 30 random parameter points (<= 1e-12), and with
+    events so far from a very narrow gaussian (|x - mu| = 5000 sigma: d ~
+    -1.25e7, where the exponential's integer scale index would wrap) that
+    their units must fail the |x - mu| certificate and take the exact fix-up."""
+    g = load(golden_dir, "c1_sumpdf.npz")
+    x, pdf, params = models.c1()
+    ds = models.dataset([x], [g["x"]])
+    rng = np.random.default_rng(21)
+    for _ in range(30):
+        pt = [rng.uniform(4.5, 5.5), rng.uniform(0.3, 0.8), rng.uniform(-0.5, -0.1), rng.uniform(0.1, 0.6)]
+        for v, val in zip(params, pt):
+            P.set_value(v, val)
+        snap = P.snapshot(pdf.param_closure())
+        dev = pf.nll(pdf, ds)
+        with pf.reference_norms():
+            want = P.nll(pdf, ds, snap, P.Backend("serial"), P.NormalizationStore())
+        assert rel(dev, want) <= 1e-12, (pt, dev, want)
+    xv = P.Variable.observable("x", 0.0, 10.0)
+    mu, sg = P.Variable("mu", 5.0, 0.0, 10.0), P.Variable("sg", 0.001, 1e-4, 5.0)
+    al, f = P.Variable("al", -0.3, -5.0, 5.0), P.Variable("f", 0.3, 0.0, 1.0)
+    narrow = P.add_pdf([P.gaussian(xv, mu, sg), P.exponential(xv, al)], [f])
+    xs = np.concatenate([rng.normal(5.0, 0.001, 20000), rng.uniform(0.0, 10.0, 20000)])
+    xs[::997] = 0.0  # |x - mu| = 5000 sigma
+    dsn = models.dataset([xv], [xs])
+    snap = P.snapshot(narrow.param_closure())
+    with pf.reference_norms():
+        want = P.nll(narrow, dsn, snap, P.Backend("serial"), P.NormalizationStore())
+    assert rel(pf.nll(narrow, dsn), want) <= 1e-12
+
+
 def test_c2_prod_parity_and_shards(pf, golden_dir):
     g = load(golden_dir, "c2_prod.npz")
     (x, y), pdf, params = models.c2()
