@@ -316,18 +316,18 @@ struct EvSop {
         *ok = good && live;
         if (NT == 1 || (!EXACT && A.nterm == 1)) {
             if (!has_value_leaf()) return -Lt[0];
-            return (A.term[0].vmask ? -(Lt[0] + log(Vt[0])) : -Lt[0]);
+            return (A.term[0].vmask ? -(Lt[0] + fast_log(Vt[0])) : -Lt[0]);
         }
         if (NT == 2 || (!EXACT && A.nterm == 2)) {
             const double d = Lt[0] - Lt[1];
             const double e = exp(-fabs(d));
             s = d >= 0.0 ? fma(Vt[1], e, Vt[0]) : fma(Vt[0], e, Vt[1]);
-            return -(fmax(Lt[0], Lt[1]) + log(s));
+            return -(fmax(Lt[0], Lt[1]) + fast_log(s));
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t)
             if (EXACT || t < A.nterm) s = fma(Vt[t], exp(Lt[t] - Lm), s);
-        return -(Lm + log(s));
+        return -(Lm + fast_log(s));
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[NC_],
@@ -461,7 +461,7 @@ struct EvDalitz {
                                                  bool* ok) {
         const double p = prob(A, s12, s13, ok);
         *ok = *ok && (p > 1e-300) && (p < 1e300);
-        return -log(p);
+        return -fast_log(p);
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
@@ -648,7 +648,7 @@ struct EvDalitzCached {
         const double I = fma(tr, tr, ti * ti);
         const double p = I * A.inv_norm;
         *ok = (p > 1e-300) && (p < 1e300);
-        return -log(p);
+        return -fast_log(p);
     }
 
     __device__ static __forceinline__ double2 eval2(const NllArgs& A, const double2 (&x)[2],
