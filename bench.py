@@ -561,8 +561,11 @@ def spawn_ranks(args) -> int:
         port = s.getsockname()[1]
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines visible on stderr
+    # torch.distributed.run resolves abbreviated options over the whole command
+    # line: pass --n as --events (its unambiguous spelling)
+    fwd = ["--events" if a == "--n" else ("--events=" + a[4:] if a.startswith("--n=") else a) for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + fwd
     return subprocess.call(cmd, env=env)
 
 
@@ -573,7 +576,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="override events per GPU")
+    ap.add_argument("--n", "--events", dest="n", type=int, default=0, help="override events per GPU")
     ap.add_argument("--sub", default=",".join(SUBS_DEFAULT),
                     help="sub-result configs at N=1 ('none' to skip)")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "fused", "peer"],
