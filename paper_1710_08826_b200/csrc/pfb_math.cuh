@@ -358,6 +358,12 @@ __device__ __forceinline__ double log_unit(double m) {
     return fma(p, r, t.y);
 }
 
+// (double)i without I2F (an XU-pipe op): 1.5 * 2^52 + 2^31 + i, exactly, minus
+// the same constant.
+__device__ __forceinline__ double int_to_double(int i) {
+    return __hiloint2double(0x43380000, i ^ (int)0x80000000) - 0x1.800008p52;
+}
+
 // ln x for a positive normal double: x = m 2^e, m in [1, 2), e converted
 // without I2F (magic-number add), ln x = e ln2 + log_unit(m).  ~14 integer /
 // FP64 instructions, no XU-pipe op (libm's log issues an I2F and a MUFU.RCP64H
@@ -367,7 +373,7 @@ __device__ __forceinline__ double log_unit(double m) {
 __device__ __forceinline__ double fast_log(double x) {
     const int hi = __double2hiint(x);
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
-    const double fe = __hiloint2double(0x43380000, ((hi >> 20) - 1023) ^ (int)0x80000000) - 0x1.800008p52;
+    const double fe = int_to_double((hi >> 20) - 1023);
     return fma(fe, kLn2Hi, fma(fe, kLn2Lo, log_unit(m)));
 }
 

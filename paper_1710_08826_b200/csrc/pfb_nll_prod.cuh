@@ -457,10 +457,10 @@ template <class Ev>
 __device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u) {
     if constexpr (IsRatio<Ev>::value) {
         constexpr double pw = (double)RatioPow<Ev>::value;
-        const double fe = (double)u.ex - pw * (double)u.exd;
+        const double fe = fma(-pw, int_to_double(u.exd), int_to_double(u.ex));
         return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, fma(-pw, log_unit(u.md), log_unit(u.m))));
     } else {
-        const double fe = (double)u.ex;
+        const double fe = int_to_double(u.ex);
         // explicit fma / add: no contraction choice left to the compiler, so
         // every kernel shell (bulk, task, TMA, SIMT, persistent) gives the same bits
         double s;
