@@ -285,6 +285,78 @@ struct EvGaussPoly {
     }
 };
 
+// Any single-term product with value leaves (ProdPdf of gaussians,
+// exponentials and polynomials on NC columns; a lone polynomial): the
+// generalisation of EvGaussPoly with the leaf kinds fixed at compile time
+// (KINDS, 2 bits per leaf as EvSop; -1: read per leaf at run time) and the
+// Horner length read per leaf.
+//   l = ln c + sum of the exp-type leaves' exponents (log sum),
+//   q = product of the polynomial values (unit product).
+// Certification as EvSop's single-term form: gaussian u >= -600, exponential
+// |u| <= 600, the exponent budget sum |u| + sum (|log2 v| ln2 + 1) <= thr, and
+// q within the unit range (positive, 2^+-250).  Layout checked by the
+// dispatcher (prod1_ok): one term, every exp-type leaf in its emask, every
+// polynomial in its vmask.
+template <int NC_, int NL, int KINDS>
+struct EvProd1 {
+    static constexpr int NC = NC_;
+    static constexpr int U = 2;
+    static constexpr int MINB = 3;
+
+    __device__ static __forceinline__ double pick(const double2 (&x)[NC_], int col, bool hi) {
+        double r = hi ? x[0].y : x[0].x;
+#pragma unroll
+        for (int c = 1; c < NC_; ++c)
+            if (col == c) r = hi ? x[c].y : x[c].x;
+        return r;
+    }
+
+    __device__ static __forceinline__ double one(const NllArgs& A, const double2 (&x)[NC_], bool hi, bool& ok,
+                                                 double& l) {
+        const double* v = A.ptv[0];
+        double q = 1.0, budget = 0.0;
+        double ls = v[kPtLeafWords];
+        bool good = true;
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            const SopLeaf& L = A.leaf[k];
+            const int kind = KINDS >= 0 ? (KINDS >> (2 * k)) & 3 : L.kind;
+            const double xv = pick(x, L.col, hi);
+            if (kind == PFB_GAUSSIAN) {
+                const double z = __dmul_rn(__dsub_rn(xv, v[L.voff]), v[L.voff + 1]);
+                const double u = __dmul_rn(__dmul_rn(-0.5, z), z);
+                good &= u >= -600.0;
+                budget = __dsub_rn(budget, u);
+                ls = __dadd_rn(ls, u);
+            } else if (kind == PFB_EXPONENTIAL) {
+                const double u = __dmul_rn(v[L.voff], xv);
+                good &= fabs(u) <= 600.0;
+                budget = __dadd_rn(budget, fabs(u));
+                ls = __dadd_rn(ls, u);
+            } else {  // polynomial (Horner, as polyval)
+                const double* c = v + L.voff;
+                double p = c[L.nv - 1];
+#pragma unroll 1
+                for (int i = L.nv - 2; i >= 0; --i) p = fma(p, xv, c[i]);
+                const int e = ((__double2hiint(p) >> 20) & 0x7ff) - 1023;
+                budget = fma(int_to_double(e < 0 ? -e : e), 0.6931471805599453, __dadd_rn(budget, 1.0));
+                q = __dmul_rn(q, p);
+            }
+        }
+        ok = good && budget <= v[kPtLeafWords + 1];
+        l = ls;
+        return q;
+    }
+
+    __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[NC_], bool& okx,
+                                                    bool& oky, const double*, double2& l) {
+        double2 q;
+        q.x = one(A, x, false, okx, l.x);
+        q.y = one(A, x, true, oky, l.y);
+        return q;
+    }
+};
+
 // Running state of one 16-event unit: the product m * 2^ex of the q factors,
 // for ratio evaluators (Ev::RATIO, p = q / r) the product md * 2^exd of the
 // r factors, and the sum ls of the log factors l.
@@ -1234,10 +1306,15 @@ static cudaError_t launch_prod(const NllArgs& A, cudaStream_t stream, int sm_cou
     // pipeline 1: per-warp bulk prefetch for single-column evaluators, the
     // TMA-fed unit kernel (producer warp + two consumer teams) for two-column
     // ones (Dalitz: 3% faster than the register window, measured);
-    // 2: bulk prefetch for all; 3: the TMA unit kernel for all
-    if (A.warps == 0 && (A.tma == 3 || (Ev::NC == 2 && A.tma == 1)))
-        return launch_tma_unit<Ev, true>(A, stream, sm_count);
-    if (A.warps == 0 && (A.tma == 2 || (Ev::NC == 1 && A.tma == 1))) return launch_prod_bulk<Ev>(A, stream, sm_count);
+    // 2: bulk prefetch for all; 3: the TMA unit kernel for all.  Three or more
+    // columns: the register-window SIMT kernel only (the staging kernels are
+    // sized for one or two 32 KB column blocks per stage)
+    if constexpr (Ev::NC <= 2) {
+        if (A.warps == 0 && (A.tma == 3 || (Ev::NC == 2 && A.tma == 1)))
+            return launch_tma_unit<Ev, true>(A, stream, sm_count);
+        if (A.warps == 0 && (A.tma == 2 || (Ev::NC == 1 && A.tma == 1)))
+            return launch_prod_bulk<Ev>(A, stream, sm_count);
+    }
     switch (A.warps) {
         case 1:
             return launch_prod_one<1, Ev>(A, stream, sm_count);

@@ -48,6 +48,25 @@ static bool gp_ok(const NllArgs& A) {
     return fabs(A.term[0].logcoef) < 600.0;
 }
 
+// EvProd1's layout: one term, exp-type leaves in its emask, polynomials in its
+// vmask, at least one polynomial (without one the log-domain unit sums need
+// no logarithm at all).
+static bool prod1_ok(const NllArgs& A) {
+    if (A.nterm != 1 || !(fabs(A.term[0].logcoef) < 600.0)) return false;
+    bool value = false;
+    for (int l = 0; l < A.nleaf; ++l) {
+        const SopLeaf& L = A.leaf[l];
+        const bool e = (A.term[0].emask >> l) & 1u, v = (A.term[0].vmask >> l) & 1u;
+        if (L.kind == PFB_POLYNOMIAL) {
+            if (!v || e || L.nv < 1) return false;
+            value = true;
+        } else if (!e || v) {
+            return false;
+        }
+    }
+    return value;
+}
+
 // pipeline 1: the unit-sum TMA kernel; 2: the reference-tree TMA kernel;
 // 0: the SIMT streaming kernel
 template <class Ev>
@@ -98,6 +117,9 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
             return launch_p<EvSop<1, 2, 2, true, kG | kE << 2>>(A, stream, sm_count);
         if (nl == 1 && nt == 1 && kinds == kG)
             return launch_stream<EvSop<1, 1, 1, true, kG>>(A, stream, sm_count);
+        // a lone polynomial: product mode (one log per 16 events)
+        if (nl == 1 && kinds == kP && A.tma && prod1_ok(A))
+            return launch_prod<EvProd1<1, 1, kP>>(A, stream, sm_count);
         if (nl == 1 && nt == 1) return launch_p<EvSop<1, 1, 1, true>>(A, stream, sm_count);
         if (nl == 2 && nt == 2) return launch_p<EvSop<1, 2, 2, true>>(A, stream, sm_count);
         return launch_p<EvSop<1>>(A, stream, sm_count);
@@ -120,9 +142,12 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         }
         if (nl == 2 && nt == 1 && kinds == (kG | kP << 2))
             return launch_stream<EvSop<2, 2, 1, true, kG | kP << 2>>(A, stream, sm_count);
+        // other single-term products with a polynomial factor: product mode
+        if (nl == 2 && A.tma && prod1_ok(A)) return launch_prod<EvProd1<2, 2, -1>>(A, stream, sm_count);
         return launch_p<EvSop<2>>(A, stream, sm_count);
     }
     // the kernels stream exactly the plan's columns (NC of them)
+    if (nc == 3 && nl == 3 && A.tma && prod1_ok(A)) return launch_prod<EvProd1<3, 3, -1>>(A, stream, sm_count);
     if (nc == 3) return launch_p<EvSop<3>>(A, stream, sm_count);
     return launch_p<EvSop<4>>(A, stream, sm_count);
 }
