@@ -820,6 +820,9 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
 template <class Ev, bool PROD>
 static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm_count) {
     constexpr int NC = Ev::NC;
+    // the team / stage phase bookkeeping needs S >= 3 stages (measured: a
+    // single stage with two teams never completes)
+    static_assert(NC <= 2, "TMA unit kernel: one or two columns");
     constexpr int S = NC == 1 ? 6 : (NC == 2 ? 3 : 1);
     const size_t smem = (size_t)S * NC * kBlock * sizeof(double);
     static bool configured = false;
