@@ -1,6 +1,8 @@
 """ProdPdf(gaussian(x), polynomial(y)) -- the C2p shape -- on its product-mode
 evaluator (EvGaussPoly: log sum of the gaussian exponents, unit product of
-the polynomial values, one logarithm per 16 events).
+the polynomial values, one logarithm per 16 events), and the general
+single-term product evaluator (EvProd1: a lone polynomial, exponential x
+polynomial, three-column products).
 
 * every product-mode shell (pipeline 1 / 3: TMA unit kernel, 2: bulk
   prefetch) gives bitwise the same block values;
@@ -142,3 +144,33 @@ def test_negative_polynomial_is_the_reference_error(pf):
         pf.nll(pdf, ds)
     assert type(dev_err.value) is type(ref_err.value)
     assert str(dev_err.value) == str(ref_err.value)
+
+
+@pytest.mark.parametrize("shape", ["poly", "expo_poly", "prod3"])
+def test_single_term_products_with_a_polynomial(pf, shape):
+    """EvProd1 on 1 / 2 / 3 columns: NLL within 1e-10 of the reference's own
+    nll on the same 1M events, product shells bitwise (pipelines 1, 2, 3 where
+    the shape has a staging kernel), the log-domain SIMT kernel (pipeline 0)
+    within 1e-10."""
+    rng = np.random.default_rng(17)
+    n = 1_000_000 + 333
+    x = P.Variable.observable("x", 0.0, 10.0)
+    y = P.Variable.observable("y", 0.0, 10.0)
+    z = P.Variable.observable("z", 0.0, 10.0)
+    poly = lambda o, cs: P.polynomial(o, [P.Variable(f"{o.name}c{k}", v, -10.0, 10.0) for k, v in enumerate(cs)])
+    if shape == "poly":
+        obs, pdf = [x], poly(x, (1.0, 0.2, 0.03, 0.001))
+    elif shape == "expo_poly":
+        obs, pdf = [x, y], P.prod_pdf([P.exponential(x, P.Variable("a", -0.2, -5.0, 5.0)), poly(y, (2.0, 0.1))])
+    else:
+        obs = [x, y, z]
+        pdf = P.prod_pdf([P.gaussian(x, P.Variable("m", 5.0, 0.0, 10.0), P.Variable("s", 1.5, 0.1, 5.0)),
+                          P.exponential(y, P.Variable("a", 0.1, -5.0, 5.0)), poly(z, (0.5, 1.0, 0.2))])
+    cols = [np.clip(rng.normal(5.0, 2.0, n), 0.0, 10.0) for _ in obs]
+    ds = pf.DeviceDataSet.from_columns(obs, cols, device=None)
+    want = ref_nll(pf, pdf, obs, cols)
+    got = {m: with_pipeline(pf, m, lambda: pf.nll(pdf, ds)) for m in (1, 2, 3, 0)}
+    if len(obs) <= 2:
+        assert got[1] == got[2] == got[3]
+    for m, v in got.items():
+        assert abs(v - want) <= RTOL * abs(want), (shape, m, v, want)
