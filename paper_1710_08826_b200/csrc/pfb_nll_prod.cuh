@@ -823,7 +823,9 @@ static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm
     // the team / stage phase bookkeeping needs S >= 3 stages (measured: a
     // single stage with two teams never completes)
     static_assert(NC <= 2, "TMA unit kernel: one or two columns");
-    constexpr int S = NC == 1 ? 6 : (NC == 2 ? 3 : 1);
+    // one-column stages: six of 32 KB, five when the evaluator's 2 KB shared
+    // table would push static + dynamic shared memory past the 227 KB limit
+    constexpr int S = NC == 1 ? (HasTab<Ev>::value ? 5 : 6) : 3;
     const size_t smem = (size_t)S * NC * kBlock * sizeof(double);
     static bool configured = false;
     if (!configured) {

@@ -114,6 +114,28 @@ def test_c1_random_points_and_far_outliers(pf, golden_dir):
     assert rel(pf.nll(narrow, dsn), want) <= 1e-12
 
 
+def test_c1_product_shells_bitwise(pf):
+    """The C1 product evaluator (EvSum2GE) through every shell the pipeline
+    modes select -- bulk prefetch (1, 2), TMA unit ring (3), warp tasks (1,
+    from ~24M events: exercised by tests/test_gpu_scale.py) -- gives the same
+    bits; the log-domain SIMT kernel (0) within 1e-12."""
+    x, pdf, params = models.c1()
+    rng = np.random.default_rng(8)
+    n = 3 * 1_000_000 + 4097
+    xs = np.clip(np.concatenate([rng.normal(5, 0.5, n // 3), rng.exponential(3.3, n - n // 3)]), 0, 10)
+    ds = models.dataset([x], [xs])
+    ctx = pf.device_context(0)
+    got = {}
+    try:
+        for mode in (1, 2, 3, 0):
+            ctx.set_pipeline(mode)
+            got[mode] = pf.nll(pdf, ds)
+    finally:
+        ctx.set_pipeline(1)
+    assert got[1] == got[2] == got[3]
+    assert rel(got[0], got[1]) <= 1e-12
+
+
 def test_c2_prod_parity_and_shards(pf, golden_dir):
     g = load(golden_dir, "c2_prod.npz")
     (x, y), pdf, params = models.c2()
