@@ -429,8 +429,6 @@ class Measure:
         """The metric through the C ABI with pinned host columns: H2D of all
         events + the result read-back inside every timed step."""
         torch, L = self.torch, self.L
-        if self.model == "c2p":
-            return None
         pinned = [torch.empty(self.n, dtype=torch.float64, pin_memory=True) for _ in self.arrays]
         for p, a in zip(pinned, self.arrays):
             p.numpy()[:] = a
@@ -547,6 +545,7 @@ class Measure:
         if self.model == "c2p":
             rec["step"] = ("the C objective (DeviceFitManager.fcn) with c1 moved: device GL quadrature kernel "
                            "(the polynomial's norm) + fused NLL kernel; CUDA events around the call")
+            rec["e2e_step"] = "the C ABI with host columns at the Variables' point (norms fixed, as every config's e2e)"
         if self.rank == 0 and self.world == 1:
             dev_nll = t["nll"]
             if self.model == "c2p":  # the timed steps alternate c1; parity at the Variables' own point
