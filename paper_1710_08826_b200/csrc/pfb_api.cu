@@ -181,6 +181,11 @@ struct pfb_ctx {
     void* bin_dev = nullptr;  // bin counts / contents
     int64_t bin_cap = 0;      // bytes
     unsigned long long* bin_key = nullptr;
+    // binned contents on the device and the host copy they were uploaded from
+    // (a fit calls binned_nll with the same contents every step)
+    double* bin_cont = nullptr;
+    int64_t bin_cont_cap = 0;
+    std::vector<double> bin_cont_host;
 };
 
 
@@ -399,6 +404,7 @@ int pfb_ctx_destroy(pfb_ctx* c) {
     cudaFree(c->bsums);
     cudaFree(c->bin_dev);
     cudaFree(c->bin_key);
+    cudaFree(c->bin_cont);
     for (int q = 0; q < 16; ++q) {
         if (c->peer_ipc[q] && c->peer_ptr[q]) cudaIpcCloseMemHandle(c->peer_ptr[q]);
     }
@@ -2184,21 +2190,34 @@ int pfb_binned_nll(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, const do
     }
     CK(cudaSetDevice(c->device));
     PFB_QUIESCE(c);
-    int rc = ensure_bin(c, (int64_t)sizeof(double) * nbins);
+    int rc = ensure_bin(c, 0);  // bin_key
     if (rc) return rc;
+    if (c->bin_cont_cap < nbins) {
+        cudaFree(c->bin_cont);
+        c->bin_cont = nullptr;
+        c->bin_cont_cap = 0;
+        c->bin_cont_host.clear();
+        CK(cudaMalloc(&c->bin_cont, sizeof(double) * nbins));
+        c->bin_cont_cap = nbins;
+    }
+    // upload the contents only when they differ from the last upload
+    if ((int64_t)c->bin_cont_host.size() != nbins ||
+        memcmp(c->bin_cont_host.data(), contents, sizeof(double) * nbins) != 0) {
+        c->bin_cont_host.assign(contents, contents + nbins);
+        CK(cudaMemcpyAsync(c->bin_cont, c->bin_cont_host.data(), sizeof(double) * nbins, cudaMemcpyHostToDevice,
+                           c->stream));
+    }
     auto A = std::make_unique<NllArgs>();
     const int frac = pack_args(p, st, 0, nbins, values, norms, A.get());
-    auto* dcont = static_cast<double*>(c->bin_dev);
-    CK(cudaMemcpyAsync(dcont, contents, sizeof(double) * nbins, cudaMemcpyHostToDevice, c->stream));
+    A->xkey = c->bin_key;  // the exporting CTA hands the key back in the result block and resets it
     CK(cudaMemsetAsync(c->bin_key, 0xff, sizeof(unsigned long long), c->stream));
     if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
-    CK(launch_binned_nll(*A, dcont, nbins, total, volume, c->bin_key, c->stream, c->sm_count));
+    CK(launch_binned_nll(*A, c->bin_cont, nbins, total, volume, c->bin_key, c->stream, c->sm_count));
     ++c->launches;
     if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
-    unsigned long long expkey = ~0ull;
-    CK(cudaMemcpyAsync(&expkey, c->bin_key, sizeof(expkey), cudaMemcpyDeviceToHost, c->stream));
     rc = read_result(c);
     if (rc) return rc;
+    const unsigned long long expkey = (unsigned long long)c->res_host[2];
     pfb_err e;
     int code = decode_error(c, p, *A, (unsigned long long)c->res_host[1], frac, 0, &e);
     if (!code && expkey != ~0ull) {

@@ -121,6 +121,7 @@ struct NllArgs {
     unsigned int* ticket;     // CTA completion counter (self-resetting)
     unsigned long long* work_counter;  // dynamic block scheduler (self-resetting)
     unsigned long long* errkey;  // min (rank<<40 | local index), ~0 when clean
+    unsigned long long* xkey;    // binned: first non-positive-expectation bin, exported into result_i[2]
     double* tail_scratch;     // 4096 doubles
     long long* acc_out;       // PFB_ACC_WORDS export target
     long long* result_i;      // [0] deferred-block count, [1] error key, [4] completion sequence

@@ -979,6 +979,7 @@ __device__ __forceinline__ void finish_launch(const NllArgs& A, long long* sacc,
     if (t == nt - 2 && !LIST)  // hand the deferred-block count to the fix-up launch
         A.result_i[0] = (long long)atomicExch(A.fix_counter, 0ull);
     if (t == nt - 3) A.result_i[1] = (long long)atomicExch(A.errkey, ~0ull);
+    if (A.xkey && t == nt - 4) A.result_i[2] = (long long)atomicExch(A.xkey, ~0ull);
     for (int i = t; i < PFB_ACC_WORDS; i += nt) {
         const long long v = (long long)atomicExch(A.acc + i, 0ull);
         if (A.mode == MODE_EXPORT)
