@@ -67,33 +67,26 @@ __global__ void grid_overlap_kernel(const double2* amps, int64_t n, const int2* 
     const int2 pr = pairs[blockIdx.y];
     const double2* Ai = amps + (int64_t)pr.x * n;
     const double2* Aj = amps + (int64_t)pr.y * n;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const double2 a = Ai[k], b = Aj[k];
-        double re, im;
-        if (pr.x == pr.y) {
-            re = Add(Mul(a.x, a.x), Mul(a.y, a.y));
-            im = 0.0;
-        } else {
-            const double bni = Sub(0.0, b.y);  // conj(b)
-            re = Sub(Mul(a.x, b.x), Mul(a.y, bni));
-            im = Add(Mul(a.x, bni), Mul(a.y, b.x));
+    // warp-uniform trip count: the accumulator adds are warp-aggregated
+    // (acc_add_warp; per-thread 64-bit shared atomics on the same few limbs
+    // serialised this kernel: 233 us for one 4-term overlap matrix, ncu)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < n; k0 += stride) {
+        const int64_t k = k0 + threadIdx.x;
+        const bool act = k < n;
+        double re = 0.0, im = 0.0;
+        if (act) {
+            const double2 a = Ai[k], b = Aj[k];
+            if (pr.x == pr.y) {
+                re = Add(Mul(a.x, a.x), Mul(a.y, a.y));
+            } else {
+                const double bni = Sub(0.0, b.y);  // conj(b)
+                re = Sub(Mul(a.x, b.x), Mul(a.y, bni));
+                im = Add(Mul(a.x, bni), Mul(a.y, b.x));
+            }
         }
-        const Digits dr = split_double(re), di = split_double(im);
-        if (dr.special)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&s[0][dr.special]), 1ull);
-        else
-            for (int q = 0; q < 3; ++q)
-                if (dr.d[q])
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&s[0][dr.limb + q]),
-                              (unsigned long long)dr.d[q]);
-        if (di.special)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&s[1][di.special]), 1ull);
-        else
-            for (int q = 0; q < 3; ++q)
-                if (di.d[q])
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&s[1][di.limb + q]),
-                              (unsigned long long)di.d[q]);
+        acc_add_warp(s[0], re, act);
+        if (pr.x != pr.y) acc_add_warp(s[1], im, act);  // block-uniform branch
     }
     __syncthreads();
     unsigned long long* dst = acc + (int64_t)blockIdx.y * 2 * PFB_ACC_WORDS;

@@ -777,52 +777,6 @@ struct Log2<1> {
     static constexpr int value = 0;
 };
 
-__device__ __forceinline__ void acc_add_shared(long long* sacc, double x) {
-    const Digits d = split_double(x);
-    if (d.special) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&sacc[d.special]), 1ull);
-        return;
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-        if (d.d[i])
-            atomicAdd(reinterpret_cast<unsigned long long*>(&sacc[d.limb + i]),
-                      (unsigned long long)d.d[i]);
-}
-
-// Warp-aggregated acc_add_shared for kernels that produce one term per thread
-// (quadrature, binned): the 32 lanes' digits are summed per limb with
-// shuffles (integer, exact) and one lane adds each limb sum, so a CTA issues
-// ~8 shared atomics per warp instead of 3 per thread (64-bit shared atomics
-// are CAS loops; 256 threads on the same few limbs serialise for tens of us).
-// Must be called by all 32 lanes; inactive lanes pass act = false.  Terms
-// spread over more than kWarpSpan limbs, and inf/NaN, take the per-lane path.
-__device__ __forceinline__ void acc_add_warp(long long* sacc, double x, bool act) {
-    constexpr unsigned kFull = 0xffffffffu;
-    constexpr int kWarpSpan = 6;
-    const Digits d = split_double(x);
-    if (act && d.special) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&sacc[d.special]), 1ull);
-        act = false;
-    }
-    if (act && !(d.d[0] | d.d[1] | d.d[2])) act = false;
-    const int lo = __reduce_min_sync(kFull, act ? d.limb : INT_MAX);
-    const int hi = __reduce_max_sync(kFull, act ? d.limb : INT_MIN);
-    if (lo == INT_MAX) return;
-    if (hi - lo > kWarpSpan) {
-        if (act) acc_add_shared(sacc, x);
-        return;
-    }
-    const bool lead = (threadIdx.x & 31) == 0;
-    for (int k = lo; k <= hi + 2; ++k) {
-        const int off = k - d.limb;
-        long long c = !act ? 0 : off == 0 ? d.d[0] : off == 1 ? d.d[1] : off == 2 ? d.d[2] : 0;
-#pragma unroll
-        for (int s = 16; s; s >>= 1) c += __shfl_xor_sync(kFull, c, s);
-        if (lead && c) atomicAdd(reinterpret_cast<unsigned long long*>(&sacc[k]), (unsigned long long)c);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Kernel modes.  The fast kernel never takes the literal path: a block that
 // contains an event its evaluator cannot certify is left out of the
