@@ -4,7 +4,8 @@ after full blocks) for the C1 SumPdf, C2 ProdPdf, C3 Dalitz, C2p gaussian x
 polynomial and a lone-polynomial model, through pipelines 1 / 2 / 3 (bulk,
 TMA-unit and per-warp staging kernels) and 0 (SIMT) -- each NLL within 1e-10
 of the reference's own nll on the same events (P/engine.py:214-243), and the
-staging shells of a product evaluator bitwise equal to each other."""
+shells of a product evaluator (staging kernels and the SIMT kernel at 1 / 2 /
+4 / 8 warps per block) bitwise equal to each other."""
 
 import os
 
@@ -78,5 +79,11 @@ def test_small_and_ragged_sizes_every_shell(pf, name):
             ctx.set_pipeline(1)
         for mode, v in got.items():
             assert abs(v - want) <= 1e-10 * abs(want), (name, n, mode, v, want)
-        if name in ("c1", "c3", "c2p", "poly"):  # product evaluators: the staging shells agree bitwise
+        if name in ("c1", "c3", "c2p", "poly"):  # product evaluators: every shell agrees bitwise
             assert got[1] == got[2] == got[3], (name, n, got)
+            try:
+                for w in (1, 2, 4, 8):  # the register-window SIMT kernel, P warps per block
+                    ctx.set_warps_per_block(w)
+                    assert pf.nll(pdf, ds) == got[1], (name, n, w)
+            finally:
+                ctx.set_warps_per_block(0)
