@@ -886,10 +886,11 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         }
         vo += L.nv;
     }
-    if (m == 0 && A->nleaf == 2 && A->leaf[0].kind == PFB_GAUSSIAN && A->leaf[1].kind == PFB_EXPONENTIAL) {
+    const bool g2_shape = A->nleaf == 2 && A->leaf[0].kind == PFB_GAUSSIAN && A->leaf[1].kind == PFB_EXPONENTIAL;
+    if (g2_shape) {
         const double mu = row[0], is = row[1], al = row[2];
-        A->g2_c2 = (-0.5 * is) * is;
-        A->g2_amu = al * mu;
+        A->g2_c2[m] = (-0.5 * is) * is;
+        A->g2_amu[m] = al * mu;
         // certified |w| = |x - mu| < min(256 / |alpha| - |mu|, 1000 sigma): |alpha x| < 256
         // (the reference's exp(alpha x) stays normal) and d >= -5e5 - 512 (the
         // exponential's scale index cannot wrap)
@@ -897,7 +898,7 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         if (!(lim > 0.0)) lim = 0.0;
         uint64_t bits;
         memcpy(&bits, &lim, 8);
-        A->g2_wlim = (int32_t)(bits >> 32);
+        A->g2_wlim[m] = (int32_t)(bits >> 32);
     }
     A->nterm = (int)p->terms.size();
     for (int t = 0; t < A->nterm; ++t) {
@@ -930,9 +931,8 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         row[kPtLeafWords + 2 * t] = T.logcoef;
         row[kPtLeafWords + 2 * t + 1] = T.thr;
     }
-    A->g2_qcert = 0;
-    if (m == 0 && A->nleaf == 2 && A->nterm == 2 && A->leaf[0].kind == PFB_GAUSSIAN &&
-        A->leaf[1].kind == PFB_EXPONENTIAL) {
+    if (m == 0) A->g2_qcert = 0;
+    if (g2_shape && A->nterm == 2) {
         // EvSum2GE: q = c1 + c0 e^d with d = u0 - u1 <= alpha^2 sigma^2 / 2 - alpha mu
         // for every x, and q >= c1: when that range sits inside the unit check's
         // [2^-250, 2^251) no event can leave it and the kernel drops the
@@ -940,7 +940,10 @@ static bool fill_sop_point(const pfb_plan* p, const double* values, const double
         const double mu = row[0], sg = 1.0 / row[1], al = row[2];
         const double c0 = A->term[0].coef, c1 = A->term[1].coef;
         const double qmax = c1 + c0 * exp(0.5 * (al * al) * (sg * sg) - al * mu);
-        A->g2_qcert = (c1 >= 0x1p-249 && c0 >= 0.0 && qmax * (1.0 + 1e-6) <= 0x1p249) ? 1 : 0;
+        const int cert = (c1 >= 0x1p-249 && c0 >= 0.0 && qmax * (1.0 + 1e-6) <= 0x1p249) ? 1 : 0;
+        A->g2_qcert = m == 0 ? cert : (A->g2_qcert & cert);
+        A->g2_c0[m] = c0;
+        A->g2_c1[m] = c1;
     }
     return true;
 }
@@ -1395,13 +1398,17 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
     if (rc) return rc;
     auto A = std::make_unique<NllArgs>();
     int frac0 = pack_args(p, st, begin, end, values, norms, A.get());
-    const bool in_kernel = A->evaluator == EV_SOP && sop_batched_in_kernel(*A, sop_ncols(p));
+    bool in_kernel = A->evaluator == EV_SOP && sop_batched_in_kernel(*A, sop_ncols(p));
     int first = PFB_OK;
     if (in_kernel) {
-        // one pass over the data for all points (TMA pipeline kernel)
         for (int m = 1; m < npts; ++m)
             fill_sop_point(p, values + (int64_t)m * nvalues, norms + (int64_t)m * nnorms, A.get(), m);
         A->npts = npts;
+        // every point must meet the batched evaluator's preconditions
+        in_kernel = sop_batched_in_kernel(*A, sop_ncols(p));
+    }
+    if (in_kernel) {
+        // one pass over the data for all points (TMA pipeline kernel)
         rc = launch_eval(p, st, begin, end, A.get(), false);
         if (rc) return rc;
         rc = read_result(c, npts);

@@ -145,11 +145,12 @@ struct NllArgs {
     int32_t nleaf, nterm;
     SopLeaf leaf[kMaxLeaves];  // voff indexes a ptv row
     SopTerm term[kMaxTerms];
-    // SumPdf(gaussian, exponential) constants of point 0 (EvSum2GE):
-    // c2 = -1/(2 sigma^2), alpha mu, and the high word of 256/|alpha|
-    double g2_c2, g2_amu;
-    int32_t g2_wlim;   // EvSum2GE: high word of the certified bound on |x - mu|
-    int32_t g2_qcert;  // EvSum2GE: q = c1 + c0 e^d provably in [2^-249, 2^249] for every x
+    // SumPdf(gaussian, exponential) constants per parameter point (EvSum2GE):
+    // c2 = -1/(2 sigma^2), alpha mu, the term coefficients c0 / c1, and the high
+    // word of the certified bound on |x - mu|
+    double g2_c2[kMaxPts], g2_amu[kMaxPts], g2_c0[kMaxPts], g2_c1[kMaxPts];
+    int32_t g2_wlim[kMaxPts];
+    int32_t g2_qcert;  // every point: q = c1 + c0 e^d provably in [2^-249, 2^249] for every x
     // batched objective: npts parameter points per pass over the data
     int32_t npts;
     int32_t fix_point;         // fix-up launch: the point whose deferred blocks it redoes

@@ -200,34 +200,36 @@ struct EvSum2GE {
     static constexpr bool LSCALE = true;  // unit sum of l times alpha
     static constexpr bool XMAX = true;    // unit check max |x - mu| < the host bound (g2_wlim)
     static constexpr bool QCERT = QC;     // q range certified on the host (g2_qcert): no per-event tracking
+    static constexpr bool POINTS = true;  // per-point constants: batched in the TMA unit kernel (m = point)
 
-    __device__ static __forceinline__ double cert_value(const NllArgs& A, double x) { return x - A.ptv[0][0]; }
-
-    __device__ static __forceinline__ double tab_entry(const NllArgs& A, int j) {
-        return A.term[0].coef * kExp2Tab256[j];
+    __device__ static __forceinline__ double cert_value(const NllArgs& A, double x, int m) {
+        return x - A.ptv[m][0];
     }
-    __device__ static __forceinline__ double lscale(const NllArgs& A) { return A.ptv[0][2]; }
+    __device__ static __forceinline__ double tab_entry(const NllArgs& A, int j, int m) {
+        return A.g2_c0[m] * kExp2Tab256[j];
+    }
+    __device__ static __forceinline__ double lscale(const NllArgs& A, int m) { return A.ptv[m][2]; }
 
     __device__ static __forceinline__ double one(const NllArgs& A, double x, const double* tab, bool& ok,
-                                                 double& l) {
+                                                 double& l, int m) {
 #ifdef PFB_EXP_CHEAP  // measurement-only build: structure cost without the exponential
         ok = true;
         l = x;
         return fma(x, 1e-3, 1.0);
 #endif
-        // per-launch constants from the host (NllArgs::g2_*)
-        const double w = x - A.ptv[0][0];
-        const double d = fma(w, fma(A.g2_c2, w, -A.ptv[0][2]), -A.g2_amu);
+        // per-call constants of point m from the host (NllArgs::g2_*)
+        const double w = x - A.ptv[m][0];
+        const double d = fma(w, fma(A.g2_c2[m], w, -A.ptv[m][2]), -A.g2_amu[m]);
         ok = true;  // |x| certified per unit (XMAX); d < -500: cexp_tab_add
         l = x;
-        return cexp_tab_add(d, tab, A.term[1].coef);
+        return cexp_tab_add(d, tab, A.g2_c1[m]);
     }
 
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[1], bool& okx,
-                                                    bool& oky, const double* tab, double2& l) {
+                                                    bool& oky, const double* tab, double2& l, int m = 0) {
         double2 q;
-        q.x = one(A, x[0].x, tab, okx, l.x);
-        q.y = one(A, x[0].y, tab, oky, l.y);
+        q.x = one(A, x[0].x, tab, okx, l.x, m);
+        q.y = one(A, x[0].y, tab, oky, l.y, m);
         return q;
     }
 };
@@ -390,6 +392,14 @@ struct HasXMax<Ev, decltype((void)Ev::XMAX)> {
     static constexpr bool value = Ev::XMAX;
 };
 template <class Ev, class = void>
+struct HasPoints {
+    static constexpr bool value = false;
+};
+template <class Ev>
+struct HasPoints<Ev, decltype((void)Ev::POINTS)> {
+    static constexpr bool value = Ev::POINTS;
+};
+template <class Ev, class = void>
 struct HasQCert {
     static constexpr bool value = false;
 };
@@ -411,7 +421,7 @@ struct RatioPow<Ev, decltype((void)Ev::RATIO_POW)> {
 // mask absent tail events (TAIL), certify, multiply into the unit.
 template <class Ev, bool TAIL>
 __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev::NC], int e, int n, Unit& u,
-                                         bool& bad, const double* tab, bool renorm_now = true) {
+                                         bool& bad, const double* tab, bool renorm_now = true, int m = 0) {
     constexpr bool RATIO = IsRatio<Ev>::value;
     bool okx, oky;
     double2 l = make_double2(0.0, 0.0);
@@ -419,6 +429,8 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
     double2 q;
     if constexpr (RATIO)
         q = Ev::prob2r(A, x, okx, oky, r);
+    else if constexpr (HasPoints<Ev>::value)
+        q = Ev::prob2(A, x, okx, oky, tab, l, m);
     else
         q = Ev::prob2(A, x, okx, oky, tab, l);
     if (TAIL) {
@@ -436,8 +448,8 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
         }
     }
     if constexpr (HasXMax<Ev>::value) {
-        const int a = (TAIL && e >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].x)) & 0x7fffffff);
-        const int b = (TAIL && e + 1 >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].y)) & 0x7fffffff);
+        const int a = (TAIL && e >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].x, m)) & 0x7fffffff);
+        const int b = (TAIL && e + 1 >= n) ? 0 : (__double2hiint(Ev::cert_value(A, x[0].y, m)) & 0x7fffffff);
         u.xhi = max(u.xhi, max(a, b));
     }
 #if PFB_UNIT_MINMAX
@@ -495,9 +507,9 @@ __device__ __forceinline__ bool unit_in_range(const Unit& u, bool ratio) {
 
 // every unit-level certificate of an evaluator
 template <class Ev>
-__device__ __forceinline__ bool unit_ok(const NllArgs& A, const Unit& u) {
+__device__ __forceinline__ bool unit_ok(const NllArgs& A, const Unit& u, int m = 0) {
     bool ok = unit_in_range(u, IsRatio<Ev>::value);
-    if constexpr (HasXMax<Ev>::value) ok = ok && u.xhi < A.g2_wlim;
+    if constexpr (HasXMax<Ev>::value) ok = ok && u.xhi < A.g2_wlim[m];
     return ok;
 }
 
@@ -519,14 +531,16 @@ struct HasLScale<Ev, decltype((void)Ev::LSCALE)> {
     static constexpr bool value = Ev::LSCALE;
 };
 template <class Ev>
-__device__ __forceinline__ void init_tab(const NllArgs& A, double* tab, int tid) {
+__device__ __forceinline__ void init_tab(const NllArgs& A, double* tab, int tid, int npts = 1, int nthreads = 0) {
+    // nthreads: the threads taking part (0: the whole CTA)
     if constexpr (HasTab<Ev>::value) {
-        for (int j = tid; j < kTabN; j += blockDim.x) tab[j] = Ev::tab_entry(A, j);
+        const int step = nthreads > 0 ? nthreads : (int)blockDim.x;
+        for (int j = tid; j < npts * kTabN; j += step) tab[j] = Ev::tab_entry(A, j % kTabN, j / kTabN);
     }
 }
 
 template <class Ev>
-__device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u) {
+__device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u, int m = 0) {
     if constexpr (IsRatio<Ev>::value) {
         constexpr double pw = (double)RatioPow<Ev>::value;
         const double fe = fma(-pw, int_to_double(u.exd), int_to_double(u.ex));
@@ -537,7 +551,7 @@ __device__ __forceinline__ double unit_value(const NllArgs& A, const Unit& u) {
         // every kernel shell (bulk, task, TMA, SIMT, persistent) gives the same bits
         double s;
         if constexpr (HasLScale<Ev>::value)
-            s = fma(Ev::lscale(A), u.ls, log_unit(u.m));
+            s = fma(Ev::lscale(A, m), u.ls, log_unit(u.m));
         else
             s = __dadd_rn(log_unit(u.m), u.ls);
         return -fma(fe, kLn2Hi, fma(fe, kLn2Lo, s));
@@ -609,7 +623,9 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
     __shared__ unsigned int s_cnt[kSumTeams][kSumRing];
     __shared__ int s_done[kSumTeams][kSumRing];
     __shared__ long long sacc[kMaxPts][PFB_ACC_WORDS];
-    __shared__ double s_tab[kTabN];
+    // the evaluator's shared tables, one per parameter point (batched product
+    // mode): dynamic shared memory after the stages (static is capped at 48 KB)
+    double* const s_tab = stage + (int64_t)S * NC * kBlock;
     __shared__ unsigned int s_last;
 
     const int tid = threadIdx.x;
@@ -675,7 +691,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
             }
         }
     } else {
-        init_tab<Ev>(A, s_tab, tid);
+        init_tab<Ev>(A, s_tab, tid, A.npts, 32 * kSumWarps * kSumTeams);  // the consumer threads only
         for (int i = tid; i < kMaxPts * PFB_ACC_WORDS; i += 32 * kSumWarps * kSumTeams) (&sacc[0][0])[i] = 0;
         if (tid < kSumTeams * kSumRing) {
             (&s_cnt[0][0])[tid] = 0u;
@@ -763,7 +779,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
 #pragma unroll
                         for (int c = 0; c < NC; ++c) x[c] = *reinterpret_cast<const double2*>(sx + c * kBlock + e);
                         if constexpr (PROD) {
-                            prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab, (r & 1) != 0);
+                            prod_row<Ev, false>(A, x, 0, kBlock, un, bad, s_tab + m * kTabN, (r & 1) != 0, m);
                         } else {
                             const double2 t = Ev::eval2(A, x, 0, sacc[0], 2, bad, m);
                             acc = (acc + t.x) + t.y;
@@ -787,7 +803,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                             }
                         }
                         if constexpr (PROD) {
-                            prod_row<Ev, true>(A, x, e, n, un, bad, s_tab);
+                            prod_row<Ev, true>(A, x, e, n, un, bad, s_tab + m * kTabN, true, m);
                         } else {
                             const double2 t = Ev::eval2(A, x, 0, sacc[0], nv, bad, m);
                             acc = acc + t.x;
@@ -796,8 +812,8 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                     }
                 }
                 if constexpr (PROD) {
-                    bad |= !unit_ok<Ev>(A, un);
-                    acc = unit_value<Ev>(A, un);
+                    bad |= !unit_ok<Ev>(A, un, m);
+                    acc = unit_value<Ev>(A, un, m);
                 }
                 if (m == A.npts - 1) {  // the stage is no longer read by this warp
                     __syncwarp();
@@ -823,10 +839,12 @@ static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm
     // the team / stage phase bookkeeping needs S >= 3 stages (measured: a
     // single stage with two teams never completes)
     static_assert(NC <= 2, "TMA unit kernel: one or two columns");
-    // one-column stages: six of 32 KB, five when the evaluator's 2 KB shared
-    // table would push static + dynamic shared memory past the 227 KB limit
-    constexpr int S = NC == 1 ? (HasTab<Ev>::value ? 5 : 6) : 3;
-    const size_t smem = (size_t)S * NC * kBlock * sizeof(double);
+    // one-column stages: six of 32 KB, four when the evaluator keeps shared
+    // tables (2 KB per parameter point) -- static + dynamic shared memory
+    // stays within the 227 KB limit
+    constexpr int S = NC == 1 ? (HasTab<Ev>::value ? 4 : 6) : 3;
+    const size_t smem = (size_t)S * NC * kBlock * sizeof(double) +
+                        (HasTab<Ev>::value ? (size_t)kMaxPts * kTabN * sizeof(double) : 0);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(nll_tma_unit_kernel<Ev, S, PROD>,

@@ -20,24 +20,30 @@ static int kinds_of(const NllArgs& A) {
     return k;
 }
 
-// True when launch_sop runs the TMA pipeline kernel for this plan -- the
-// kernel that evaluates A.npts parameter points per pass over the data.
-bool sop_batched_in_kernel(const NllArgs& A, int nc) {
-    if (!A.tma) return false;
-    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
-    if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
-    if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
-    return false;
-}
-
 // EvSum2GE's fixed layout (leaf 0 gaussian, leaf 1 exponential, term t =
 // leaf t alone) and |ln c_t| < 200 (see EvSum2GE).
 static bool sum2ge_ok(const NllArgs& A) {
     if (A.leaf[0].voff != 0 || A.leaf[1].voff != 2) return false;
     if (A.term[0].emask != 1u || A.term[1].emask != 2u || A.term[0].vmask || A.term[1].vmask) return false;
-    for (int t = 0; t < 2; ++t)
-        if (!(fabs(A.term[t].logcoef) < 200.0)) return false;
+    const int npts = A.npts > 0 ? A.npts : 1;
+    for (int m = 0; m < npts; ++m)  // every parameter point's log coefficients (the ptv rows)
+        for (int t = 0; t < 2; ++t)
+            if (!(fabs(A.ptv[m][kPtLeafWords + 2 * t]) < 200.0)) return false;
     return true;
+}
+
+// True when launch_sop runs the TMA pipeline kernel for this plan -- the
+// kernel that evaluates A.npts parameter points per pass over the data.
+bool sop_batched_in_kernel(const NllArgs& A, int nc) {
+    if (!A.tma) return false;
+    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
+    // C1 / C5 SumPdf(gaussian, exponential): product mode with per-point
+    // constants and tables in the TMA unit kernel (EvSum2GE::POINTS); the
+    // caller re-checks sum2ge_ok once every point is filled
+    if (nc == 1 && nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.warps == 0) return sum2ge_ok(A);
+    if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
+    if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
+    return false;
 }
 
 // EvGaussPoly's fixed layout: leaf 0 gaussian, leaf 1 polynomial, one term
@@ -107,6 +113,9 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // 2: bulk prefetch; 3: the TMA unit kernel -- the same canonical blocks
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A)) {
             const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
+            if (A.npts > 1)  // batched points: one pass, the stage reused by every point
+                return A.g2_qcert ? launch_tma_unit<EvSum2GE<true>, true>(A, stream, sm_count)
+                                  : launch_tma_unit<EvSum2GE<>, true>(A, stream, sm_count);
             if (A.tma == 1 && A.warps == 0 && nitems >= PFB_TASK_ITEMS_PER_SM * (int64_t)sm_count)
                 return A.g2_qcert ? launch_task<EvSum2GE<true>>(A, stream, sm_count)
                                   : launch_task<EvSum2GE<>>(A, stream, sm_count);
