@@ -22,6 +22,7 @@ cudaError_t launch_fix(const NllArgs& A, cudaStream_t stream, int sm_count);
 int persist_kind(const NllArgs& A, int nc);
 cudaError_t launch_persist_kind(int kind, const PersistCtl& P, cudaStream_t stream, int sm_count);
 bool sop_batched_in_kernel(const NllArgs& A, int nc);
+bool dal_batched_in_kernel(const NllArgs& A);
 cudaError_t launch_export(unsigned long long* acc, long long* out, long long* result_i,
                           unsigned long long* fix_counter, unsigned long long* errkey,
                           cudaStream_t stream);
@@ -1406,6 +1407,33 @@ int pfb_nll_batch(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int64_t b
         A->npts = npts;
         // every point must meet the batched evaluator's preconditions
         in_kernel = sop_batched_in_kernel(*A, sop_ncols(p));
+    }
+    if (!in_kernel && npts > 1 && A->evaluator == EV_DALITZ && dal_batched_in_kernel(*A)) {
+        // the D0 ratio form: every point's four scaled coefficients per term go
+        // into its ptv row -- when the shapes (masses, widths) are point 0's
+        static_assert(kPtWords >= 4 * 4, "ptv row holds 4 Dalitz terms x 4 coefficients");
+        bool same = true;
+        auto Am = std::make_unique<NllArgs>();
+        for (int m = 0; m < npts && same; ++m) {
+            const NllArgs* S = A.get();
+            if (m > 0) {
+                pack_args(p, st, begin, end, values + (int64_t)m * nvalues, norms + (int64_t)m * nnorms, Am.get());
+                S = Am.get();
+            }
+            for (int k = 0; k < 4; ++k) {
+                const DalTerm& T = S->dal.t[k];
+                const DalTerm& T0 = A->dal.t[k];
+                if (!(T.m2 == T0.m2 && T.mg == T0.mg && T.mg2 == T0.mg2)) same = false;
+                A->ptv[m][4 * k] = T.scre;
+                A->ptv[m][4 * k + 1] = T.scim;
+                A->ptv[m][4 * k + 2] = T.salpha;
+                A->ptv[m][4 * k + 3] = T.sbeta;
+            }
+        }
+        if (same) {
+            A->npts = npts;
+            in_kernel = true;
+        }
     }
     if (in_kernel) {
         // one pass over the data for all points (TMA pipeline kernel)

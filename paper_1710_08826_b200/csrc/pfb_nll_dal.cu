@@ -20,9 +20,17 @@ static int signature_of(const DalDesc& D) {
     return sig | (D.need12 ? 1 << 12 : 0) | (D.need13 ? 1 << 13 : 0) | (D.need23 ? 1 << 14 : 0);
 }
 
+// Batched parameter points in one pass (pfb_nll_batch): the D0 ratio form,
+// pipeline 1, the coefficients of every point in the ptv rows.
+bool dal_batched_in_kernel(const NllArgs& A) {
+    return A.tma == 1 && A.warps == 0 && A.evaluator == EV_DALITZ && A.dal.K == 4 && signature_of(A.dal) == kSigD0;
+}
+
 cudaError_t launch_dalitz(const NllArgs& A, cudaStream_t stream, int sm_count) {
     if (A.evaluator == EV_DALITZ_CACHED) return launch_p<EvDalitzCached>(A, stream, sm_count);
     const bool d0 = A.dal.K == 4 && signature_of(A.dal) == kSigD0;
+    if (A.npts > 1 && dal_batched_in_kernel(A))
+        return launch_tma_unit<EvDalitzR<4, kSigD0, true>, true>(A, stream, sm_count);
     if (A.tma) {
         // product kernels.  D0 -> pi+ pi- pi0 (C3/C4): the reciprocal-free
         // ratio form with the term structure fixed at compile time.  Other

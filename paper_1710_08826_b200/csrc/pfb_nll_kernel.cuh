@@ -497,8 +497,11 @@ struct EvDalitz {
 // square is taken on the unit's logarithm), and 1/norm rides in the
 // coefficients (sqrt(1/norm) each).  ~47 FP64 operations per event against
 // ~57 plus a reciprocal for EvDalitz.
-template <int K_, int SIG = -1>
+template <int K_, int SIG = -1, bool PTS = false>
 struct EvDalitzR {
+    // PTS: batched parameter points -- the four scaled coefficients of term k
+    // for point m in A.ptv[m][4k .. 4k+3] (the shapes are shared)
+    static constexpr bool POINTS = PTS;
     static constexpr int NC = 2;
     static constexpr int U = 2;
     static constexpr int MINB = PFB_DALR_MINB;
@@ -528,7 +531,7 @@ struct EvDalitzR {
     }
 
     __device__ static __forceinline__ void one(const NllArgs& A, double s12, double s13, double& num,
-                                               double& den) {
+                                               double& den, int m = 0) {
         const DalDesc& D = A.dal;
         const double s23 = (D.mss - s12) - s13;
         const double dd12 = s13 - s23, dd13 = s12 - s23, dd23 = s12 - s13;  // Zemach differences
@@ -588,18 +591,20 @@ struct EvDalitzR {
                 }
             }
             const double E = ex[k] * F;
-            tr = fma(E, fma(-T.scre, sv[k], T.salpha), tr);  // coefficients carry sqrt(1/norm)
-            ti = fma(E, fma(-T.scim, sv[k], T.sbeta), ti);
+            const double scre = PTS ? A.ptv[m][4 * k] : T.scre, scim = PTS ? A.ptv[m][4 * k + 1] : T.scim;
+            const double salpha = PTS ? A.ptv[m][4 * k + 2] : T.salpha, sbeta = PTS ? A.ptv[m][4 * k + 3] : T.sbeta;
+            tr = fma(E, fma(-scre, sv[k], salpha), tr);  // coefficients carry sqrt(1/norm)
+            ti = fma(E, fma(-scim, sv[k], sbeta), ti);
         }
         num = fma(tr, tr, ti * ti);
         den = any ? (pre[K - 1] * d[K - 1]) * sig : pre[K - 1] * d[K - 1];  // D'; the kernel squares at the unit end
     }
 
     __device__ static __forceinline__ double2 prob2r(const NllArgs& A, const double2 (&x)[2], bool& okx,
-                                                     bool& oky, double2& den) {
+                                                     bool& oky, double2& den, int m = 0) {
         double2 q;
-        one(A, x[0].x, x[1].x, q.x, den.x);
-        one(A, x[0].y, x[1].y, q.y, den.y);
+        one(A, x[0].x, x[1].x, q.x, den.x, m);
+        one(A, x[0].y, x[1].y, q.y, den.y, m);
         okx = oky = true;  // certified by the kernel's range checks on q and den
         return q;
     }

@@ -427,7 +427,9 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
     double2 l = make_double2(0.0, 0.0);
     double2 r = make_double2(1.0, 1.0);
     double2 q;
-    if constexpr (RATIO)
+    if constexpr (RATIO && HasPoints<Ev>::value)
+        q = Ev::prob2r(A, x, okx, oky, r, m);
+    else if constexpr (RATIO)
         q = Ev::prob2r(A, x, okx, oky, r);
     else if constexpr (HasPoints<Ev>::value)
         q = Ev::prob2(A, x, okx, oky, tab, l, m);

@@ -170,3 +170,38 @@ def test_batched_fit_equals_unbatched_fit(pf, golden_dir):
     for fm in (fm1, fm2):
         assert fm0.store.kernel_evals == fm.store.kernel_evals
         assert fm0.store.norm_computations == fm.store.norm_computations
+
+
+def test_dalitz_points_in_one_pass_bitwise(pf, golden_dir):
+    """The D0 Dalitz ratio form evaluates a batch of coefficient points in one
+    pass (each point's scaled coefficients in its ptv row): every value
+    bitwise its own single-point NLL; a batch whose points move a mass falls
+    back to one launch per point with the same result."""
+    import os
+
+    g = np.load(os.path.join(golden_dir, "c3_dalitz.npz"))
+    (s12, s13), pdf, terms = models.c3(grid=(128, 128))
+    ds = models.dataset([s12, s13], [g["s12"], g["s13"]])
+    free = [v for t in terms for v in (t.magnitude, t.phase) if not v.fixed]
+    base = np.array([v.value for v in free])
+    pts = [base * (1.0 + 0.003 * k) for k in range(9)]
+    want = [outcome(single(pf, pdf, ds, free, p)) for p in pts]
+    snaps, norms = points_eval(pf, pdf, ds, free, pts)
+    cols = {"s12": ds.column("s12"), "s13": ds.column("s13")}
+    ctx = pf.device_context(0)
+    b = ctx.launch_count()
+    got = pf.DeviceBackend().evaluate_batch(pdf, cols, snaps, norms, 0, ds.n_events)
+    assert ctx.launch_count() - b == 1  # one pass for all nine points
+    assert [outcome(r) for r in got] == want
+    # a floating mass: shapes differ between points -> per-point launches, same bits
+    mass = terms[1].mass
+    mass.fixed = False
+    try:
+        params = free + [mass]
+        pts2 = [np.append(p, mass.value * (1.0 + 1e-4 * k)) for k, p in enumerate(pts[:4])]
+        want2 = [outcome(single(pf, pdf, ds, params, p)) for p in pts2]
+        snaps2, norms2 = points_eval(pf, pdf, ds, params, pts2)
+        got2 = pf.DeviceBackend().evaluate_batch(pdf, cols, snaps2, norms2, 0, ds.n_events)
+        assert [outcome(r) for r in got2] == want2
+    finally:
+        mass.fixed = True
