@@ -254,9 +254,11 @@ struct EvGaussPoly {
     static constexpr int NC = 2;
     static constexpr int U = 2;
     static constexpr int MINB = 3;
+    static constexpr bool POINTS = true;  // every value from the point's ptv row: batchable
 
-    __device__ static __forceinline__ double one(const NllArgs& A, double xg, double y, bool& ok, double& l) {
-        const double* v = A.ptv[0];
+    __device__ static __forceinline__ double one(const NllArgs& A, double xg, double y, bool& ok, double& l,
+                                                 int m = 0) {
+        const double* v = A.ptv[m];
         const double z = __dmul_rn(__dsub_rn(xg, v[0]), v[1]);
         const double u = __dmul_rn(__dmul_rn(-0.5, z), z);
         const int nv = NV > 0 ? NV : A.leaf[1].nv;
@@ -278,11 +280,11 @@ struct EvGaussPoly {
     }
 
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[2], bool& okx,
-                                                    bool& oky, const double*, double2& l) {
+                                                    bool& oky, const double*, double2& l, int m = 0) {
         const bool g1 = A.leaf[0].col != 0;
         double2 q;
-        q.x = one(A, g1 ? x[1].x : x[0].x, g1 ? x[0].x : x[1].x, okx, l.x);
-        q.y = one(A, g1 ? x[1].y : x[0].y, g1 ? x[0].y : x[1].y, oky, l.y);
+        q.x = one(A, g1 ? x[1].x : x[0].x, g1 ? x[0].x : x[1].x, okx, l.x, m);
+        q.y = one(A, g1 ? x[1].y : x[0].y, g1 ? x[0].y : x[1].y, oky, l.y, m);
         return q;
     }
 };

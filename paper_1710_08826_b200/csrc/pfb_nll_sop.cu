@@ -32,6 +32,17 @@ static bool sum2ge_ok(const NllArgs& A) {
     return true;
 }
 
+// EvGaussPoly's fixed layout: leaf 0 gaussian, leaf 1 polynomial, one term
+// multiplying both (gaussian in the log sum, polynomial as a value).
+static bool gp_ok(const NllArgs& A) {
+    if (A.leaf[0].voff != 0 || A.leaf[1].voff != 2 || A.leaf[1].nv < 1) return false;
+    if (A.term[0].emask != 1u || A.term[0].vmask != 2u) return false;
+    const int npts = A.npts > 0 ? A.npts : 1;
+    for (int m = 0; m < npts; ++m)  // every parameter point's log coefficient (the ptv rows)
+        if (!(fabs(A.ptv[m][kPtLeafWords]) < 600.0)) return false;
+    return true;
+}
+
 // True when launch_sop runs the TMA pipeline kernel for this plan -- the
 // kernel that evaluates A.npts parameter points per pass over the data.
 bool sop_batched_in_kernel(const NllArgs& A, int nc) {
@@ -42,16 +53,9 @@ bool sop_batched_in_kernel(const NllArgs& A, int nc) {
     // caller re-checks sum2ge_ok once every point is filled
     if (nc == 1 && nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.warps == 0) return sum2ge_ok(A);
     if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
+    if (nc == 2 && nl == 2 && nt == 1 && kinds == (kG | kP << 2) && A.warps == 0) return gp_ok(A);  // EvGaussPoly
     if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
     return false;
-}
-
-// EvGaussPoly's fixed layout: leaf 0 gaussian, leaf 1 polynomial, one term
-// multiplying both (gaussian in the log sum, polynomial as a value).
-static bool gp_ok(const NllArgs& A) {
-    if (A.leaf[0].voff != 0 || A.leaf[1].voff != 2 || A.leaf[1].nv < 1) return false;
-    if (A.term[0].emask != 1u || A.term[0].vmask != 2u) return false;
-    return fabs(A.term[0].logcoef) < 600.0;
 }
 
 // EvProd1's layout: one term, exp-type leaves in its emask, polynomials in its

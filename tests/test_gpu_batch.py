@@ -205,3 +205,27 @@ def test_dalitz_points_in_one_pass_bitwise(pf, golden_dir):
         assert [outcome(r) for r in got2] == want2
     finally:
         mass.fixed = True
+
+
+def test_gauss_poly_points_in_one_pass_bitwise(pf):
+    """ProdPdf(gaussian(x), polynomial(y)) (C2p's product evaluator) batches
+    points in one pass too; every value bitwise its single-point NLL."""
+    rng = np.random.default_rng(6)
+    n = 30 * 4096 + 321
+    x = P.Variable.observable("x", 0.0, 10.0)
+    y = P.Variable.observable("y", 0.0, 10.0)
+    mu, sg = P.Variable("mu", 5.0, 0.0, 10.0), P.Variable("sg", 1.0, 0.1, 5.0)
+    cs = [P.Variable(f"c{k}", v, -10.0, 10.0) for k, v in enumerate((1.0, 0.3, 0.05))]
+    pdf = P.prod_pdf([P.gaussian(x, mu, sg), P.polynomial(y, cs)])
+    ds = models.dataset([x, y], [np.clip(rng.normal(5, 1, n), 0, 10), rng.uniform(0, 10, n)])
+    params = [mu, sg] + cs
+    base = np.array([5.0, 1.0, 1.0, 0.3, 0.05])
+    pts = [base + 0.01 * np.eye(5)[k % 5] * (1 if k < 5 else -1) for k in range(10)]
+    want = [outcome(single(pf, pdf, ds, params, p)) for p in pts]
+    snaps, norms = points_eval(pf, pdf, ds, params, pts)
+    ctx = pf.device_context(0)
+    b = ctx.launch_count()
+    got = pf.DeviceBackend().evaluate_batch(pdf, {"x": ds.column("x"), "y": ds.column("y")}, snaps, norms, 0,
+                                            ds.n_events)
+    assert ctx.launch_count() - b == 1
+    assert [outcome(r) for r in got] == want
