@@ -306,6 +306,7 @@ struct EvProd1 {
     static constexpr int NC = NC_;
     static constexpr int U = 2;
     static constexpr int MINB = 3;
+    static constexpr bool POINTS = true;  // every value from the point's ptv row: batchable
 
     __device__ static __forceinline__ double pick(const double2 (&x)[NC_], int col, bool hi) {
         double r = hi ? x[0].y : x[0].x;
@@ -316,8 +317,8 @@ struct EvProd1 {
     }
 
     __device__ static __forceinline__ double one(const NllArgs& A, const double2 (&x)[NC_], bool hi, bool& ok,
-                                                 double& l) {
-        const double* v = A.ptv[0];
+                                                 double& l, int m = 0) {
+        const double* v = A.ptv[m];
         double q = 1.0, budget = 0.0;
         double ls = v[kPtLeafWords];
         bool good = true;
@@ -353,10 +354,10 @@ struct EvProd1 {
     }
 
     __device__ static __forceinline__ double2 prob2(const NllArgs& A, const double2 (&x)[NC_], bool& okx,
-                                                    bool& oky, const double*, double2& l) {
+                                                    bool& oky, const double*, double2& l, int m = 0) {
         double2 q;
-        q.x = one(A, x, false, okx, l.x);
-        q.y = one(A, x, true, oky, l.y);
+        q.x = one(A, x, false, okx, l.x, m);
+        q.y = one(A, x, true, oky, l.y, m);
         return q;
     }
 };

@@ -43,26 +43,14 @@ static bool gp_ok(const NllArgs& A) {
     return true;
 }
 
-// True when launch_sop runs the TMA pipeline kernel for this plan -- the
-// kernel that evaluates A.npts parameter points per pass over the data.
-bool sop_batched_in_kernel(const NllArgs& A, int nc) {
-    if (!A.tma) return false;
-    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
-    // C1 / C5 SumPdf(gaussian, exponential): product mode with per-point
-    // constants and tables in the TMA unit kernel (EvSum2GE::POINTS); the
-    // caller re-checks sum2ge_ok once every point is filled
-    if (nc == 1 && nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.warps == 0) return sum2ge_ok(A);
-    if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
-    if (nc == 2 && nl == 2 && nt == 1 && kinds == (kG | kP << 2) && A.warps == 0) return gp_ok(A);  // EvGaussPoly
-    if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
-    return false;
-}
-
 // EvProd1's layout: one term, exp-type leaves in its emask, polynomials in its
 // vmask, at least one polynomial (without one the log-domain unit sums need
 // no logarithm at all).
 static bool prod1_ok(const NllArgs& A) {
-    if (A.nterm != 1 || !(fabs(A.term[0].logcoef) < 600.0)) return false;
+    if (A.nterm != 1) return false;
+    const int npts = A.npts > 0 ? A.npts : 1;
+    for (int m = 0; m < npts; ++m)  // every parameter point's log coefficient (the ptv rows)
+        if (!(fabs(A.ptv[m][kPtLeafWords]) < 600.0)) return false;
     bool value = false;
     for (int l = 0; l < A.nleaf; ++l) {
         const SopLeaf& L = A.leaf[l];
@@ -75,6 +63,24 @@ static bool prod1_ok(const NllArgs& A) {
         }
     }
     return value;
+}
+
+// True when launch_sop runs the TMA pipeline kernel for this plan -- the
+// kernel that evaluates A.npts parameter points per pass over the data.
+bool sop_batched_in_kernel(const NllArgs& A, int nc) {
+    if (!A.tma) return false;
+    const int nl = A.nleaf, nt = A.nterm, kinds = kinds_of(A);
+    // C1 / C5 SumPdf(gaussian, exponential): product mode with per-point
+    // constants and tables in the TMA unit kernel (EvSum2GE::POINTS); the
+    // caller re-checks sum2ge_ok once every point is filled
+    if (nc == 1 && nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.warps == 0) return sum2ge_ok(A);
+    if (nc == 2 && nl == 2 && nt == 1 && kinds == (kG | kP << 2) && A.warps == 0) return gp_ok(A);  // EvGaussPoly
+    // EvProd1 on one or two columns (a lone polynomial; exp-type x polynomial)
+    if (nc == 1 && nl == 1 && kinds == kP && A.warps == 0) return prod1_ok(A);
+    if (nc == 2 && nl == 2 && A.warps == 0 && prod1_ok(A)) return true;
+    if (nc == 1) return nl == 1 && nt == 1 && kinds == kG;
+    if (nc == 2) return nl == 2 && nt == 1 && kinds == (kG | kE << 2);
+    return false;
 }
 
 // pipeline 1: the unit-sum TMA kernel; 2: the reference-tree TMA kernel;
@@ -132,7 +138,8 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
             return launch_stream<EvSop<1, 1, 1, true, kG>>(A, stream, sm_count);
         // a lone polynomial: product mode (one log per 16 events)
         if (nl == 1 && kinds == kP && A.tma && prod1_ok(A))
-            return launch_prod<EvProd1<1, 1, kP>>(A, stream, sm_count);
+            return A.npts > 1 ? launch_tma_unit<EvProd1<1, 1, kP>, true>(A, stream, sm_count)
+                              : launch_prod<EvProd1<1, 1, kP>>(A, stream, sm_count);
         if (nl == 1 && nt == 1) return launch_p<EvSop<1, 1, 1, true>>(A, stream, sm_count);
         if (nl == 2 && nt == 2) return launch_p<EvSop<1, 2, 2, true>>(A, stream, sm_count);
         return launch_p<EvSop<1>>(A, stream, sm_count);

@@ -229,3 +229,31 @@ def test_gauss_poly_points_in_one_pass_bitwise(pf):
                                             ds.n_events)
     assert ctx.launch_count() - b == 1
     assert [outcome(r) for r in got] == want
+
+
+@pytest.mark.parametrize("shape", ["poly", "expo_poly"])
+def test_single_term_product_points_in_one_pass_bitwise(pf, shape):
+    """EvProd1 (a lone polynomial; exponential x polynomial) batches points in
+    one pass; every value bitwise its single-point NLL."""
+    rng = np.random.default_rng(8)
+    n = 20 * 4096 + 77
+    x = P.Variable.observable("x", 0.0, 10.0)
+    y = P.Variable.observable("y", 0.0, 10.0)
+    cs = [P.Variable(f"q{k}", v, -10.0, 10.0) for k, v in enumerate((1.0, 0.3, 0.05))]
+    if shape == "poly":
+        pdf, obs, params, base = P.polynomial(x, cs), [x], cs, np.array([1.0, 0.3, 0.05])
+    else:
+        a = P.Variable("a", -0.2, -5.0, 5.0)
+        pdf, obs, params = P.prod_pdf([P.exponential(x, a), P.polynomial(y, cs)]), [x, y], [a] + cs
+        base = np.array([-0.2, 1.0, 0.3, 0.05])
+    cols = [rng.uniform(0, 10, n) for _ in obs]
+    ds = models.dataset(obs, cols)
+    pts = [base * (1.0 + 0.002 * k) for k in range(7)]
+    want = [outcome(single(pf, pdf, ds, params, p)) for p in pts]
+    snaps, norms = points_eval(pf, pdf, ds, params, pts)
+    ctx = pf.device_context(0)
+    b = ctx.launch_count()
+    got = pf.DeviceBackend().evaluate_batch(pdf, {o.name: ds.column(o.name) for o in obs}, snaps, norms, 0,
+                                            ds.n_events)
+    assert ctx.launch_count() - b == 1
+    assert [outcome(r) for r in got] == want
