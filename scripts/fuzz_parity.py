@@ -1,0 +1,130 @@
+"""Randomised parity sweep: random PDF trees (gaussian / exponential /
+polynomial leaves; sums over shared observables, products over disjoint
+ones; 1-3 observables), random parameters, random event counts (1 .. 300k,
+ragged), every pipeline mode and a random warps-per-block override -- each
+device NLL against the reference's own nll on the same events (<= 1e-10, or
+the same exception class and index).
+
+    python scripts/fuzz_parity.py [--cases 300] [--seed 1] [--out profiles/r2_fuzz.json]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+OBS = {"x": (0.0, 10.0), "y": (-2.0, 3.0), "z": (0.0, 1.0)}
+
+
+def leaf(P, rng, o, name, hostile=False):
+    """A primitive on one observable; `hostile` draws parameters that can make
+    the density vanish (narrow gaussians far from the data) or go negative
+    (polynomials with sign changes) -- the reference's error paths."""
+    lo, hi = OBS[name]
+    var = lambda v, a, b: P.Variable(f"p{rng.integers(1 << 30)}", float(v), a, b)
+    k = int(rng.integers(3))
+    if k == 0:
+        sg = (hi - lo) * (rng.uniform(0.002, 0.01) if hostile else rng.uniform(0.05, 0.6))
+        return P.gaussian(o, var(rng.uniform(lo, hi), lo - 5, hi + 5), var(sg, 1e-4, 100))
+    if k == 1:
+        return P.exponential(o, var(rng.uniform(-1.0, 1.0) / (hi - lo) * 3, -50, 50))
+    deg = int(rng.integers(1, 4))
+    if hostile:
+        cs = list(rng.uniform(-1.0, 1.0, deg + 1))
+    else:  # positive on the box
+        cs = [1.0 + (2.0 if lo < 0 else 0.0)] + list(rng.uniform(0.0, 0.3, deg) / max(hi, 1.0) ** np.arange(1, deg + 1))
+    return P.polynomial(o, [var(c, -100, 100) for c in cs])
+
+
+def random_tree(P, rng, obs, names, depth=0, hostile=False):
+    """A tree over exactly `names`: products split the observables, sums share them."""
+    if len(names) > 1:
+        cut = int(rng.integers(1, len(names)))
+        return P.prod_pdf([random_tree(P, rng, obs, names[:cut], depth + 1, hostile),
+                           random_tree(P, rng, obs, names[cut:], depth + 1, hostile)])
+    if depth < 2 and rng.random() < 0.4:
+        n = int(rng.integers(2, 4))
+        kids = [random_tree(P, rng, obs, names, depth + 1, hostile) for _ in range(n)]
+        fr = rng.dirichlet(np.ones(n))[: n - 1] * 0.9
+        return P.add_pdf(kids, [P.Variable(f"f{rng.integers(1 << 30)}", float(f), 0.0, 1.0) for f in fr])
+    return leaf(P, rng, obs[names[0]], names[0], hostile)
+
+
+def outcome(fn):
+    try:
+        return ("ok", float(fn()))
+    except Exception as exc:  # the reference's class and index
+        return (type(exc).__name__, getattr(exc, "index", None))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=300)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+
+    import paper_1710_08826_b200 as pf
+
+    P = pf.parafit
+    ctx = pf.device_context(0)
+    rng = np.random.default_rng(args.seed)
+    bad, n_ok, n_err, worst = [], 0, 0, 0.0
+    t0 = time.perf_counter()
+    for case in range(args.cases):
+        obs = {k: P.Variable.observable(k, *OBS[k]) for k in OBS}
+        use = list(rng.permutation(list(OBS))[: int(rng.integers(1, 4))])
+        pdf = random_tree(P, rng, obs, use, hostile=bool(rng.random() < 0.3))
+        names = sorted({n for node in pdf.walk() for n in node.observable_names()})
+        n = int(rng.choice([1, 2, 17, 4095, 4097, 9000, 50_001, 300_000]))
+        cols = [rng.uniform(*OBS[k], n) for k in names]
+        ds = pf.DeviceDataSet.from_columns([obs[k] for k in names], cols, device=None)
+        snap = P.snapshot(pdf.param_closure())
+        with pf.reference_norms():
+            want = outcome(lambda: P.nll(pdf, ds, snap, P.Backend("serial"), P.NormalizationStore()))
+        results = {}
+        try:
+            for mode in (1, 2, 3, 0):
+                ctx.set_pipeline(mode)
+                results[mode] = outcome(lambda: pf.nll(pdf, ds))
+            w = int(rng.choice([1, 2, 4, 8]))
+            ctx.set_pipeline(1)
+            ctx.set_warps_per_block(w)
+            results[f"w{w}"] = outcome(lambda: pf.nll(pdf, ds))
+        finally:
+            ctx.set_pipeline(1)
+            ctx.set_warps_per_block(0)
+        for key, got in results.items():
+            if want[0] == "ok":
+                r = abs(got[1] - want[1]) / max(abs(want[1]), 1e-300) if got[0] == "ok" else math.inf
+                worst = max(worst, r)
+                if not r <= 1e-10:
+                    bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
+            elif got != want:
+                bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
+        if want[0] == "ok":
+            n_ok += 1
+        else:
+            n_err += 1
+    out = {"cases": args.cases, "seed": args.seed, "ok_cases": n_ok, "error_cases": n_err,
+           "evaluations": args.cases * 5, "worst_rel": worst, "mismatches": bad[:20], "n_mismatches": len(bad),
+           "wall_s": time.perf_counter() - t0}
+    line = json.dumps(out)
+    print(line)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(line + "\n")
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
