@@ -3,7 +3,9 @@ polynomial leaves; sums over shared observables, products over disjoint
 ones; 1-3 observables), random parameters, random event counts (1 .. 300k,
 ragged), every pipeline mode and a random warps-per-block override -- each
 device NLL against the reference's own nll on the same events (<= 1e-10, or
-the same exception class and index).
+the same exception class and index); for valid cases, three perturbed
+parameter points evaluated as one batch (pfb_nll_batch) must equal their
+single-point values bit for bit.
 
     python scripts/fuzz_parity.py [--cases 300] [--seed 1] [--out profiles/r2_fuzz.json]
 """
@@ -78,7 +80,7 @@ def main():
     P = pf.parafit
     ctx = pf.device_context(0)
     rng = np.random.default_rng(args.seed)
-    bad, n_ok, n_err, worst = [], 0, 0, 0.0
+    bad, n_ok, n_err, worst, n_batch = [], 0, 0, 0.0, 0
     t0 = time.perf_counter()
     for case in range(args.cases):
         obs = {k: P.Variable.observable(k, *OBS[k]) for k in OBS}
@@ -111,12 +113,33 @@ def main():
                     bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
             elif got != want:
                 bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
+        # batched points (pfb_nll_batch) bitwise their single-point values
+        free = [v for v in pdf.param_closure() if not v.fixed]
+        if free and want[0] == "ok":
+            base = np.array([v.value for v in free])
+            pts = [base * (1.0 + 1e-4 * k) for k in range(3)]
+            singles, snaps, norms = [], [], []
+            store = P.NormalizationStore()
+            for pt in pts:
+                for v, val in zip(free, pt):
+                    P.set_value(v, float(np.clip(val, v.lower, v.upper)))
+                singles.append(outcome(lambda: pf.nll(pdf, ds)))
+                sn = P.snapshot(pdf.param_closure())
+                snaps.append(sn)
+                norms.append(P.resolve_norms(pdf, sn, store))
+            cols_d = {k: ds.column(k) for k in names}
+            got = pf.DeviceBackend().evaluate_batch(pdf, cols_d, snaps, norms, 0, ds.n_events)
+            got = [("ok", float(g)) if not isinstance(g, Exception) else (type(g).__name__, getattr(g, "index", None))
+                   for g in got]
+            if got != singles:
+                bad.append({"case": case, "mode": "batch", "n": n, "tree": repr(pdf), "want": singles, "got": got})
+            n_batch += 1
         if want[0] == "ok":
             n_ok += 1
         else:
             n_err += 1
     out = {"cases": args.cases, "seed": args.seed, "ok_cases": n_ok, "error_cases": n_err,
-           "evaluations": args.cases * 5, "worst_rel": worst, "mismatches": bad[:20], "n_mismatches": len(bad),
+           "evaluations": args.cases * 5, "batched_cases": n_batch, "worst_rel": worst, "mismatches": bad[:20], "n_mismatches": len(bad),
            "wall_s": time.perf_counter() - t0}
     line = json.dumps(out)
     print(line)
