@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -96,10 +97,12 @@ static int cuda_fail(cudaError_t e) {
 }
 
 static constexpr int kStoreMaxCols = 16;
-// result words: [0, 72) exported accumulator, [72] deferred-block count, [73] error key
+// result words: a head, one exported accumulator per point, then the heads of
+// the quadrature slots (quad_enqueue: up to kMaxPts launches behind one wait)
 static constexpr int kResHead = 5;  // [0] deferred-block count, [1] error key, [2] [3] fused exchange
                                     // status, [4] completion sequence (post_seq)
-static constexpr int kResWords = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
+static constexpr int kResQuad = kResHead + kMaxPts * PFB_ACC_WORDS;  // + one accumulator per point
+static constexpr int kResWords = kResQuad + kMaxPts * 4;             // + {count, error key} per slot
 enum { MODE_EXPORT = 0, MODE_ADD_EXPORT = 1, MODE_ACCUM = 2 };
 
 static constexpr int64_t kIoChunk = 4 << 20;  // doubles per staging buffer (32 MB)
@@ -2178,32 +2181,71 @@ int pfb_bin_fill(pfb_ctx* c, const pfb_store* st, int64_t begin, int64_t end, in
     return PFB_OK;
 }
 
-int pfb_quadrature(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int32_t weight_col, const double* values,
-                   int32_t nvalues, const double* norms, int32_t nnorms, double* out, pfb_err* out_err) {
-    pfb_plan* p = const_cast<pfb_plan*>(pc);
-    if (!c || !p || !st || !values || !norms || !out || p->ctx != c || st->ctx != c)
-        return PFB_E_INVALID_ARGUMENT;
-    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
+}  // extern "C"
+
+// One quadrature launch into result slot q (accumulator q, head kResQuad + 4q),
+// without a wait: the objective enqueues every quadrature norm of a batch of
+// points and waits once (pfb_objective_eval_batch).  A keeps the packed
+// arguments for quad_collect's error decoding; *frac the fraction status.
+static int quad_enqueue(pfb_ctx* c, pfb_plan* p, const pfb_store* st, int32_t weight_col, const double* values,
+                        const double* norms, int q, NllArgs* A, int* frac) {
+    *frac = pack_args(p, st, 0, st->n, values, norms, A);
+    A->acc_out = c->res_dev + kResHead + (int64_t)q * PFB_ACC_WORDS;
+    A->result_i = c->res_dev + kResQuad + 4 * q;
+    CK(launch_quadrature(*A, st->cols[weight_col], st->n, c->stream, c->sm_count));
+    ++c->launches;
+    return PFB_OK;
+}
+
+// Slots [0, nq) after their launches: copy the result block back if it is not mapped.
+static int quad_wait(pfb_ctx* c) {
+    if (!c->res_mapped)
+        CK(cudaMemcpyAsync(c->res_host, c->res_dev, sizeof(long long) * kResWords, cudaMemcpyDeviceToHost,
+                           c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return PFB_OK;
+}
+
+// Slot q's integral (after quad_wait): the status and the rounded sum.
+static int quad_collect(pfb_ctx* c, const pfb_plan* p, const NllArgs& A, int q, int frac, double* out,
+                        pfb_err* err) {
+    int code = decode_error(c, p, A, (unsigned long long)c->res_host[kResQuad + 4 * q + 1], frac, 0, err);
+    double r = 0.0;
+    if (!code) code = acc_round(c->res_host + kResHead + (int64_t)q * PFB_ACC_WORDS, &r);
+    if (err) err->code = code;
+    *out = r;
+    return code;
+}
+
+static int quad_check(const pfb_ctx* c, const pfb_plan* p, const pfb_store* st, int32_t weight_col) {
+    if (!c || !p || !st || p->ctx != c || st->ctx != c) return PFB_E_INVALID_ARGUMENT;
     if (weight_col < 0 || weight_col >= st->ncols || st->n < 1) return PFB_E_INVALID_ARGUMENT;
     for (int s = 0; s < p->nslots; ++s)
         if (p->slot_col[s] >= st->ncols || p->slot_col[s] == weight_col) return PFB_E_INVALID_ARGUMENT;
+    return PFB_OK;
+}
+
+extern "C" {
+
+int pfb_quadrature(pfb_ctx* c, const pfb_plan* pc, const pfb_store* st, int32_t weight_col, const double* values,
+                   int32_t nvalues, const double* norms, int32_t nnorms, double* out, pfb_err* out_err) {
+    pfb_plan* p = const_cast<pfb_plan*>(pc);
+    if (!values || !norms || !out || quad_check(c, p, st, weight_col)) return PFB_E_INVALID_ARGUMENT;
+    if (nvalues != p->nraw || nnorms != (int32_t)p->nodes.size()) return PFB_E_INVALID_ARGUMENT;
     clear_err(out_err);
     CK(cudaSetDevice(c->device));
     PFB_QUIESCE(c);
     auto A = std::make_unique<NllArgs>();
-    const int frac = pack_args(p, st, 0, st->n, values, norms, A.get());
+    int frac = -1;
     if (c->timing) CK(cudaEventRecord(c->ev0, c->stream));
-    CK(launch_quadrature(*A, st->cols[weight_col], st->n, c->stream, c->sm_count));
-    ++c->launches;
-    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
-    int rc = read_result(c);
+    int rc = quad_enqueue(c, p, st, weight_col, values, norms, 0, A.get(), &frac);
     if (rc) return rc;
+    if (c->timing) CK(cudaEventRecord(c->ev1, c->stream));
+    rc = quad_wait(c);
+    if (rc) return rc;
+    if (c->timing) cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1);
     pfb_err e;
-    int code = decode_error(c, p, *A, (unsigned long long)c->res_host[1], frac, 0, &e);
-    double r = 0.0;
-    if (!code) code = acc_round(c->res_host + kResHead, &r);
-    e.code = code;
-    *out = r;
+    const int code = quad_collect(c, p, *A, 0, frac, out, &e);
     if (out_err) *out_err = e;
     return code;
 }

@@ -40,6 +40,20 @@ struct pfb_objective {
     std::vector<double> values, norms;
     std::vector<std::vector<double>> last_in;
     std::vector<char> have;
+    std::vector<int> pend;  // per node: the unresolved quadrature slot its norm waits on, or -1
+};
+
+// The quadrature norms of one pfb_objective_eval_batch: each is launched into
+// its own result slot as obj_fill meets it and the batch waits once for all
+// of them (instead of a launch + wait per norm); a point's norm that is still
+// in flight is recorded as a use (point, node, slot) and filled in at the wait.
+struct QuadBatch {
+    struct Req {
+        int m, node, frac;
+        std::unique_ptr<NllArgs> A;
+    };
+    std::vector<Req> req;
+    std::vector<std::array<int, 3>> use;  // (point, node, slot)
 };
 
 static const double kSqrt2 = 1.4142135623730951;        // math.sqrt(2.0)
@@ -117,8 +131,9 @@ static int obj_norm(const pfb_objective* o, int i, const double* raw, double* ou
     return PFB_OK;
 }
 
-// x -> o->values, o->norms (cached per node on its raw inputs' bits).
-static int obj_fill(pfb_objective* o, const double* x, pfb_err* err) {
+// x -> o->values, o->norms (cached per node on its raw inputs' bits).  With
+// `qb`, quadrature norms are enqueued for point m (o->pend) instead of waited for.
+static int obj_fill(pfb_objective* o, const double* x, pfb_err* err, QuadBatch* qb = nullptr, int m = 0) {
     pfb_plan* p = o->plan;
     for (size_t k = 0; k < o->lower.size(); ++k)
         if (!(o->lower[k] <= x[k] && x[k] <= o->upper[k])) {  // NaN fails too
@@ -137,6 +152,22 @@ static int obj_fill(pfb_objective* o, const double* x, pfb_err* err) {
         const double* raw = o->values.data() + off;
         std::vector<double>& last = o->last_in[i];
         if (o->have[i] && memcmp(last.data(), raw, sizeof(double) * np) == 0) continue;
+        const pfb_obj_node& nd = o->node[i];
+        if (qb && nd.norm_kind == PFB_NORM_QUADRATURE) {
+            const int q = (int)qb->req.size();  // the caller keeps a slot per quadrature node free
+            if (quad_check(o->ctx, nd.quad_plan, nd.quad_rule, nd.weight_col)) return PFB_E_INVALID_ARGUMENT;
+            QuadBatch::Req r{m, i, -1, std::make_unique<NllArgs>()};
+            const double one = 1.0;
+            const int rc = quad_enqueue(o->ctx, nd.quad_plan, nd.quad_rule, nd.weight_col, raw, &one, q, r.A.get(),
+                                        &r.frac);
+            if (rc) return rc;
+            qb->req.push_back(std::move(r));
+            o->pend[i] = q;
+            o->norms[i] = NAN;
+            last.assign(raw, raw + np);
+            o->have[i] = 1;
+            continue;
+        }
         double v = 0.0;
         const int st = obj_norm(o, i, raw, &v);
         if (st) {
@@ -150,10 +181,52 @@ static int obj_fill(pfb_objective* o, const double* x, pfb_err* err) {
             return st;
         }
         o->norms[i] = v;
+        if (!o->pend.empty()) o->pend[i] = -1;
         last.assign(raw, raw + np);
         o->have[i] = 1;
     }
     return PFB_OK;
+}
+
+// Wait for the batch's quadratures and fill their norms into the points that
+// use them (nv: npts x nn) and into the node cache.  Returns PFB_OK, a fatal
+// code, or -1 with the first failing norm in sequential order (lowest point,
+// then lowest node) in *fail_m / *fail_err -- the cache is then dropped (the
+// sequential objective stops at that norm; recomputing gives the same bits).
+static int quad_flush(pfb_objective* o, QuadBatch* qb, double* nv, int* fail_m, pfb_err* fail_err) {
+    if (qb->req.empty()) return PFB_OK;
+    const int nn = (int)o->norms.size();
+    int rc = quad_wait(o->ctx);
+    if (rc) return rc;
+    std::vector<double> v(qb->req.size());
+    std::vector<int> code(qb->req.size());
+    int worst = -1;
+    for (size_t q = 0; q < qb->req.size(); ++q) {
+        const QuadBatch::Req& r = qb->req[q];
+        pfb_err e;
+        code[q] = quad_collect(o->ctx, o->node[r.node].quad_plan, *r.A, (int)q, r.frac, &v[q], &e);
+        if (code[q] >= PFB_E_INVALID_ARGUMENT) return code[q];
+        if (!code[q] && !(std::isfinite(v[q]) && v[q] > 0.0)) code[q] = PFB_E_NONPOSITIVE_NORM;
+        if (code[q] && (worst < 0 || r.m < qb->req[worst].m || (r.m == qb->req[worst].m && r.node < qb->req[worst].node)))
+            worst = (int)q;
+    }
+    for (const auto& u : qb->use) nv[(size_t)u[0] * nn + u[1]] = v[u[2]];
+    for (int i = 0; i < nn; ++i)
+        if (o->pend[i] >= 0) {
+            o->norms[i] = v[o->pend[i]];
+            o->pend[i] = -1;
+        }
+    if (worst >= 0) {
+        *fail_m = qb->req[worst].m;
+        fail_err->code = code[worst];
+        fail_err->node = qb->req[worst].node;
+        fail_err->index = -1;
+        fail_err->value = NAN;
+        for (auto& h : o->have) h = 0;
+    }
+    qb->req.clear();
+    qb->use.clear();
+    return worst >= 0 ? -1 : PFB_OK;
 }
 
 // ---- the persistent kernel (pfb_nll_task.cuh nll_persist_kernel) -----------------
@@ -339,6 +412,7 @@ int pfb_objective_create(pfb_ctx* c, pfb_plan* p, const pfb_store* st, int64_t b
     o->norms.assign(nn, 1.0);
     o->last_in.resize(nn);
     o->have.assign(nn, 0);
+    o->pend.assign(nn, -1);
     *out = o.release();
     return PFB_OK;
 }
@@ -376,16 +450,44 @@ int pfb_objective_eval_batch(pfb_objective* o, const double* xs, int32_t npts, i
         return PFB_E_INVALID_ARGUMENT;
     const int nraw = o->plan->nraw, nn = (int)o->norms.size();
     std::vector<double> vals((size_t)npts * nraw), nv((size_t)npts * nn);
+    int nquad = 0;
+    for (const auto& nd : o->node) nquad += nd.norm_kind == PFB_NORM_QUADRATURE;
+    QuadBatch qb;
+    QuadBatch* qbp = nquad && nquad <= kMaxPts && !o->persistent ? &qb : nullptr;
+    if (qbp) {
+        CK(cudaSetDevice(o->ctx->device));
+        PFB_QUIESCE(o->ctx);
+    }
     int first_bad = npts;  // sequential semantics: nothing after the first host failure
+    int fail_m = npts;
+    pfb_err fail_err;
     for (int m = 0; m < npts; ++m) {
         clear_err(out_err + m);
-        const int st = obj_fill(o, xs + (size_t)m * nfree, out_err + m);
+        if (qbp && (int)qb.req.size() + nquad > kMaxPts) {  // keep a slot per quadrature node free
+            const int rc = quad_flush(o, qbp, nv.data(), &fail_m, &fail_err);
+            if (rc > 0) return rc;
+            if (rc < 0) break;
+        }
+        const int st = obj_fill(o, xs + (size_t)m * nfree, out_err + m, qbp, m);
+        if (st >= PFB_E_INVALID_ARGUMENT) return st;
         if (st) {
             first_bad = m;
             break;
         }
         std::copy(o->values.begin(), o->values.end(), vals.begin() + (size_t)m * nraw);
         std::copy(o->norms.begin(), o->norms.end(), nv.begin() + (size_t)m * nn);
+        if (qbp)
+            for (int i = 0; i < nn; ++i)
+                if (o->pend[i] >= 0) qb.use.push_back({m, i, o->pend[i]});
+    }
+    if (qbp && fail_m == npts) {
+        const int rc = quad_flush(o, qbp, nv.data(), &fail_m, &fail_err);
+        if (rc > 0) return rc;
+    }
+    if (fail_m < npts && fail_m <= first_bad) {  // a quadrature norm failed first (in sequential order)
+        if (first_bad < npts) clear_err(out_err + first_bad);
+        first_bad = fail_m;
+        out_err[fail_m] = fail_err;
     }
     if (first_bad > 0) {
         const int code = pfb_nll_batch(o->ctx, o->plan, o->store, o->begin, o->end, 0, vals.data(), first_bad,

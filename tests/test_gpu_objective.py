@@ -165,3 +165,64 @@ def test_polynomial_norm_in_c_and_fallback(pf):
         fcn = pf.DeviceFitManager(g, ds).fcn()
         assert type(fcn._objective) is DeviceObjective and not isinstance(fcn._objective, FastObjective)
         assert math.isfinite(fcn(np.array([0.5, 0.3])))
+
+
+def test_batched_quadrature_norms_equal_sequential(pf):
+    """pfb_objective_eval_batch enqueues every quadrature norm of its points
+    into separate result slots and waits once (flushing when the 16 slots run
+    out); the values must be the sequential objective's bit for bit, norms
+    reused from the previous point included, and a quadrature that fails
+    mid-batch (NegativeDensity at a GL abscissa) must end the list where the
+    sequential calls end it, with the same exception."""
+    from paper_1710_08826_b200.fitting import FastObjective
+
+    x = P.Variable.observable("x", 0.0, 1.0)
+    p1 = P.polynomial(x, [P.Variable("a0", 1.0, 0.01, 2.0), P.Variable("a1", 0.2, -1.0, 1.0)])
+    p2 = P.polynomial(x, [P.Variable("b0", 0.5, 0.01, 2.0), P.Variable("b1", 0.1, -1.0, 1.0),
+                          P.Variable("b2", 0.3, 0.0, 1.0)])
+    pdf = P.add_pdf([p1, p2], [P.Variable("f", 0.4, 0.0, 1.0)])
+    ds = models.dataset([x], [np.random.default_rng(5).uniform(0.0, 1.0, 50_001)])
+    fcn = pf.DeviceFitManager(pdf, ds).fcn()
+    obj = fcn._objective
+    assert isinstance(obj, FastObjective)
+    rng = np.random.default_rng(11)
+    base = np.array([1.0, 0.2, 0.5, 0.1, 0.3, 0.4])  # a0 a1 b0 b1 b2 f (free-parameter order below)
+    names = [v.name for v in obj.free]
+    assert sorted(names) == sorted(["a0", "a1", "b0", "b1", "b2", "f"])
+    order = [["a0", "a1", "b0", "b1", "b2", "f"].index(n) for n in names]
+
+    def pts(k, bad=None):
+        out = []
+        for j in range(k):
+            pt = base.copy()
+            if j % 3 == 1:
+                pt[5] = rng.uniform(0.1, 0.9)  # only the fraction moves: both norms reused
+            elif j % 3 == 2:
+                pt[0], pt[1] = rng.uniform(0.5, 1.5), rng.uniform(-0.3, 0.3)  # one quadrature
+            else:
+                pt[:5] = [rng.uniform(0.5, 1.5), rng.uniform(-0.3, 0.3), rng.uniform(0.5, 1.5),
+                          rng.uniform(-0.3, 0.3), rng.uniform(0.0, 0.5)]  # two
+            if j == bad:
+                pt[2], pt[3], pt[4] = 0.02, -0.9, 0.0  # b(x) < 0 for x > 0.022: the GL integral fails
+            out.append(pt[order])
+        return out
+
+    def sequential(xs):
+        out = []
+        for pt in xs:
+            v = obj._try(lambda pt=pt: obj._direct(pt))
+            out.append(v)
+            if isinstance(v, BaseException):
+                break
+        return out
+
+    for k, bad in ((16, None), (16, 9), (5, 0), (16, 15), (12, 4)):
+        xs = pts(k, bad)
+        got = obj.evaluate_points(xs)
+        want = sequential(xs)
+        assert len(got) == len(want), (k, bad)
+        for g, w in zip(got, want):
+            if isinstance(w, BaseException):
+                assert type(g) is type(w), (k, bad, g, w)
+            else:
+                assert g == w, (k, bad, g, w)
