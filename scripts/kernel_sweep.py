@@ -1,6 +1,6 @@
 """Device-time sweep of the NLL kernels: evaluator x warps-per-block.
 
-    python scripts/kernel_sweep.py [--n 10000000] [--configs terms,c1,c2,c3] [--warps 0,1,2,4,8]
+    python scripts/kernel_sweep.py [--n 10000000] [--configs terms,c1,c2,c2p,c3] [--warps 0,1,2,4,8]
 
 Each measurement: 3 warm-up calls, then `reps` calls each preceded by a
 256 MB L2-evicting write; device time of the fused kernel from CUDA events
@@ -88,6 +88,11 @@ def main():
         elif cfg == "c2":
             cols = list(mcgen.prod_2d(n, 5.0, 1.0, -0.4, 0.0, 10.0, 2))
             obs, pdf, _ = models.c2()
+        elif cfg == "c2p":  # gaussian(x) x polynomial(y), bench.py's C2p sub-result
+            import bench
+
+            obs, pdf, _ = bench.build_model(pf.parafit, "c2p")
+            cols = bench.host_events("c2p", n, 5)
         else:
             terms = [(p, s, m, w, mag, ph) for (p, m, w, s, mag, ph) in models.C3_TERMS]
             cols = list(mcgen.device_dalitz(n, terms, models.D_CHANNEL_T, 3))  # Philox on the GPU
