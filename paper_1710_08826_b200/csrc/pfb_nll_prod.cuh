@@ -29,8 +29,6 @@
 // <= 16 u, i.e. an absolute error <= 4e-15 in each unit's -ln -- orders of
 // magnitude inside the 1e-10 relative NLL tolerance.
 #pragma once
-#include <type_traits>
-
 #include "pfb_nll_tma.cuh"
 
 
@@ -611,7 +609,10 @@ constexpr int kSumRing = 4;
 
 // PFB_TRACE timeline helpers: pfb_nll_kernel.cuh
 
-template <class Ev, int S, bool PROD, int TEAMS = UnitTeams<Ev>::value>
+// ONE: a single parameter point (A.npts == 1) with the point index a
+// compile-time 0 -- POINTS evaluators then read constant parameter offsets as
+// unbatched ones do (a runtime index cost the C2p kernel 15%).
+template <class Ev, int S, bool PROD, int TEAMS = UnitTeams<Ev>::value, bool ONE = false>
 __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_kernel(const __grid_constant__ NllArgs A) {
     constexpr int kSumTeams = TEAMS;
     constexpr int NC = Ev::NC;
@@ -774,11 +775,7 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
             const double* sx = stage + (int64_t)s * NC * kBlock;
             const bool tail = A.tail && bidx == A.nfull;
             const int n = tail ? A.tail : kBlock;
-            // one parameter point's pass over the staged block; a single point of
-            // a POINTS evaluator runs with m a compile-time 0 (constant parameter
-            // offsets, as unbatched: a runtime m cost the C2p kernel 15%)
-            auto point = [&](auto mm) {
-                const int m = mm;
+            for (int m = 0; m < (ONE ? 1 : A.npts); ++m) {
                 bool bad = false;
                 double acc = 0.0;
                 Unit un;
@@ -826,20 +823,11 @@ __global__ void __launch_bounds__(32 * (kSumWarps * TEAMS + 1), 1) nll_tma_unit_
                     bad |= !unit_ok<Ev>(A, un, m);
                     acc = unit_value<Ev>(A, un, m);
                 }
-                if (m == A.npts - 1) {  // the stage is no longer read by this warp
+                if (ONE || m == A.npts - 1) {  // the stage is no longer read by this warp
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty_bar[s]);
                 }
                 post_fold(acc, bad, m, bidx);
-            };
-            if constexpr (HasPoints<Ev>::value && !IsRatio<Ev>::value) {
-                if (A.npts == 1) {
-                    point(std::integral_constant<int, 0>{});
-                } else {
-                    for (int m = 0; m < A.npts; ++m) point(m);
-                }
-            } else {
-                for (int m = 0; m < A.npts; ++m) point(m);
             }
         }
     }
@@ -865,17 +853,25 @@ static cudaError_t launch_tma_unit(const NllArgs& A, cudaStream_t stream, int sm
     constexpr int S = NC == 1 ? (HasTab<Ev>::value ? 4 : 6) : 3;
     const size_t smem = (size_t)S * NC * kBlock * sizeof(double) +
                         (HasTab<Ev>::value ? (size_t)kMaxPts * kTabN * sizeof(double) : 0);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(nll_tma_unit_kernel<Ev, S, PROD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr int T = UnitTeams<Ev>::value;
+    constexpr bool kOne = HasPoints<Ev>::value && !IsRatio<Ev>::value;  // a single-point instance pays off
+    const bool one = kOne && A.npts == 1;
+    static bool configured[2] = {false, false};
+    if (!configured[one]) {
+        cudaError_t e = one ? cudaFuncSetAttribute(nll_tma_unit_kernel<Ev, S, PROD, T, kOne>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                            : cudaFuncSetAttribute(nll_tma_unit_kernel<Ev, S, PROD, T>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured[one] = true;
     }
     const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
     int64_t grid = sm_count;
     if (grid > nitems) grid = nitems > 0 ? nitems : 1;
-    nll_tma_unit_kernel<Ev, S, PROD><<<(unsigned)grid, 32 * (kSumWarps * UnitTeams<Ev>::value + 1), smem, stream>>>(A);
+    if (one)
+        nll_tma_unit_kernel<Ev, S, PROD, T, kOne><<<(unsigned)grid, 32 * (kSumWarps * T + 1), smem, stream>>>(A);
+    else
+        nll_tma_unit_kernel<Ev, S, PROD, T><<<(unsigned)grid, 32 * (kSumWarps * T + 1), smem, stream>>>(A);
     return cudaGetLastError();
 }
 

@@ -93,6 +93,27 @@ def test_batch_equals_single_bitwise(pf, config):
     assert any(w[0] == "ok" for w in want)
 
 
+@pytest.mark.parametrize("npts", [2, 8, 16])
+def test_c1_points_many_blocks_per_cta_bitwise(pf, npts):
+    """C1 SumPdf points (EvSum2GE::POINTS in the TMA unit kernel) over 3M
+    events -- ~5 blocks per CTA, so every stage of the ring and every fold
+    slot is reused while the points of a block are in flight -- each bitwise
+    its single-point value (a fit-like stencil: steps of 1e-3 around a point)."""
+    rng = np.random.default_rng(17)
+    n = 3_000_000 + 1234
+    x, pdf, params = models.c1()
+    xs = np.clip(np.concatenate([rng.normal(5, 0.5, n // 3), rng.exponential(3.3, n - n // 3)]), 0, 10)
+    ds = models.dataset([x], [xs])
+    base = np.array([4.9789, 0.5726, -0.3046, 0.3041])
+    pts = [base + 1e-3 * rng.standard_normal(4) * (k > 0) for k in range(npts)]
+    want = [outcome(single(pf, pdf, ds, params, p)) for p in pts]
+    snaps, norms = points_eval(pf, pdf, ds, params, pts)
+    cols = {"x": ds.column("x")}
+    for _ in range(3):
+        got = pf.DeviceBackend().evaluate_batch(pdf, cols, snaps, norms, 0, ds.n_events)
+        assert [outcome(r) for r in got] == want
+
+
 def test_sixteen_points_all_blocks_deferred(pf):
     """16 points (the batch maximum) over 2000 blocks where every block holds
     an event whose gaussian exponent lies in (-746, -600) at every point: all
