@@ -246,7 +246,10 @@ struct EvSum2GE {
 // Certification: u >= -600 (the reference's exp(u) is a normal double), q
 // positive within 2^+-250 (unit check), and the EvSop budget
 // |u| + |log2 q| ln2 + 1 <= thr (thr = 690 - |ln c|: the reference's linear
-// product stays normal).  Explicit _rn operations: every shell that runs
+// product stays normal).  Per unit (LMIN, lmin_ok): the smallest l bounds
+// every -u and the unit's q range bounds every |log2 q|, so one check covers
+// the unit's 16 events (a conservative superset of the per-event checks:
+// ~9 fewer instructions per event).  Explicit _rn operations: every shell that runs
 // this evaluator (bulk, TMA unit, SIMT) gives the same bits.  NV > 0: the
 // coefficient count at compile time (unrolled Horner); 0: A.leaf[1].nv.
 template <int NV = 0>
@@ -255,6 +258,9 @@ struct EvGaussPoly {
     static constexpr int U = 2;
     static constexpr int MINB = 3;
     static constexpr bool POINTS = true;  // every value from the point's ptv row: batchable
+    static constexpr bool LMIN = PFB_UNIT_MINMAX != 0;  // the budget checked per unit
+    __device__ static __forceinline__ double lcoef(const NllArgs& A, int m) { return A.ptv[m][kPtLeafWords]; }
+    __device__ static __forceinline__ double lthr(const NllArgs& A, int m) { return A.ptv[m][kPtLeafWords + 1]; }
 
     __device__ static __forceinline__ double one(const NllArgs& A, double xg, double y, bool& ok, double& l,
                                                  int m = 0) {
@@ -271,11 +277,15 @@ struct EvGaussPoly {
             for (int i = nv - 1; i >= 1; --i) q = fma(q, y, v[1 + i]);
         }
         l = __dadd_rn(v[kPtLeafWords], u);
-        // |binary exponent of q| as a double without I2F (magic-number add)
-        const int e = ((__double2hiint(q) >> 20) & 0x7ff) - 1023;
-        const double ae = __dsub_rn(__hiloint2double(0x43300000, e < 0 ? -e : e), 0x1p52);
-        const double budget = fma(ae, 0.6931471805599453, __dsub_rn(1.0, u));
-        ok = (u >= -600.0) && (budget <= v[kPtLeafWords + 1]);
+        if constexpr (LMIN) {
+            ok = true;
+        } else {
+            // |binary exponent of q| as a double without I2F (magic-number add)
+            const int e = ((__double2hiint(q) >> 20) & 0x7ff) - 1023;
+            const double ae = __dsub_rn(__hiloint2double(0x43300000, e < 0 ? -e : e), 0x1p52);
+            const double budget = fma(ae, 0.6931471805599453, __dsub_rn(1.0, u));
+            ok = (u >= -600.0) && (budget <= v[kPtLeafWords + 1]);
+        }
         return q;
     }
 
@@ -375,6 +385,7 @@ struct Unit {
     // and NaN all fall outside any finite positive range -- one unit-level
     // range check instead of one per event
     int qlo = 0x7fffffff, qhi = 0, rlo = 0x7fffffff, rhi = 0;
+    double lmin = 1e300;  // Ev::LMIN: smallest l (every unit holds at least one event)
 #endif
 };
 
@@ -385,6 +396,14 @@ struct IsRatio {
 template <class Ev>
 struct IsRatio<Ev, decltype((void)Ev::RATIO)> {
     static constexpr bool value = Ev::RATIO;
+};
+template <class Ev, class = void>
+struct HasLMin {
+    static constexpr bool value = false;
+};
+template <class Ev>
+struct HasLMin<Ev, decltype((void)Ev::LMIN)> {
+    static constexpr bool value = Ev::LMIN;
 };
 template <class Ev, class = void>
 struct HasXMax {
@@ -438,6 +457,10 @@ __device__ __forceinline__ void prod_row(const NllArgs& A, const double2 (&x)[Ev
         q = Ev::prob2(A, x, okx, oky, tab, l, m);
     else
         q = Ev::prob2(A, x, okx, oky, tab, l);
+#if PFB_UNIT_MINMAX
+    // (before the tail masking: an absent second event duplicates the first)
+    if constexpr (HasLMin<Ev>::value) u.lmin = fmin(u.lmin, fmin(l.x, l.y));
+#endif
     if (TAIL) {
         if (e >= n) {
             q.x = 1.0;
@@ -510,11 +533,31 @@ __device__ __forceinline__ bool unit_in_range(const Unit& u, bool ratio) {
 #endif
 }
 
+// Ev::LMIN's budget for the whole unit: -u <= ln c - lmin (+ 1e-9 for the
+// rounding of l = ln c + u and of the difference, both < 2^-41 here) bounds
+// every event's -u, and the high words qlo / qhi (positive, within 2^+-kSpanM
+// once unit_in_range holds) bound every |binary exponent of q|.
+template <class Ev>
+__device__ __forceinline__ bool lmin_ok(const NllArgs& A, const Unit& u, int m) {
+#if PFB_UNIT_MINMAX
+    const double negu = __dadd_rn(__dsub_rn(Ev::lcoef(A, m), u.lmin), 1e-9);
+    const int elo = ((u.qlo >> 20) & 0x7ff) - 1023, ehi = ((u.qhi >> 20) & 0x7ff) - 1023;
+    const int me = max(abs(elo), abs(ehi));
+    return negu <= 600.0 && fma(int_to_double(me), 0.6931471805599453, __dadd_rn(1.0, negu)) <= Ev::lthr(A, m);
+#else
+    (void)A;
+    (void)u;
+    (void)m;
+    return true;
+#endif
+}
+
 // every unit-level certificate of an evaluator
 template <class Ev>
 __device__ __forceinline__ bool unit_ok(const NllArgs& A, const Unit& u, int m = 0) {
     bool ok = unit_in_range(u, IsRatio<Ev>::value);
     if constexpr (HasXMax<Ev>::value) ok = ok && u.xhi < A.g2_wlim[m];
+    if constexpr (HasLMin<Ev>::value) ok = ok && lmin_ok<Ev>(A, u, m);
     return ok;
 }
 
