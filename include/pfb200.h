@@ -167,10 +167,12 @@ int pfb_ctx_set_warps_per_block(pfb_ctx* ctx, int warps);
  *  1 (default) TMA-fed kernels -- the unit-sum kernel for log-domain plans
  *    (C2; the register-window SIMT form of the same blocks up to 8 blocks
  *    per SM), the TMA product kernel for two-column product evaluators
- *    (Dalitz), per-warp bulk prefetch for one-column ones (C1);
+ *    (Dalitz), per-warp bulk prefetch for one-column ones (C1; the TMA
+ *    product kernel from 24 blocks per SM);
  *  2 the reference-tree TMA kernel for log-domain plans, per-warp bulk
  *    prefetch for every product evaluator;
  *  3 the TMA product kernel for every product evaluator;
+ *  4 as 1, with the one-column SumPdf (C1 / C5) on the warp-task kernel;
  *  0 the SIMT log-domain streaming kernel (reference tree) everywhere. */
 int pfb_ctx_set_pipeline(pfb_ctx* ctx, int mode);
 /* Number of engine kernels launched on this context since creation. */

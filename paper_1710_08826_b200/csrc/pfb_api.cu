@@ -457,7 +457,7 @@ int pfb_ctx_set_warps_per_block(pfb_ctx* c, int w) {
 }
 
 int pfb_ctx_set_pipeline(pfb_ctx* c, int mode) {
-    if (!c || mode < 0 || mode > 3) return PFB_E_INVALID_ARGUMENT;
+    if (!c || mode < 0 || mode > 4) return PFB_E_INVALID_ARGUMENT;
     c->pipeline = mode;
     return PFB_OK;
 }
@@ -973,7 +973,8 @@ static int pack_args(const pfb_plan* p, const pfb_store* st, int64_t begin, int6
     // one 4096-event block per 8-warp group: measured fastest for every
     // evaluator at 1M-10M events (scripts/kernel_sweep.py)
     A->warps = c->warps_override;  // 0: the evaluator's default kernel shape
-    A->tma = c->pipeline;
+    A->tma = c->pipeline == 4 ? 1 : c->pipeline;  // 4: pipeline 1 with the warp-task C1 shell
+    A->task_shell = c->pipeline == 4;
     A->acc = c->acc;
     A->ticket = c->ticket;
     A->work_counter = c->work_counter;
@@ -1698,7 +1699,8 @@ int pfb_terms_block_sums(pfb_ctx* c, const double* host_terms, int64_t n, double
     A->evaluator = 100;
     A->npts = 1;
     A->warps = c->warps_override;  // 0: the evaluator's default kernel shape
-    A->tma = c->pipeline;
+    A->tma = c->pipeline == 4 ? 1 : c->pipeline;  // 4: pipeline 1 with the warp-task C1 shell
+    A->task_shell = c->pipeline == 4;
     A->acc = c->acc;
     A->ticket = c->ticket;
     A->work_counter = c->work_counter;

@@ -114,6 +114,7 @@ struct NllArgs {
     int32_t evaluator;
     int32_t warps;            // warps cooperating on one block (1,2,4,8)
     int32_t tma;              // 1: TMA bulk-copy pipeline for HBM-bound evaluators
+    int32_t task_shell;       // pipeline 4: C1 / C5 single points on the warp-task kernel
     int32_t mode;             // KernelMode: export / add-export / accumulate
     int64_t idx_base;         // added to local event indices in error keys
     int64_t block_base;       // global block index of this range's block 0

@@ -8,8 +8,8 @@
 
 namespace pfb {
 
-#ifndef PFB_TASK_ITEMS_PER_SM
-#define PFB_TASK_ITEMS_PER_SM 40  // C1 / C5: the warp-task kernel from ~24M events
+#ifndef PFB_TMA1_ITEMS_PER_SM
+#define PFB_TMA1_ITEMS_PER_SM 24  // C1 / C5 single points: the TMA unit kernel from ~14.5M events
 #endif
 
 static constexpr int kG = PFB_GAUSSIAN, kE = PFB_EXPONENTIAL, kP = PFB_POLYNOMIAL;
@@ -117,18 +117,23 @@ cudaError_t launch_sop(const NllArgs& A, cudaStream_t stream, int sm_count, int 
         // (two exp per event, one log per 16 events) on the SIMT streaming
         // kernel; the log-domain kernel (one exp + one log per event) when
         // the pipeline is off or the shape's preconditions do not hold.
-        // pipeline 1: per-warp bulk prefetch below ~40 blocks per SM, the
-        // warp-task kernel (pfb_nll_task.cuh: no end-of-launch imbalance;
-        // 100M events 202 -> 189 us, 10M 29.7 vs 31.7 us, measured) above;
-        // 2: bulk prefetch; 3: the TMA unit kernel -- the same canonical blocks
+        // pipeline 1: per-warp bulk prefetch below 24 blocks per SM, the TMA
+        // unit kernel above (its single-point instance: 10M 27.6 vs 27.6 us,
+        // 20M 42.0 vs 46.1, 40M 72.7 vs 76.8 for the warp-task kernel, 100M
+        // 160.8 vs 164.8 -- measured); 2: bulk prefetch; 3: the TMA unit
+        // kernel; 4: the warp-task kernel (pfb_nll_task.cuh) -- the same
+        // canonical blocks, the same bits
         if (nl == 2 && nt == 2 && kinds == (kG | kE << 2) && A.tma && sum2ge_ok(A)) {
             const int64_t nitems = A.nfull + (A.tail ? 1 : 0);
             if (A.npts > 1)  // batched points: one pass, the stage reused by every point
                 return A.g2_qcert ? launch_tma_unit<EvSum2GE<true>, true>(A, stream, sm_count)
                                   : launch_tma_unit<EvSum2GE<>, true>(A, stream, sm_count);
-            if (A.tma == 1 && A.warps == 0 && nitems >= PFB_TASK_ITEMS_PER_SM * (int64_t)sm_count)
+            if (A.task_shell && A.warps == 0)
                 return A.g2_qcert ? launch_task<EvSum2GE<true>>(A, stream, sm_count)
                                   : launch_task<EvSum2GE<>>(A, stream, sm_count);
+            if (A.tma == 1 && A.warps == 0 && nitems >= PFB_TMA1_ITEMS_PER_SM * (int64_t)sm_count)
+                return A.g2_qcert ? launch_tma_unit<EvSum2GE<true>, true>(A, stream, sm_count)
+                                  : launch_tma_unit<EvSum2GE<>, true>(A, stream, sm_count);
             return A.g2_qcert ? launch_prod<EvSum2GE<true>>(A, stream, sm_count)
                               : launch_prod<EvSum2GE<>>(A, stream, sm_count);
         }

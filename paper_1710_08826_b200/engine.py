@@ -94,7 +94,8 @@ class DeviceContext:
 
     def set_pipeline(self, mode: int) -> None:
         """Kernel structure (include/pfb200.h pfb_ctx_set_pipeline): 1 default,
-        2 / 3 alternative TMA layouts, 0 the SIMT reference-tree kernels."""
+        2 / 3 alternative TMA layouts, 4 as 1 with the C1 warp-task kernel,
+        0 the SIMT reference-tree kernels."""
         L.check(L.lib().pfb_ctx_set_pipeline(self.handle, int(mode)), "pfb_ctx_set_pipeline")
 
     def launch_count(self) -> int:

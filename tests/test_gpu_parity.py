@@ -116,9 +116,9 @@ def test_c1_random_points_and_far_outliers(pf, golden_dir):
 
 def test_c1_product_shells_bitwise(pf):
     """The C1 product evaluator (EvSum2GE) through every shell the pipeline
-    modes select -- bulk prefetch (1, 2), TMA unit ring (3), warp tasks (1,
-    from ~24M events: exercised by tests/test_gpu_scale.py) -- gives the same
-    bits; the log-domain SIMT kernel (0) within 1e-12."""
+    modes select -- bulk prefetch (1, 2), TMA unit ring (3; 1 from 24 blocks
+    per SM: tests/test_gpu_scale.py), warp tasks (4) -- gives the same bits;
+    the log-domain SIMT kernel (0) within 1e-12."""
     x, pdf, params = models.c1()
     rng = np.random.default_rng(8)
     n = 3 * 1_000_000 + 4097
@@ -127,12 +127,12 @@ def test_c1_product_shells_bitwise(pf):
     ctx = pf.device_context(0)
     got = {}
     try:
-        for mode in (1, 2, 3, 0):
+        for mode in (1, 2, 3, 4, 0):
             ctx.set_pipeline(mode)
             got[mode] = pf.nll(pdf, ds)
     finally:
         ctx.set_pipeline(1)
-    assert got[1] == got[2] == got[3]
+    assert got[1] == got[2] == got[3] == got[4]
     assert rel(got[0], got[1]) <= 1e-12
 
 
@@ -386,3 +386,25 @@ def test_c1_narrow_pure_gaussian_far_tails(pf):
     got = pf.nll(pdf, ds)
     want = O.nll(models.c1_spec(point), {"x": xs})
     assert rel(got, want) <= RTOL
+
+
+def test_c1_product_shells_bitwise_above_the_tma_threshold(pf):
+    """C1 at 20M events (above the 24 blocks per SM where pipeline 1 moves
+    the one-column SumPdf onto the TMA unit kernel): pipeline 1, bulk
+    prefetch (2) and warp tasks (4) give the same bits; the log-domain SIMT
+    kernel (0) agrees within 1e-12."""
+    x, pdf, params = models.c1()
+    rng = np.random.default_rng(12)
+    n = 20_000_000 + 333
+    xs = np.clip(np.concatenate([rng.normal(5, 0.5, n // 3), rng.exponential(3.3, n - n // 3)]), 0, 10)
+    ds = models.dataset([x], [xs])
+    ctx = pf.device_context(0)
+    got = {}
+    try:
+        for mode in (1, 2, 4, 0):
+            ctx.set_pipeline(mode)
+            got[mode] = pf.nll(pdf, ds)
+    finally:
+        ctx.set_pipeline(1)
+    assert got[1] == got[2] == got[4]
+    assert rel(got[1], got[0]) <= 1e-12
