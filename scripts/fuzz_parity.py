@@ -2,8 +2,9 @@
 polynomial leaves; sums over shared observables, products over disjoint
 ones; 1-3 observables), random parameters, random event counts (1 .. 300k,
 ragged), every pipeline mode and a random warps-per-block override -- each
-device NLL against the reference's own nll on the same events (<= 1e-10, or
-the same exception class and index); for valid cases, three perturbed
+device NLL against the reference's own nll on the same events (<= 1e-10
+relative plus n ulp-level norm differences, see the comparison; or the same
+exception class and index); for valid cases, three perturbed
 parameter points evaluated as one batch (pfb_nll_batch) must equal their
 single-point values bit for bit.
 
@@ -80,7 +81,7 @@ def main():
     P = pf.parafit
     ctx = pf.device_context(0)
     rng = np.random.default_rng(args.seed)
-    bad, n_ok, n_err, worst, n_batch = [], 0, 0, 0.0, 0
+    bad, n_ok, n_err, worst, n_batch, n_cond = [], 0, 0, 0.0, 0, 0
     t0 = time.perf_counter()
     for case in range(args.cases):
         obs = {k: P.Variable.observable(k, *OBS[k]) for k in OBS}
@@ -109,8 +110,16 @@ def main():
             if want[0] == "ok":
                 r = abs(got[1] - want[1]) / max(abs(want[1]), 1e-300) if got[0] == "ok" else math.inf
                 worst = max(worst, r)
-                if not r <= 1e-10:
+                # 1e-10 relative, plus n ulp-level norm differences: the
+                # reference's polynomial norm is np.dot (BLAS order, not
+                # correctly rounded), the device's the correctly rounded dot
+                # product, and a 1-ulp norm moves the NLL by ~n * 2^-53 -- which
+                # is more than 1e-10 relative only when the NLL cancels to ~0
+                allow = 1e-10 * abs(want[1]) + 8.0 * n * 2.0 ** -53
+                if not (got[0] == "ok" and abs(got[1] - want[1]) <= allow):
                     bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
+                elif r > 1e-10:
+                    n_cond += 1
             elif got != want:
                 bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
         # batched points (pfb_nll_batch) bitwise their single-point values
@@ -139,7 +148,8 @@ def main():
         else:
             n_err += 1
     out = {"cases": args.cases, "seed": args.seed, "ok_cases": n_ok, "error_cases": n_err,
-           "evaluations": args.cases * 5, "batched_cases": n_batch, "worst_rel": worst, "mismatches": bad[:20], "n_mismatches": len(bad),
+           "evaluations": args.cases * 5, "batched_cases": n_batch, "worst_rel": worst,
+           "within_norm_allowance_only": n_cond, "mismatches": bad[:20], "n_mismatches": len(bad),
            "wall_s": time.perf_counter() - t0}
     line = json.dumps(out)
     print(line)
