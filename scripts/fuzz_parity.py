@@ -3,8 +3,8 @@ polynomial leaves; sums over shared observables, products over disjoint
 ones; 1-3 observables), random parameters, random event counts (1 .. 300k,
 ragged), every pipeline mode and a random warps-per-block override -- each
 device NLL against the reference's own nll on the same events (<= 1e-10
-relative plus n ulp-level norm differences, see the comparison; or the same
-exception class and index); for valid cases, three perturbed
+relative plus the ~n * 2^-53 absolute rounding of an n-term sum, see the
+comparison; or the same exception class and index); for valid cases, three perturbed
 parameter points evaluated as one batch (pfb_nll_batch) must equal their
 single-point values bit for bit.
 
@@ -110,11 +110,12 @@ def main():
             if want[0] == "ok":
                 r = abs(got[1] - want[1]) / max(abs(want[1]), 1e-300) if got[0] == "ok" else math.inf
                 worst = max(worst, r)
-                # 1e-10 relative, plus n ulp-level norm differences: the
-                # reference's polynomial norm is np.dot (BLAS order, not
-                # correctly rounded), the device's the correctly rounded dot
-                # product, and a 1-ulp norm moves the NLL by ~n * 2^-53 -- which
-                # is more than 1e-10 relative only when the NLL cancels to ~0
+                # 1e-10 relative, plus the absolute rounding of a sum of n
+                # per-event terms (~n * 2^-53: product-mode units, table
+                # logarithms, and the reference's own np.dot polynomial norm,
+                # BLAS order, vs the device's correctly rounded dot product) --
+                # more than 1e-10 relative only when the NLL cancels to far
+                # below n (e.g. 0.22 over 300k events of a near-flat density)
                 allow = 1e-10 * abs(want[1]) + 8.0 * n * 2.0 ** -53
                 if not (got[0] == "ok" and abs(got[1] - want[1]) <= allow):
                     bad.append({"case": case, "mode": key, "n": n, "tree": repr(pdf), "want": want, "got": got})
@@ -149,7 +150,7 @@ def main():
             n_err += 1
     out = {"cases": args.cases, "seed": args.seed, "ok_cases": n_ok, "error_cases": n_err,
            "evaluations": args.cases * 5, "batched_cases": n_batch, "worst_rel": worst,
-           "within_norm_allowance_only": n_cond, "mismatches": bad[:20], "n_mismatches": len(bad),
+           "within_sum_rounding_allowance_only": n_cond, "mismatches": bad[:20], "n_mismatches": len(bad),
            "wall_s": time.perf_counter() - t0}
     line = json.dumps(out)
     print(line)
