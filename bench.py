@@ -645,10 +645,11 @@ def main():
         "metric": METRIC, "value": rec["value"], "unit": "events/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(config_of(cfg, head.n), evaluator=rec["evaluator"],
-                       parallelism=(f"events sharded over {world} GPUs (reference shard() bounds), one exchange of "
-                                    f"the 72-limb exact accumulator per call ({args.collective})"
-                                    if world > 1 else "one GPU, no exchange")),
+        # config: the workload only, key for key the reference arm's (same arrays)
+        "config": config_of(cfg, head.n), "evaluator": rec["evaluator"],
+        "parallelism": (f"events sharded over {world} GPUs (reference shard() bounds), one exchange of "
+                        f"the 72-limb exact accumulator per call ({args.collective})"
+                        if world > 1 else "one GPU, no exchange"),
         "nll_evals_per_s": rec["nll_evals_per_s"], "nll": rec["nll"],
         "e2e": rec["e2e"], "gpu_launches": launches, "roofline": rec["roofline"],
         "cpu_baseline": rec.get("cpu_baseline"), "parity": rec.get("parity"), "fit": rec.get("fit"),

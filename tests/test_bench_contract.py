@@ -43,3 +43,13 @@ def test_gpus_flag_spawns_ranks_without_a_launcher():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_both_arms_share_the_config():
+    """The driver compares the two arms' `config`: the workload keys only,
+    identical for the B200 arm and the reference arm (same arrays)."""
+    import bench
+
+    for cfg in ("c2", "c1", "c3"):
+        c = bench.config_of(cfg, bench.CONFIGS[cfg]["n"])
+        assert set(c) == {"workload", "n_events_per_gpu", "inputs", "l2"}
