@@ -292,8 +292,10 @@ int pfb_bin_fill(pfb_ctx* ctx, const pfb_store* store, int64_t begin, int64_t en
  * failure returns PFB_E_NONPOSITIVE_NORM / PFB_E_UNBOUNDED_OBSERVABLE with
  * err->node (callers re-evaluate that point through the reference path for
  * the reference's exception).  eval_batch: npts <= 16 points (rows of x),
- * one pass over the events where the plan allows (pfb_nll_batch); points
- * after a host norm failure are not evaluated. */
+ * one pass over the events where the plan allows (pfb_nll_batch); the
+ * points' quadrature norms are launched back to back into separate result
+ * slots and waited for once; points after a host norm failure (in
+ * sequential order) are not evaluated. */
 int pfb_objective_create(pfb_ctx* ctx, pfb_plan* plan, const pfb_store* store, int64_t begin, int64_t end,
                          int32_t nfree, const int32_t* value_src, const double* value_const,
                          const pfb_obj_node* nodes, const double* dalitz_matrix, pfb_objective** out);
